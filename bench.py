@@ -1,0 +1,400 @@
+#!/usr/bin/env python
+"""Benchmark of the XDG solver hot path on B200 (contract: see DESIGN.md).
+
+Default workload (BASELINE config 3, the config the metric's
+"block-SpMV GB/s vs HBM peak" half is quoted on): the synthetic block-MSR
+operator on 128^3 cells, p=2 (N=10), 7-point cell stencil, 5 % cut cells
+with doubled species blocks, FP64; one step = one SpMV y = M x over the
+whole operator (z-slab sharded with halo exchange when N > 1, strong
+scaling).  Also reported in the same line: the XDG solves (DOF/s per solve,
+the metric's first half) on the serialized reference hierarchies of
+BASELINE config 1 (2D 16^2 p=2) and the 8^3 p=3 sphere case.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+--impl reference times the reference's CPU path (the oracle C restatement of
+scipy csr_matvec over tocsr(), oracle/bsr_spmv.c, all host threads) on a
+bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "XDG multigrid-GMRES DOF/s per solve; block-SpMV GB/s vs HBM peak"
+NOMINAL_HBM_GBS = 8000.0
+
+
+def measured_peak():
+    for p in (os.path.join(ROOT, "MEASURED_PEAKS.json"),):
+        try:
+            d = json.load(open(p))
+            return float(d["hbm_gbs"]), "measured"
+        except Exception:  # noqa: BLE001
+            pass
+    return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled DURING the timed region (B200_PROFILING.md)
+
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:  # noqa: BLE001
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:  # noqa: BLE001
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [v.strip() for v in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"],
+                    "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_spmv_sample(n_sample: int, seconds: float, threads: int):
+    """Oracle C SpMV (restated scipy csr_matvec) on a 5 %-cut n^3 sample."""
+    from oracle import cfg3, spmv
+
+    rp, col, val, x = cfg3.build(n_sample)
+    nbr, N = len(rp) - 1, val.shape[1]
+    nnzb = len(col)
+    B = 8 * N * N * nnzb + 4 * nnzb + 4 * (nbr + 1) + 16 * nbr * N
+    spmv.bsr_spmv(rp, col, val, x, threads)  # warm
+    times = []
+    t_end = time.perf_counter() + seconds
+    while time.perf_counter() < t_end or len(times) < 3:
+        t0 = time.perf_counter()
+        spmv.bsr_spmv(rp, col, val, x, threads)
+        times.append(time.perf_counter() - t0)
+    t = statistics.median(times)
+    return dict(value=B / t / 1e9, unit="GB/s", cores=threads, kind="port",
+                sample=f"cfg3 recipe at {n_sample}^3 ({nbr} block rows, {nnzb} blocks, "
+                       f"{B / 1e9:.3f} GB/SpMV), median of {len(times)} SpMVs, "
+                       f"oracle/bsr_spmv.c on {threads} host threads",
+                seconds=t, reps=len(times))
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if world > 1 and rank != 0:
+        return
+    from oracle import spmv
+
+    threads = spmv.max_threads()
+    vals = []
+    for _ in range(args.warmup):
+        cpu_spmv_sample(args.ref_sample, 0.0, threads)
+        break
+    t0 = time.perf_counter()
+    res = cpu_spmv_sample(args.ref_sample, max(5.0, 2.0 * args.steps), threads)
+    wall = time.perf_counter() - t0
+    vals.append(res["value"])
+    line = {
+        "impl": "reference", "metric": METRIC, "value": res["value"], "unit": "GB/s",
+        "n_gpus": 0, "steps": res["reps"], "warmup": args.warmup,
+        "ms_per_step": res["seconds"] * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (SURVEY 8(d) cfg3 recipe, seed 0)",
+        "config": {"workload": f"cfg3 block-MSR SpMV, bounded sample {args.ref_sample}^3 "
+                               f"of the {args.n}^3 operator", "N": 10, "cut_fraction": 0.05},
+        "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": res["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "wall_s": wall,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+
+def time_solves(torch, budget_s: float):
+    """XDG solves on the serialized reference hierarchies: DOF/s per solve."""
+    from paper_2003_02431_b200.hierarchy import load_hierarchy
+    from paper_2003_02431_b200.solvers import SolverConfig, gmres_pmg_solve, ortho_mg_solve
+
+    out = []
+    t_start = time.perf_counter()
+    for case in ("cfg1", "sphere8p3"):
+        path = os.path.join(ROOT, "tests", "golden", f"{case}.npz")
+        if not os.path.exists(path):
+            continue
+        z = np.load(path)
+        meta = json.loads(bytes(z["meta"]).decode())
+        hier = load_hierarchy(z)
+        lv = hier.level(1)
+        for solver in ("gmres", "omg"):
+            if time.perf_counter() - t_start > budget_s:
+                break
+            cfg = SolverConfig(**meta[solver])
+            torch.cuda.synchronize()
+            if solver == "omg":
+                x, rep = ortho_mg_solve(hier, lv.rhs, None, cfg, 1)
+            else:
+                x, rep = gmres_pmg_solve(lv.matrix, lv.rhs, cfg, dim=meta["dim"])
+            ref_x = z[f"{solver}_x"]
+            rel = float(np.linalg.norm(x - ref_x) / np.linalg.norm(ref_x))
+            ref_s = meta.get(f"{solver}_seconds")
+            out.append({
+                "case": case, "solver": "omg" if solver == "omg" else "gmres-pmg",
+                "config": meta[solver], "dofs_raw": meta["dofs_raw"],
+                "dofs_agglomerated": lv.num_dofs, "iterations": rep.iterations,
+                "ref_iterations_envelope": [int(z[f"{solver}_envelope"].min()),
+                                            int(z[f"{solver}_envelope"].max())],
+                "converged": rep.converged, "solve_s": rep.time_iterations,
+                "dof_per_s": meta["dofs_raw"] / rep.time_iterations,
+                "ms_per_iteration": 1e3 * rep.time_iterations / max(rep.iterations, 1),
+                "rel_err_vs_reference": rel,
+                "reference_cpu_s_build_container": ref_s,
+                "reference_cpu_dof_per_s_build_container":
+                    (meta["dofs_raw"] / ref_s) if ref_s else None,
+            })
+    return out
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local = dist_env()
+    if world != args.gpus:
+        args.gpus = world
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    from paper_2003_02431_b200 import _native as nat
+    from paper_2003_02431_b200.device import Context
+    from paper_2003_02431_b200.distributed import DistributedSpMV, HaloPlan
+    from paper_2003_02431_b200.synthetic import cfg3_slab_device
+
+    ctx = Context.get(dev)
+    t_setup = time.perf_counter()
+    s = cfg3_slab_device(args.n, rank, world, ctx=ctx)
+    D = s["D"]
+    N = D.N
+    nloc = s["row1"] - s["row0"]
+    ghosts = np.concatenate([s["halo_lo"], s["halo_hi"]])
+    # global row partition
+    starts = torch.zeros(world + 1, dtype=torch.int64)
+    if world > 1:
+        r0 = torch.tensor([s["row0"]], dtype=torch.int64, device=dev)
+        allr = [torch.zeros_like(r0) for _ in range(world)]
+        dist.all_gather(allr, r0)
+        starts[:world] = torch.cat(allr).cpu()
+    starts[world] = s["nbr_global"]
+    halo = HaloPlan(starts.numpy(), ghosts, rank, world, N, dev)
+    op = DistributedSpMV(D, halo)
+    g = torch.Generator(device=dev).manual_seed(99 + rank)
+    x_ext = torch.randn((nloc + len(ghosts)) * N, generator=g, device=dev, dtype=torch.float64)
+    y = torch.empty(nloc * N, dtype=torch.float64, device=dev)
+    setup_s = time.perf_counter() - t_setup
+
+    # algorithmic bytes of the whole operator and of this rank
+    nnzb_g = int(D.nnzb)
+    if world > 1:
+        t = torch.tensor([D.nnzb], dtype=torch.int64, device=dev)
+        dist.all_reduce(t)
+        nnzb_g = int(t.item())
+    nbr_g = s["nbr_global"]
+    B_global = 8 * N * N * nnzb_g + 4 * nnzb_g + 4 * (nbr_g + 1) + 16 * nbr_g * N
+    B_local = D.algorithmic_bytes()
+
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        op(x_ext, y)
+    barrier()
+    # timed region: K steps; per-step kernel events for the roofline
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        start.record(stream)
+        for k in range(args.steps):
+            ev[k][0].record(stream)
+            op(x_ext, y)
+            ev[k][1].record(stream)
+        end.record(stream)
+        barrier()
+    elapsed_ms = start.elapsed_time(end)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed_ms = float(t.item())
+    ms_per_step = elapsed_ms / args.steps
+    value = B_global * args.steps / (elapsed_ms * 1e-3) / 1e9
+    # dominant kernel: the SpMV launch(es) of one step (N=1: one launch)
+    kern_ms = statistics.mean(step_ms)
+    achieved = B_local / (kern_ms * 1e-3) / 1e9
+    peak, peak_kind = measured_peak()
+    gpu_launches = args.steps * ((1 if world == 1 else 3) + (len(halo.sends) if world > 1 else 0))
+
+    # ---- e2e through the C-ABI with pinned host buffers -------------------
+    xh = torch.empty(nloc * N, dtype=torch.float64, pin_memory=True)
+    xh.copy_(x_ext[: nloc * N].cpu())
+    yh = torch.empty(nloc * N, dtype=torch.float64, pin_memory=True)
+    xd = x_ext  # device buffer the host copy lands in
+    for _ in range(2):
+        xd[: nloc * N].copy_(xh, non_blocking=True)
+        op(xd, y)
+        yh.copy_(y, non_blocking=True)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        xd[: nloc * N].copy_(xh, non_blocking=True)
+        op(xd, y)
+        yh.copy_(y, non_blocking=True)
+    e1.record(stream)
+    barrier()
+    e2e_ms = e0.elapsed_time(e1)
+    t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_ms = float(t.item())
+    e2e_val = B_global * args.steps / (e2e_ms * 1e-3) / 1e9
+
+    line = None
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (SURVEY 8(d) cfg3 recipe pattern, seed 0; "
+                                    "seeded device values of the recipe's distributions)",
+            "config": {"workload": f"BASELINE cfg3: block-MSR SpMV {args.n}^3 cells, p=2 "
+                                   f"(N=10), 5% cut, {nbr_g} block rows, {nnzb_g} blocks",
+                       "algorithmic_bytes_per_step": B_global,
+                       "l2": "inputs larger than L2 (matrix 12.4 GB >> 126 MB); no flush",
+                       "parallelism": f"z-slab x{world}, NCCL halo" if world > 1 else "1 GPU",
+                       "setup_s": setup_s},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "peak_kind": peak_kind,
+                         "frac_of_nominal_8TBs": achieved / NOMINAL_HBM_GBS,
+                         "kernel": "xdg spmv_warp_rows<10>",
+                         "kernel_ms": kern_ms, "bytes_per_launch": B_local,
+                         "traffic": None},
+            "e2e": {"value": e2e_val, "unit": "GB/s",
+                    "h2d_bytes_per_step": 8 * nloc * N, "d2h_bytes_per_step": 8 * nloc * N,
+                    "path": "pinned host x -> H2D -> xdg_bsr_spmv (C-ABI) -> D2H y"},
+            "gpu_launches": gpu_launches,
+            "clocks": clk.summary(),
+        }
+    if world == 1 and not args.no_solve:
+        try:
+            line["solve"] = time_solves(torch, args.solve_budget)
+        except Exception as exc:  # noqa: BLE001
+            line["solve_error"] = repr(exc)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            from oracle import spmv as ospmv
+
+            line["cpu_baseline"] = {k: v for k, v in cpu_spmv_sample(
+                args.ref_sample, args.cpu_seconds, ospmv.max_threads()).items()
+                if k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as exc:  # noqa: BLE001
+            line["cpu_baseline"] = {"error": repr(exc)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier(device_ids=[local])
+        dist.destroy_process_group()
+    del nat
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--n", type=int, default=128)
+    ap.add_argument("--ref-sample", type=int, default=48)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--solve-budget", type=float, default=120.0)
+    ap.add_argument("--no-solve", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,174 @@
+/*
+ * xdg_b200 — C-ABI of the B200 (sm_100a) XDG solver hot path.
+ *
+ * Drop-in boundary for the reference package `cutdg` (arXiv 2003.02431
+ * restatement, /root/reference/pkg/src/cutdg).  Every entry point takes plain
+ * device pointers and sizes, returns an int status (XDG_OK == 0) and runs on
+ * the caller's CUDA stream.  No torch types cross this boundary; the Python
+ * host layer (paper_2003_02431_b200/) binds it with ctypes.
+ *
+ * Data layout ("BSR-T"): a uniform-block sparse matrix with nbr block rows
+ * and N x N dense blocks is (row_ptr int32[nbr+1], col int32[nnzb],
+ * val f64[nnzb][N][N]) with blocks sorted by (block row, block col) -- the
+ * order BlockSparseMatrix.tocsr() uses (blockmatrix.py:98) -- and every
+ * block stored COLUMN-major: val[k*N*N + j*N + i] = block_k(i, j).
+ * xdg_blocks_transpose() converts the reference's row-major blocks.
+ * Vectors are f64, block-major (block b owns [b*N, (b+1)*N)).
+ *
+ * Reductions (dot, norms) are deterministic: per-CTA partials are summed in
+ * CTA order by the last CTA; they need a workspace of
+ * xdg_reduce_workspace_bytes() bytes, zero-initialised once by the caller.
+ */
+#ifndef XDG_B200_H_
+#define XDG_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* xdg_stream_t; /* == cudaStream_t */
+
+enum {
+  XDG_OK = 0,
+  XDG_ERR_ARG = 1,      /* -> DimensionMismatchError / InvalidConfigError */
+  XDG_ERR_CUDA = 2,     /* CUDA runtime failure                           */
+  XDG_ERR_SINGULAR = 3, /* -> SingularSystemError                         */
+  XDG_ERR_UNSUPPORTED = 4
+};
+
+/* ---- library info ------------------------------------------------------ */
+int xdg_version(void);
+const char* xdg_last_error(void);
+/* Bytes of reduction workspace the reduction entry points need. */
+int64_t xdg_reduce_workspace_bytes(void);
+
+/* ---- block layout ------------------------------------------------------ */
+/* Row-major -> column-major block storage (and back: the op is an
+ * involution on square blocks).  in and out must not alias.
+ * Replaces the cached CSR build, cutdg blockmatrix.py:91-114. */
+int xdg_blocks_transpose(int64_t nnzb, int N, const double* in, double* out,
+                         xdg_stream_t stream);
+
+/* out[i*N + q] = x[idx[i]*N + q]: packs the owned x blocks a neighbouring
+ * rank needs (multi-GPU halo send buffer). */
+int xdg_gather_blocks(int64_t nidx, int N, const int* idx, const double* x,
+                      double* out, xdg_stream_t stream);
+
+/* ---- block-sparse matrix-vector product -------------------------------- */
+/* Block rows [row_begin, row_end) of
+ *     b == NULL :  y = alpha * (M x) + beta * y   (beta == 0: y not read)
+ *     b != NULL :  y = b - M x                    (alpha, beta ignored)
+ * Each scalar row is summed over its blocks in column order, then over the
+ * block's columns in order, with separately rounded multiply and add: the
+ * summation order of scipy's csr_matvec on BlockSparseMatrix.tocsr(), so
+ * alpha=1, beta=0 reproduces cutdg BlockSparseMatrix.matvec
+ * (blockmatrix.py:119-125) bit for bit.
+ * If norm2_out != NULL, *norm2_out (device) = sum over the computed rows of
+ * y_i^2 (deterministic), using ws (xdg_reduce_workspace_bytes()).
+ * x is indexed by block column (it may be longer than M's rows: owned
+ * blocks followed by halo blocks on a multi-GPU rank). */
+int xdg_bsr_spmv(int row_begin, int row_end, int N, const int* row_ptr,
+                 const int* col, const double* val_t, const double* x,
+                 double* y, double alpha, double beta, const double* b,
+                 double* norm2_out, void* ws, xdg_stream_t stream);
+
+/* ---- vector kernels (deterministic reductions) ------------------------- */
+/* *out = sum_i x_i * y_i  (device scalar).   numpy `x @ y`,
+ * used at solvers.py:587,594,604,607,700,782,803,805,834. */
+int xdg_dot(int64_t n, const double* x, const double* y, double* out,
+            void* ws, xdg_stream_t stream);
+/* y += s * x with s = a            if a_dev == NULL
+ *                 s = a * (*a_dev) otherwise (device scalar)   */
+int xdg_axpy(int64_t n, double a, const double* a_dev, const double* x,
+             double* y, xdg_stream_t stream);
+/* y = s * x with s = a                   if a_dev == NULL and !invert
+ *                s = a * (*a_dev)        if a_dev != NULL and !invert
+ * y = a * (x / (*a_dev))                 if a_dev != NULL and invert
+ * y = x / a                              if a_dev == NULL and invert
+ * (division per element, x_i / d, like numpy `w /= norm_w`, solvers.py:601) */
+int xdg_scale(int64_t n, double a, const double* a_dev, int invert,
+              const double* x, double* y, xdg_stream_t stream);
+/* out = x + y (elementwise): RmState.current() x0 + y (solvers.py:546). */
+int xdg_add(int64_t n, const double* x, const double* y, double* out,
+            xdg_stream_t stream);
+/* rm_step's exact-image update (solvers.py:605-607), fused:
+ *   My_new = My + (*alpha_dev) * Mz ;  *rho2 = ||r0 - My_new||^2 (device). */
+int xdg_rm_update(int64_t n, const double* r0, const double* My,
+                  const double* Mz, const double* alpha_dev, double* My_new,
+                  double* rho2, void* ws, xdg_stream_t stream);
+/* r = b - y (elementwise). */
+int xdg_sub(int64_t n, const double* b, const double* y, double* r,
+            xdg_stream_t stream);
+/* y = x ./ d (elementwise), the overlap damping of schwarz_apply
+ * (solvers.py:478). */
+int xdg_div(int64_t n, const double* x, const double* d, double* y,
+            xdg_stream_t stream);
+
+/* ---- tall-skinny kernels for residual minimisation / GMRES ------------- */
+/* coeff[c] = sum_i W[c*ldw + i] * w[i], c < ncols: `W.T @ w`
+ * (solvers.py:590).  Deterministic; ws >= xdg_gemv_t_workspace_bytes. */
+int64_t xdg_gemv_t_workspace_bytes(int ncols);
+int xdg_gemv_t(int64_t L, int ncols, const double* W, int64_t ldw,
+               const double* w, double* coeff, void* ws, xdg_stream_t stream);
+/* w -= W coeff ; z -= Z coeff  (Z may be NULL): the fused update pair of
+ * the classical Gram-Schmidt pass, solvers.py:591-592. */
+int xdg_gemv_update2(int64_t L, int ncols, const double* W, const double* Z,
+                     int64_t ld, const double* coeff, double* w, double* z,
+                     xdg_stream_t stream);
+
+
+/* ---- dense LU solves (batched, variable size) --------------------------- */
+/* For s < nsys: n = dims[s]; LU + lu_off[s] is the packed row-major n x n
+ * factor of a partial-pivoting LU (A = P L U, unit L); x + vec_off[s]
+ * receives the solution of A x = b_s where b_s[i] = b[src[vec_off[s]+i]]
+ * (pivot permutation pre-composed with the gather).  One CTA per system.
+ * Replaces SuperLU solve (blockmatrix.py:224) for the low-order PMG
+ * systems (solvers.py:249-251) and the coarsest-level direct solve
+ * (solvers.py:699). */
+int xdg_lu_solve_batched(int nsys, const int64_t* lu_off, const int* dims,
+                         const int64_t* vec_off, const double* LU,
+                         const int* src, const double* b, double* x,
+                         xdg_stream_t stream);
+/* LAPACK ipiv (1-based sequential swaps) -> permutation perm with
+ * (P^T b)[i] = b[perm[i]], per system (setup). */
+int xdg_ipiv_to_perm(int nsys, const int* dims, const int64_t* vec_off,
+                     const int* ipiv, int* perm, xdg_stream_t stream);
+
+/* ---- degree-separated preconditioner / Schwarz -------------------------- */
+/* Work item w = one cell (block row) of one system; its blocks restricted
+ * to the system's cell set are wi_blk[wi_ptr[w] .. wi_ptr[w+1]) with local
+ * column index wi_lcol (sorted by column).  m = number of low modes.
+ * Setup: dense low-order matrices A_s (zero-initialised by the caller)
+ * (solvers.py:208-215). */
+int xdg_pmg_build_low(int nwork, int N, int m, const int* wi_ptr,
+                      const int* wi_blk, const int* wi_lcol, const int* wi_lrow,
+                      const int* wi_sys, const int64_t* lu_off, const int* dims,
+                      const double* val_t, double* A, xdg_stream_t stream);
+/* Setup: H[c] = M[cells[c], cells[c]](m:, m:), row-major, diag_blk[c] the
+ * block index of the diagonal block (solvers.py:232). */
+int xdg_pmg_gather_high(int ncells, int N, int m, const int* cells,
+                        const int* diag_blk, const double* val_t, double* H,
+                        xdg_stream_t stream);
+/* Apply, fused: for every work item, r = b_hi - M_II(hi, lo) x_lo over the
+ * system's blocks (solvers.py:257), x_hi = H^-1 r with the cell's pivoted
+ * column-major LU (HLU + wi_hidx*nh*nh, hperm) (solvers.py:258-262), and
+ * out[wi_out + 0..N) = [x_lo(cell), x_hi].  N - m <= 64. */
+int xdg_pmg_high(int nwork, int N, int m, const int* wi_ptr, const int* wi_blk,
+                 const int* wi_lcol, const int* wi_cell, const int* wi_lrow,
+                 const int64_t* wi_xlo, const int* wi_hidx,
+                 const int64_t* wi_out, const double* val_t, const double* HLU,
+                 const int* hperm, const double* b, const double* xlo,
+                 double* out, xdg_stream_t stream);
+/* z[bi*N+i] = (sum_e out[cpos[e] + i], e in [cptr[bi], cptr[bi+1]) in
+ * order) / damping[bi*N+i]  (damping may be NULL): the additive Schwarz
+ * sum and overlap damping of schwarz_apply (solvers.py:473-478). */
+int xdg_pmg_combine(int nbr, int N, const int* cptr, const int64_t* cpos,
+                    const double* out, const double* damping, double* z,
+                    xdg_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* XDG_B200_H_ */

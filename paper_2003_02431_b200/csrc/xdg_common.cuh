@@ -1,0 +1,113 @@
+// Shared helpers for the xdg_b200 kernels (sm_100a).
+//
+// Error model: every exported entry point returns an int status (XDG_OK = 0)
+// and records a message retrievable through xdg_last_error().  The Python
+// layer maps statuses onto the reference's exception classes
+// (cutdg/errors.py: DimensionMismatchError, SingularSystemError, ...).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include "../../include/xdg_b200.h"
+
+namespace xdg {
+
+void set_error(const char* fmt, ...);
+
+#define XDG_TRY_CUDA(expr)                                                 \
+  do {                                                                     \
+    cudaError_t _e = (expr);                                               \
+    if (_e != cudaSuccess) {                                               \
+      ::xdg::set_error("%s:%d: %s -> %s", __FILE__, __LINE__, #expr,       \
+                       cudaGetErrorString(_e));                            \
+      return XDG_ERR_CUDA;                                                 \
+    }                                                                      \
+  } while (0)
+
+#define XDG_CHECK_LAUNCH() XDG_TRY_CUDA(cudaGetLastError())
+
+#define XDG_REQUIRE(cond, code, ...)                                       \
+  do {                                                                     \
+    if (!(cond)) {                                                         \
+      ::xdg::set_error(__VA_ARGS__);                                       \
+      return (code);                                                       \
+    }                                                                      \
+  } while (0)
+
+// Number of SMs on the current device (cached per process; one device per
+// process is the deployment model).
+int sm_count();
+
+// Grid for a grid-stride kernel: enough CTAs to cover `work` threads but at
+// most `per_sm` resident CTAs on every SM (persistent-style sizing in
+// multiples of the SM count).
+inline int grid_for(int64_t work, int threads, int per_sm) {
+  int64_t need = (work + threads - 1) / threads;
+  int64_t cap = (int64_t)sm_count() * per_sm;
+  if (need < 1) need = 1;
+  return (int)(need < cap ? need : cap);
+}
+
+// ---------------------------------------------------------------------------
+// Deterministic reductions.  A CTA reduces its threads' values through a
+// fixed shuffle tree, writes one partial per CTA, and the last CTA to finish
+// (ticket counter) sums the partials in CTA order.  No floating-point
+// atomics, so results are bit-reproducible run to run.
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Sum `v` over the CTA; result valid in thread 0.  blockDim.x % 32 == 0.
+__device__ __forceinline__ double block_sum(double v, double* smem32) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) smem32[warp] = v;
+  __syncthreads();
+  const int nw = blockDim.x >> 5;
+  double r = 0.0;
+  if (warp == 0) {
+    r = lane < nw ? smem32[lane] : 0.0;
+    r = warp_sum(r);
+  }
+  __syncthreads();
+  return r;
+}
+
+// Workspace layout for the reductions: [counter(8 B)][partials...].
+// Every CTA calls this with its thread-0 value; the last CTA writes
+// out[0] = sum of partials in CTA order and re-arms the counter.
+__device__ __forceinline__ void grid_finalize(double cta_value, double* ws,
+                                              double* out) {
+  __shared__ bool am_last;
+  unsigned int* counter = reinterpret_cast<unsigned int*>(ws);
+  double* partials = ws + 1;
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = cta_value;
+    __threadfence();
+    unsigned int t = atomicAdd(counter, 1u);
+    am_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (am_last) {
+    __threadfence();
+    // fixed-order sum of the partials by warp 0, lanes striding, then a
+    // shuffle tree: deterministic for a fixed grid size.
+    double s = 0.0;
+    if (threadIdx.x < 32) {
+      for (int i = threadIdx.x; i < (int)gridDim.x; i += 32)
+        s += ((volatile double*)partials)[i];
+      s = warp_sum(s);
+      if (threadIdx.x == 0) {
+        out[0] = s;
+        *counter = 0u;
+      }
+    }
+  }
+}
+
+}  // namespace xdg

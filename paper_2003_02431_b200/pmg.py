@@ -1,0 +1,231 @@
+"""Device plan for the degree-separated block preconditioner over a batch of
+cell sets (cutdg solvers.py:183-305) -- one set for `pmg_apply`/GMRES, all
+extended Schwarz blocks of a partition for `schwarz_apply`
+(solvers.py:460-478).
+
+Setup (counted in the solve time, like the reference's lazy factorisations,
+solvers.py:300-305):
+  * per set S: restricted block lists (extract_block_submatrix semantics),
+    dense low-order matrix A_S (modes < m of every block in S x S) built on
+    the device, pivoted LU;
+  * per cell: pivoted LU of the high-order diagonal block H_c, shared by
+    every set containing the cell (H_c depends only on M[c, c]).
+Apply (3 launches, all sets at once):
+  xdg_lu_solve_batched  -> x_lo of every set (one CTA per set)
+  xdg_pmg_high          -> residual on the high rows + per-cell H_c solves
+  xdg_pmg_combine       -> ordered sum over sets / damping (or scatter)
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .direct import ipiv_to_perm, lu_factor_dense
+from .errors import SingularSystemError
+
+F64 = torch.float64
+I32 = torch.int32
+I64 = torch.int64
+
+
+def _ranges(starts: np.ndarray, ends: np.ndarray) -> np.ndarray:
+    """Concatenation of arange(s, e) for each pair (vectorised)."""
+    lens = ends - starts
+    if lens.sum() == 0:
+        return np.zeros(0, np.int64)
+    offs = np.repeat(starts - np.concatenate([[0], np.cumsum(lens)[:-1]]), lens)
+    return np.arange(lens.sum(), dtype=np.int64) + offs
+
+
+class PmgPlan:
+    def __init__(self, D, cell_sets, m: int, damping: torch.Tensor | None = None,
+                 combine: bool = True):
+        """D: DeviceBSR (square, uniform N); cell_sets: list of sorted int
+        arrays; m: number of low modes (1 <= m <= N)."""
+        ctx = D.ctx
+        self.ctx, self.D, self.m = ctx, D, int(m)
+        N = D.N
+        self.N = N
+        dev = ctx.device
+        rp = D.row_ptr.cpu().numpy().astype(np.int64)
+        col = D.col.cpu().numpy().astype(np.int64)
+        nbr = D.nbr
+        self.nsys = len(cell_sets)
+        sets = [np.asarray(S, np.int64) for S in cell_sets]
+        self.sets = sets
+
+        # ---- restricted block lists per work item (set, local row) -------
+        loc = np.full(nbr, -1, np.int64)
+        wi_cnt, wi_blk, wi_lcol, wi_cell, wi_lrow, wi_sys = [], [], [], [], [], []
+        for s, S in enumerate(sets):
+            loc[S] = np.arange(len(S))
+            ks = _ranges(rp[S], rp[S + 1])
+            lc = loc[col[ks]]
+            keep = lc >= 0
+            rows = np.repeat(np.arange(len(S)), rp[S + 1] - rp[S])
+            wi_cnt.append(np.bincount(rows[keep], minlength=len(S)))
+            wi_blk.append(ks[keep])
+            wi_lcol.append(lc[keep])
+            wi_cell.append(S)
+            wi_lrow.append(np.arange(len(S)))
+            wi_sys.append(np.full(len(S), s))
+            loc[S] = -1
+        cat = (lambda xs: np.concatenate(xs) if xs else np.zeros(0, np.int64))
+        cnt = cat(wi_cnt)
+        self.nwork = len(cnt)
+        wi_ptr = np.zeros(self.nwork + 1, np.int64)
+        np.cumsum(cnt, out=wi_ptr[1:])
+        wcell, wlrow, wsys = cat(wi_cell), cat(wi_lrow), cat(wi_sys)
+
+        sizes = np.array([len(S) for S in sets], np.int64)
+        dims = sizes * self.m
+        vec_off = np.zeros(self.nsys + 1, np.int64)
+        np.cumsum(dims, out=vec_off[1:])
+        lu_off = np.zeros(self.nsys + 1, np.int64)
+        np.cumsum(dims * dims, out=lu_off[1:])
+        out_off = np.zeros(self.nsys + 1, np.int64)
+        np.cumsum(sizes * N, out=out_off[1:])
+
+        def up(a, dt):
+            return torch.from_numpy(np.ascontiguousarray(a)).to(dev, dt)
+
+        self.wi_ptr = up(wi_ptr, I32)
+        self.wi_blk = up(cat(wi_blk), I32)
+        self.wi_lcol = up(cat(wi_lcol), I32)
+        self.wi_cell = up(wcell, I32)
+        self.wi_lrow = up(wlrow, I32)
+        self.wi_sys = up(wsys, I32)
+        self.dims = up(dims, I32)
+        self.vec_off = up(vec_off[:-1], I64)
+        self.lu_off = up(lu_off[:-1], I64)
+        self.xlo = torch.zeros(int(vec_off[-1]), dtype=F64, device=dev)
+
+        # ---- low-order dense factors (solvers.py:208-221) ----------------
+        A = torch.zeros(int(lu_off[-1]), dtype=F64, device=dev)
+        nat.check(ctx.lib.xdg_pmg_build_low(
+            self.nwork, N, self.m, self.wi_ptr.data_ptr(),
+            self.wi_blk.data_ptr(), self.wi_lcol.data_ptr(),
+            self.wi_lrow.data_ptr(), self.wi_sys.data_ptr(),
+            self.lu_off.data_ptr(), self.dims.data_ptr(), D.val_t.data_ptr(),
+            A.data_ptr(), ctx.stream), "pmg_build_low")
+        piv = torch.zeros(int(vec_off[-1]), dtype=I32, device=dev)
+        # factor systems of equal size as one batch
+        for n in np.unique(dims):
+            idx = np.flatnonzero(dims == n)
+            n = int(n)
+            if n == 0:
+                continue
+            views = torch.stack([A[lu_off[s]:lu_off[s] + n * n] for s in idx]
+                                ).view(len(idx), n, n)
+            try:
+                LU, pv = lu_factor_dense(views, "low-order system")
+            except SingularSystemError as exc:
+                cells = tuple(int(c) for c in sets[idx[0]][:8])
+                raise SingularSystemError(
+                    f"low-order system on cells {cells}... is singular") from exc
+            for q, s in enumerate(idx):
+                A[lu_off[s]:lu_off[s] + n * n] = LU[q].reshape(-1)
+                piv[vec_off[s]:vec_off[s] + n] = pv[q].to(I32)
+        self.LU = A
+        perm = ipiv_to_perm(ctx, piv, self.dims, self.vec_off).long()
+        # src = global DOF of local low unknown perm[i]:  cell*N + mode
+        gidx = torch.from_numpy(
+            np.concatenate([np.repeat(S * N, self.m) + np.tile(np.arange(self.m), len(S))
+                            for S in sets]) if sets else np.zeros(0, np.int64)).to(dev)
+        base = torch.from_numpy(np.repeat(vec_off[:-1], dims)).to(dev)
+        # perm is local to each system: global position = base + local index
+        self.src = gidx[base + perm].to(I32) if perm.numel() else perm.to(I32)
+
+        # ---- high-order per-cell factors (solvers.py:225-243) ------------
+        self.has_high = self.m < N
+        if self.has_high:
+            nh = N - self.m
+            ucells = np.unique(wcell) if len(wcell) else np.zeros(0, np.int64)
+            rows_of_k = np.repeat(np.arange(nbr), rp[1:] - rp[:-1])
+            diag_k = np.full(nbr, -1, np.int64)
+            isdiag = col == rows_of_k
+            diag_k[rows_of_k[isdiag]] = np.flatnonzero(isdiag)
+            missing = ucells[diag_k[ucells] < 0]
+            if len(missing):
+                raise SingularSystemError(f"cell {int(missing[0])} has no diagonal block")
+            H = torch.empty(len(ucells) * nh * nh, dtype=F64, device=dev)
+            nat.check(ctx.lib.xdg_pmg_gather_high(
+                len(ucells), N, self.m, up(ucells, I32).data_ptr(),
+                up(diag_k[ucells], I32).data_ptr(), D.val_t.data_ptr(),
+                H.data_ptr(), ctx.stream), "pmg_gather_high")
+            LUh, pvh, info = torch.linalg.lu_factor_ex(H.view(len(ucells), nh, nh))
+            dg = torch.diagonal(LUh, dim1=-2, dim2=-1)
+            bad = (~torch.isfinite(LUh).flatten(1).all(1)) | (dg == 0).any(1)
+            if bool(bad.any()):
+                c = int(ucells[int(torch.nonzero(bad)[0])])
+                raise SingularSystemError(f"high-order block of cell {c} is singular")
+            self.HLU = torch.empty_like(H)
+            nat.check(ctx.lib.xdg_blocks_transpose(
+                len(ucells), nh, LUh.contiguous().data_ptr(), self.HLU.data_ptr(),
+                ctx.stream), "blocks_transpose(H)")
+            hdims = torch.full((len(ucells),), nh, dtype=I32, device=dev)
+            hoff = torch.arange(len(ucells), dtype=I64, device=dev) * nh
+            self.hperm = ipiv_to_perm(ctx, pvh.to(I32).contiguous(), hdims, hoff)
+            hidx = np.full(nbr, -1, np.int64)
+            hidx[ucells] = np.arange(len(ucells))
+            self.wi_hidx = up(hidx[wcell], I32)
+            self.wi_xlo = up(vec_off[:-1][wsys], I64)
+
+        # ---- output placement ---------------------------------------------
+        # direct mode: one set equal to all rows in order -> write z in place
+        self.direct = (not combine and self.nsys == 1 and len(sets[0]) == nbr
+                       and np.array_equal(sets[0], np.arange(nbr)))
+        if self.direct:
+            self.wi_out = up(wcell * N, I64) if self.has_high else None
+            self.out = None
+        else:
+            self.wi_out = up(out_off[:-1][wsys] + wlrow * N, I64)
+            # out buffer: the low-only case reuses xlo (same local layout)
+            self.out = (torch.empty(int(out_off[-1]), dtype=F64, device=dev)
+                        if self.has_high else self.xlo)
+            order = np.lexsort((wsys, wcell))  # by cell, then set index
+            cptr = np.zeros(nbr + 1, np.int64)
+            np.cumsum(np.bincount(wcell, minlength=nbr), out=cptr[1:])
+            cpos = (out_off[:-1][wsys] + wlrow * N)[order]
+            self.cptr = up(cptr, I32)
+            self.cpos = up(cpos, I64)
+        self.damping = damping
+
+    # ------------------------------------------------------------------
+    def apply(self, b: torch.Tensor, z: torch.Tensor) -> torch.Tensor:
+        """z = sum_S PMG_S(b) ./ damping   (or the single-set PMG)."""
+        ctx, D, lib, st = self.ctx, self.D, self.ctx.lib, self.ctx.stream
+        xlo = z if (self.direct and not self.has_high) else self.xlo
+        nat.check(lib.xdg_lu_solve_batched(
+            self.nsys, self.lu_off.data_ptr(), self.dims.data_ptr(),
+            self.vec_off.data_ptr(), self.LU.data_ptr(), self.src.data_ptr(),
+            b.data_ptr(), xlo.data_ptr(), st), "lu_solve_batched")
+        if self.has_high:
+            out = z if self.direct else self.out
+            nat.check(lib.xdg_pmg_high(
+                self.nwork, self.N, self.m, self.wi_ptr.data_ptr(),
+                self.wi_blk.data_ptr(), self.wi_lcol.data_ptr(),
+                self.wi_cell.data_ptr(), self.wi_lrow.data_ptr(),
+                self.wi_xlo.data_ptr(), self.wi_hidx.data_ptr(),
+                self.wi_out.data_ptr(), D.val_t.data_ptr(), self.HLU.data_ptr(),
+                self.hperm.data_ptr(), b.data_ptr(), xlo.data_ptr(),
+                out.data_ptr(), st), "pmg_high")
+        if not self.direct:
+            nat.check(lib.xdg_pmg_combine(
+                D.nbr, self.N, self.cptr.data_ptr(), self.cpos.data_ptr(),
+                self.out.data_ptr(),
+                None if self.damping is None else self.damping.data_ptr(),
+                z.data_ptr(), st), "pmg_combine")
+        return z
+
+    def algorithmic_bytes(self) -> int:
+        """Bytes one apply must move (SURVEY 8(d) PMG apply)."""
+        N, m = self.N, self.m
+        lo = int(self.dims.double().pow(2).sum().item()) * 8
+        hi = 0
+        if self.has_high:
+            nh = N - m
+            hi = self.nwork * nh * nh * 8 + int(self.wi_blk.numel()) * (nh * m * 8 + 4)
+        vec = self.nwork * N * 8 * 3
+        return lo + hi + vec

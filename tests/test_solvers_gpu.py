@@ -1,0 +1,106 @@
+"""Residual minimization, OMG and GMRES-PMG on the device vs the reference
+(golden fixtures): parity protocol items 2-4."""
+import json
+
+import numpy as np
+import pytest
+
+from conftest import golden_path
+from paper_2003_02431_b200.hierarchy import load_hierarchy
+from paper_2003_02431_b200.solvers import (
+    RmState,
+    SolverConfig,
+    gmres_pmg_solve,
+    ortho_mg_solve,
+    rm_step,
+)
+
+pytestmark = pytest.mark.gpu
+SOL_TOL = 1e-8      # north_star: final solution within 1e-8 relative L2
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+def load(case):
+    z = np.load(golden_path(case))
+    return z, json.loads(bytes(z["meta"]).decode()), load_hierarchy(z)
+
+
+@pytest.mark.parametrize("case", ["bench4", "cfg1"])
+def test_rm_step_sequence_matches_reference(case):
+    z, meta, hier = load(case)
+    lv = hier.level(1)
+    b = lv.rhs
+    state = RmState(np.zeros_like(b), b, 3)
+    for i, cand in enumerate(z["rm_cands"]):
+        x, r, state = rm_step(state, cand, lv.matrix)
+        info = [state.ncols, int(state.last_dependent), state.dependent_count,
+                state.rejected_count, state.restart_count]
+        assert info == list(z["rm_info"][i]), (i, info, z["rm_info"][i])
+        assert rel(x, z["rm_x"][i]) <= 1e-10, (i, rel(x, z["rm_x"][i]))
+        assert rel(r, z["rm_r"][i]) <= 1e-10, (i, rel(r, z["rm_r"][i]))
+
+
+@pytest.mark.parametrize("case", ["bench4", "cfg1"])
+def test_omg_matches_reference(case):
+    z, meta, hier = load(case)
+    lv = hier.level(1)
+    cfg = SolverConfig(**meta["omg"])
+    x, rep = ortho_mg_solve(hier, lv.rhs, None, cfg, 1)
+    assert rep.converged
+    assert rel(x, z["omg_x"]) <= SOL_TOL
+    assert rel(x, z["L1_direct_rhs"]) <= SOL_TOL
+    env = z["omg_envelope"]
+    assert env.min() - 1 <= rep.iterations <= env.max() + 1, (rep.iterations, env)
+    h = rep.residual_history
+    assert len(h) == rep.iterations + 1
+    assert all(b <= a * (1 + 1e-12) for a, b in zip(h, h[1:]))
+    assert rep.dofs == lv.num_dofs
+
+
+@pytest.mark.parametrize("case", ["bench4", "cfg1"])
+def test_gmres_matches_reference(case):
+    z, meta, hier = load(case)
+    lv = hier.level(1)
+    cfg = SolverConfig(**meta["gmres"])
+    x, rep = gmres_pmg_solve(lv.matrix, lv.rhs, cfg, dim=meta["dim"])
+    assert rep.converged
+    assert rel(x, z["gmres_x"]) <= SOL_TOL
+    assert rel(x, z["L1_direct_rhs"]) <= SOL_TOL
+    env = z["gmres_envelope"]
+    assert env.min() - 1 <= rep.iterations <= env.max() + 1, (rep.iterations, env)
+    assert rep.residual_history[-1] == rep.final_residual
+
+
+def test_omg_coarsest_is_direct_and_nonconvergence_reported():
+    z, meta, hier = load("bench4")
+    lv = hier.level(1)
+    x, rep = ortho_mg_solve(hier, lv.rhs, None, SolverConfig(max_iterations=3, k_lo=1), 1)
+    assert not rep.converged and rep.iterations == 3
+    lc = hier.level(hier.num_levels)
+    xc, repc = ortho_mg_solve(hier, lc.rhs, None, SolverConfig(), hier.num_levels)
+    assert repc.iterations == 0 and repc.converged
+
+
+def test_omg_respects_initial_guess():
+    z, meta, hier = load("bench4")
+    lv = hier.level(1)
+    xd = z["L1_direct_rhs"]
+    x, rep = ortho_mg_solve(hier, lv.rhs, xd.copy(),
+                            SolverConfig(max_iterations=5, k_lo=1), 1)
+    assert rep.converged and rep.iterations == 0 and np.allclose(x, xd)
+
+
+def test_direct_factorization_matches_reference():
+    from paper_2003_02431_b200.blockmatrix import direct_factor
+
+    for case in ("bench4", "cfg1"):
+        z, meta, hier = load(case)
+        for lam in range(1, hier.num_levels + 1):
+            lv = hier.level(lam)
+            F = direct_factor(lv.matrix)
+            x = F.apply(lv.rhs)
+            assert rel(x, z[f"L{lam}_direct_rhs"]) <= 1e-9
+            assert F.factor_count == 1
