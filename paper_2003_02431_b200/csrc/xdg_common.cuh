@@ -50,6 +50,36 @@ inline int grid_for(int64_t work, int threads, int per_sm) {
   return (int)(need < cap ? need : cap);
 }
 
+// Grid for a grid-stride kernel sized to exactly one resident wave:
+// SMs x (CTAs of this kernel that fit on one SM), capped by the work.  A
+// grid larger than the resident capacity leaves a partial second wave whose
+// CTAs carry a full share of the grid-stride work (tail effect).
+template <typename Kernel>
+int resident_grid(Kernel kernel, int threads, size_t smem, int64_t work) {
+  static thread_local const void* keys[64];
+  static thread_local int vals[64];
+  static thread_local int n = 0;
+  const void* key = reinterpret_cast<const void*>(kernel);
+  int per_sm = 0;
+  for (int i = 0; i < n; ++i)
+    if (keys[i] == key) per_sm = vals[i];
+  if (per_sm == 0) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads,
+                                                      smem) != cudaSuccess ||
+        per_sm < 1)
+      per_sm = 1;
+    if (n < 64) {
+      keys[n] = key;
+      vals[n] = per_sm;
+      ++n;
+    }
+  }
+  int64_t need = (work + threads - 1) / threads;
+  int64_t cap = (int64_t)sm_count() * per_sm;
+  if (need < 1) need = 1;
+  return (int)(need < cap ? need : cap);
+}
+
 // ---------------------------------------------------------------------------
 // Deterministic reductions.  A CTA reduces its threads' values through a
 // fixed shuffle tree, writes one partial per CTA, and the last CTA to finish

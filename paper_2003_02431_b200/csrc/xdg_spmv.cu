@@ -155,7 +155,8 @@ cudaError_t launch_warp(int rb, int re, const int* rp, const int* col,
                         double* ws, cudaStream_t s) {
   constexpr int RPW = 32 / N;
   const int64_t warps = ((int64_t)(re - rb) + RPW - 1) / RPW;
-  const int grid = grid_for(warps * 32, kThreads, 8);
+  const int grid = resident_grid(spmv_warp_rows<N, MODE, NORM>, kThreads, 0,
+                                 warps * 32);
   spmv_warp_rows<N, MODE, NORM>
       <<<grid, kThreads, 0, s>>>(rb, re, rp, col, val, x, y, a, bt, b, nrm, ws);
   return cudaGetLastError();
@@ -166,7 +167,8 @@ cudaError_t launch_flat(int rb, int re, int N, const int* rp, const int* col,
                         const double* val, const double* x, double* y,
                         double a, double bt, const double* b, double* nrm,
                         double* ws, cudaStream_t s) {
-  const int grid = grid_for((int64_t)(re - rb) * N, kThreads, 8);
+  const int grid = resident_grid(spmv_flat<NT, MODE, NORM>, kThreads, 0,
+                                 (int64_t)(re - rb) * N);
   spmv_flat<NT, MODE, NORM><<<grid, kThreads, 0, s>>>(rb, re, N, rp, col, val,
                                                       x, y, a, bt, b, nrm, ws);
   return cudaGetLastError();
