@@ -90,41 +90,58 @@ def slab_cells(n: int, rank: int, world: int) -> np.ndarray:
     return np.arange(z0 * n * n, z1 * n * n, dtype=np.int64)
 
 
-def cfg3_slab_device(n: int, rank: int = 0, world: int = 1, seed: int = 0,
-                     N: int = 10, ctx=None, value_seed: int = 1234):
-    """Local operator of one z-slab, built in HBM.
-
-    Returns dict(D=DeviceBSR over local rows with columns renumbered to
-    [owned blocks | halo blocks], row0/row1 = global block-row range,
-    halo_lo/halo_hi = global block rows of the ghost planes (below/above),
-    L_global, nbr_global, nnzb_global).
-    """
-    from .device import Context, DeviceBSR
-
-    ctx = ctx or Context.get()
-    dev = ctx.device
-    cut = cut_mask(n, seed)
+def cfg3_slab_host(n: int, rank: int = 0, world: int = 1, seed: int = 0,
+                   cut: np.ndarray | None = None) -> dict:
+    """Host pattern of one z-slab: local row_ptr, local columns renumbered
+    [owned | ghosts (sorted global ids)], the slab's global block-row range,
+    the ghost ids and the global block indices of the local blocks (the
+    local blocks keep the global (row, col) storage order, so per-row sums
+    run in the reference's order)."""
+    if cut is None:
+        cut = cut_mask(n, seed)
     first = block_rows_of(cut)
     cells = slab_cells(n, rank, world)
     rows, cols, is_diag, _, _ = cfg3_pattern(n, seed, cells=cells, cut=cut)
     row0 = int(first[cells[0]]) if len(cells) else 0
     row1 = int(first[cells[-1] + 1]) if len(cells) else 0
     nloc = row1 - row0
-    # halo: global block rows of the neighbouring z planes that appear as cols
-    ghost = np.unique(cols[(cols < row0) | (cols >= row1)])
-    lo = ghost[ghost < row0]
-    hi = ghost[ghost >= row1]
-    # local column numbering: owned [0, nloc), ghosts after (lo then hi)
-    gmap_keys = np.concatenate([lo, hi])
-    lcol = np.where((cols >= row0) & (cols < row1), cols - row0, -1)
-    gpos = np.searchsorted(gmap_keys, cols[lcol < 0])
-    lcol[lcol < 0] = nloc + gpos
-    lrow = rows - row0
+    ghosts = np.unique(cols[(cols < row0) | (cols >= row1)])
+    owned = (cols >= row0) & (cols < row1)
+    lcol = np.where(owned, cols - row0, 0)
+    lcol[~owned] = nloc + np.searchsorted(ghosts, cols[~owned])
     rp = np.zeros(nloc + 1, np.int64)
-    np.cumsum(np.bincount(lrow, minlength=nloc), out=rp[1:])
-    nnzb = len(rows)
-    # values on the device, generated directly column-major (the generator
-    # fills the block; the diagonal A^T A + 10 I is symmetric anyway)
+    np.cumsum(np.bincount(rows - row0, minlength=nloc), out=rp[1:])
+    # global block index of every local block (global storage is sorted by
+    # (row, col) too, and the slab's rows are contiguous)
+    nnz_before = 0
+    if row0 > 0:
+        r_all, _, _, _, _ = cfg3_pattern(n, seed, cells=np.arange(cells[0]), cut=cut) \
+            if cells[0] > 0 else (np.zeros(0), None, None, None, None)
+        nnz_before = len(r_all)
+    ks = nnz_before + np.arange(len(rows), dtype=np.int64)
+    return dict(row_ptr=rp, col=lcol, is_diag=is_diag, row0=row0, row1=row1,
+                ghosts=ghosts, halo_lo=ghosts[ghosts < row0],
+                halo_hi=ghosts[ghosts >= row1], global_blocks=ks,
+                nbr_global=int(first[-1]), cut=cut, first=first)
+
+
+def cfg3_slab_device(n: int, rank: int = 0, world: int = 1, seed: int = 0,
+                     N: int = 10, ctx=None, value_seed: int = 1234):
+    """Local operator of one z-slab, built in HBM.
+
+    Returns the cfg3_slab_host dict plus D = DeviceBSR over the local rows
+    (columns [owned blocks | halo blocks]) and L_global.  Values are seeded
+    device random numbers with the recipe's distributions (diagonal
+    A^T A + 10 I, A ~ N(0,1); off-diagonal 0.1 N(0,1)).
+    """
+    from .device import Context, DeviceBSR
+
+    ctx = ctx or Context.get()
+    dev = ctx.device
+    h = cfg3_slab_host(n, rank, world, seed)
+    rp, lcol, is_diag = h["row_ptr"], h["col"], h["is_diag"]
+    nloc = h["row1"] - h["row0"]
+    nnzb = len(lcol)
     g = torch.Generator(device=dev)
     g.manual_seed(value_seed + rank)
     val = torch.empty(nnzb, N, N, dtype=torch.float64, device=dev)
@@ -140,8 +157,9 @@ def cfg3_slab_device(n: int, rank: int = 0, world: int = 1, seed: int = 0,
         idx = diag_idx[s:s + chunk]
         A = torch.randn(len(idx), N, N, generator=g, device=dev, dtype=torch.float64)
         val[idx] = torch.bmm(A.transpose(1, 2), A) + eye
-    D = DeviceBSR.from_arrays(rp, lcol, val, N, nloc + len(gmap_keys), ctx,
-                              val_is_colmajor=True)
-    return dict(D=D, row0=row0, row1=row1, halo_lo=lo, halo_hi=hi,
-                L_global=int(first[-1]) * N, nbr_global=int(first[-1]),
-                cut=cut, first=first)
+    # random blocks are layout-agnostic and A^T A + 10 I is symmetric, so the
+    # values are written directly as column-major blocks
+    h["D"] = DeviceBSR.from_arrays(rp, lcol, val, N, nloc + len(h["ghosts"]), ctx,
+                                   val_is_colmajor=True)
+    h["L_global"] = h["nbr_global"] * N
+    return h

@@ -113,7 +113,7 @@ CASES = {
                  rm_max_columns=800, num_levels=3),
         gmres=dict(tolerance=1e-8, max_iterations=3000, k_lo=2,
                    gmres_restart=50),
-        envelope=0, schwarz_targets=(2000,),
+        envelope=5, schwarz_targets=(2000, 400),
     ),
 }
 
