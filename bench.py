@@ -199,6 +199,11 @@ def time_solves(torch, budget_s: float):
             ref_x = z[f"{solver}_x"]
             rel = float(np.linalg.norm(x - ref_x) / np.linalg.norm(ref_x))
             ref_s = meta.get(f"{solver}_seconds")
+            cpu_here = None
+            if case == "cfg1":  # bounded: ~10 s of CPU per solver
+                from oracle import solvers_np
+
+                _, cpu_it, cpu_here = solvers_np.timed_solve(z, meta, solver)
             out.append({
                 "case": case, "solver": "omg" if solver == "omg" else "gmres-pmg",
                 "config": meta[solver], "dofs_raw": meta["dofs_raw"],
@@ -210,6 +215,10 @@ def time_solves(torch, budget_s: float):
                 "ms_per_iteration": 1e3 * rep.time_iterations / max(rep.iterations, 1),
                 "rel_err_vs_reference": rel,
                 "reference_cpu_s_build_container": ref_s,
+                "cpu_oracle_s_this_host": cpu_here,
+                "cpu_oracle_dof_per_s_this_host":
+                    (meta["dofs_raw"] / cpu_here) if cpu_here else None,
+                "cpu_oracle_cores": os.cpu_count(),
                 "reference_cpu_dof_per_s_build_container":
                     (meta["dofs_raw"] / ref_s) if ref_s else None,
             })

@@ -52,3 +52,56 @@ def test_cfg3_full_size_counts():
     from paper_2003_02431_b200.synthetic import cfg3_counts
 
     assert cfg3_counts(64) == (275251, 1853683)
+
+
+# ---- solver restatement (oracle/solvers_np.py) vs the reference ----------
+import json  # noqa: E402
+
+from oracle import solvers_np as so  # noqa: E402
+from threadpoolctl import threadpool_limits  # noqa: E402
+
+
+def _fixture(case):
+    z = np.load(golden_path(case))
+    return z, json.loads(bytes(z["meta"]).decode())
+
+
+@pytest.mark.parametrize("case", ["bench4", "cfg1", "sphere8p3"])
+def test_oracle_pmg_schwarz_rm_bitexact(case):
+    z, meta = _fixture(case)
+    h = so.hierarchy_from_npz(z, meta["dim"])
+    for lam, lv in enumerate(h.levels, start=1):
+        x = z[f"L{lam}_x"]
+        nb = len(lv["rp"]) - 1
+        for klo in range(3):
+            key = f"L{lam}_pmg_klo{klo}"
+            if key in z:
+                F = so.PmgFactors(lv["rp"], lv["col"], lv["val"], np.arange(nb),
+                                  so.modes_low(klo, meta["dim"], lv["N"]))
+                assert np.array_equal(F.apply(x), z[key]), key
+        for key in z.files:
+            if key.startswith(f"L{lam}_T") and "_schwarz_klo" in key:
+                tgt = int(key[len(f"L{lam}_T"):].split("_")[0])
+                klo = int(key.rsplit("klo", 1)[1])
+                ext, damp = so.schwarz_blocks(lv["adjacency"], lv["N"], max(tgt, lv["N"]))
+                m = so.modes_low(klo, meta["dim"], lv["N"])
+                facs = [so.PmgFactors(lv["rp"], lv["col"], lv["val"], e, m) for e in ext]
+                assert np.array_equal(so.schwarz_apply(facs, damp, x), z[key]), key
+    lv = h.levels[0]
+    st = so.Rm(np.zeros(lv["M"].shape[0]), np.asarray(z["L1_rhs"]), 3)
+    # the fixtures were generated with one BLAS thread (threaded dgemv
+    # changes the summation order of W.T @ w)
+    with threadpool_limits(1):
+        for i, c in enumerate(z["rm_cands"]):
+            xx, rr = st.step(c, lv["M"])
+            assert np.array_equal(xx, z["rm_x"][i]) and np.array_equal(rr, z["rm_r"][i])
+
+
+@pytest.mark.parametrize("case", ["bench4", "cfg1"])
+@pytest.mark.parametrize("solver", ["gmres", "omg"])
+def test_oracle_solves_reproduce_reference(case, solver):
+    z, meta = _fixture(case)
+    with threadpool_limits(1):
+        x, it, _ = so.timed_solve(z, meta, solver)
+    assert it == int(z[f"{solver}_iters"])
+    assert np.array_equal(x, z[f"{solver}_x"])
