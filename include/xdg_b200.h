@@ -131,6 +131,13 @@ int xdg_lu_solve_batched(int nsys, const int64_t* lu_off, const int* dims,
                          const int64_t* vec_off, const double* LU,
                          const int* src, const double* b, double* x,
                          xdg_stream_t stream);
+/* One large system: x = U^-1 L^-1 (b[src[i]])_i with one CTA per 64-row
+ * panel chained through counters (4 ints of device scratch, zeroed by the
+ * call).  Linv / Uinv: inverses of the 64x64 diagonal blocks of L (unit) and
+ * U, (ceil(n/64), 64, 64) row-major, identity-padded past n.  Deterministic. */
+int xdg_lu_solve_panels(int n, const double* LU, const double* Linv,
+                        const double* Uinv, const int* src, const double* b,
+                        double* x, int* counters, xdg_stream_t stream);
 /* LAPACK ipiv (1-based sequential swaps) -> permutation perm with
  * (P^T b)[i] = b[perm[i]], per system (setup). */
 int xdg_ipiv_to_perm(int nsys, const int* dims, const int64_t* vec_off,

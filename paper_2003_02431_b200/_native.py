@@ -45,6 +45,7 @@ SIGNATURES = {
                                 _vp]),
     "xdg_lu_solve_batched": (_i32, [_i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                     _vp]),
+    "xdg_lu_solve_panels": (_i32, [_i32] + [_vp] * 8),
     "xdg_ipiv_to_perm": (_i32, [_i32, _vp, _vp, _vp, _vp, _vp]),
     "xdg_pmg_build_low": (_i32, [_i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp,
                                  _vp, _vp, _vp, _vp, _vp]),

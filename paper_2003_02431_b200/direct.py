@@ -68,6 +68,44 @@ def dense_from_device_bsr(D) -> torch.Tensor:
     return A.view(n, n)
 
 
+PANEL = 64          # rows per panel of xdg_lu_solve_panels
+PANEL_MIN_N = 2048  # systems at least this large use the multi-CTA solve
+
+
+class PanelFactor:
+    """Extra setup for the multi-CTA solve of one large factored system:
+    inverses of the 64x64 diagonal blocks of L (unit lower) and U."""
+
+    def __init__(self, LU: torch.Tensor, ctx):
+        n = LU.shape[0]
+        self.n, self.ctx = n, ctx
+        npan = (n + PANEL - 1) // PANEL
+        pad = npan * PANEL - n
+        dev = LU.device
+        eye = torch.eye(PANEL, dtype=F64, device=dev)
+        Lb = torch.empty(npan, PANEL, PANEL, dtype=F64, device=dev)
+        Ub = torch.empty_like(Lb)
+        for p in range(npan):
+            r0, r1 = p * PANEL, min((p + 1) * PANEL, n)
+            blk = eye.clone()
+            blk[: r1 - r0, : r1 - r0] = LU[r0:r1, r0:r1]
+            Lb[p] = torch.tril(blk, -1) + eye
+            Ub[p] = torch.triu(blk)
+            if r1 - r0 < PANEL:
+                Ub[p, r1 - r0:, r1 - r0:] = eye[: pad, : pad]
+        self.Linv = torch.linalg.solve_triangular(
+            Lb, eye.expand_as(Lb), upper=False, unitriangular=True).contiguous()
+        self.Uinv = torch.linalg.solve_triangular(
+            Ub, eye.expand_as(Ub), upper=True).contiguous()
+        self.counters = torch.zeros(4, dtype=I32, device=dev)
+
+    def solve(self, LU_ptr: int, src_ptr: int, b: torch.Tensor, x_ptr: int):
+        nat.check(self.ctx.lib.xdg_lu_solve_panels(
+            self.n, LU_ptr, self.Linv.data_ptr(), self.Uinv.data_ptr(), src_ptr,
+            b.data_ptr(), x_ptr, self.counters.data_ptr(), self.ctx.stream),
+            "lu_solve_panels")
+
+
 class DeviceDirect:
     """Device-side factor of one dense system: apply(b_dev) -> x_dev."""
 
@@ -86,11 +124,16 @@ class DeviceDirect:
         self.dims = torch.tensor([n], dtype=I32, device=dev)
         self.perm = ipiv_to_perm(ctx, piv.to(I32).contiguous(), self.dims,
                                  self.vec_off)
+        self.panel = PanelFactor(self.LU, ctx) if n >= PANEL_MIN_N else None
 
     def apply(self, b: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         if out is None:
             out = torch.empty(self.n, dtype=F64, device=b.device)
         if self.n == 0:
+            return out
+        if self.panel is not None:
+            self.panel.solve(self.LU.data_ptr(), self.perm.data_ptr(), b,
+                             out.data_ptr())
             return out
         nat.check(self.ctx.lib.xdg_lu_solve_batched(
             1, self.lu_off.data_ptr(), self.dims.data_ptr(),

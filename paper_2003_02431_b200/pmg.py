@@ -21,7 +21,7 @@ import numpy as np
 import torch
 
 from . import _native as nat
-from .direct import ipiv_to_perm, lu_factor_dense
+from .direct import PANEL_MIN_N, PanelFactor, ipiv_to_perm, lu_factor_dense
 from .errors import SingularSystemError
 
 F64 = torch.float64
@@ -116,8 +116,11 @@ class PmgPlan:
             n = int(n)
             if n == 0:
                 continue
-            views = torch.stack([A[lu_off[s]:lu_off[s] + n * n] for s in idx]
-                                ).view(len(idx), n, n)
+            if len(idx) == 1:
+                views = A[lu_off[idx[0]]:lu_off[idx[0]] + n * n].view(1, n, n)
+            else:
+                views = torch.stack([A[lu_off[s]:lu_off[s] + n * n] for s in idx]
+                                    ).view(len(idx), n, n)
             try:
                 LU, pv = lu_factor_dense(views, "low-order system")
             except SingularSystemError as exc:
@@ -136,6 +139,19 @@ class PmgPlan:
         base = torch.from_numpy(np.repeat(vec_off[:-1], dims)).to(dev)
         # perm is local to each system: global position = base + local index
         self.src = gidx[base + perm].to(I32) if perm.numel() else perm.to(I32)
+        # large systems: multi-CTA panel solve; the batched kernel skips them
+        self.panels = []
+        small = dims.copy()
+        # (only when the systems are few: many systems already fill the GPU
+        # one CTA each)
+        big = np.flatnonzero(dims >= PANEL_MIN_N) if self.nsys <= 4 else []
+        for s_ in big:
+            n = int(dims[s_])
+            LUs = A[lu_off[s_]:lu_off[s_] + n * n].view(n, n)
+            self.panels.append((int(lu_off[s_]), int(vec_off[s_]), PanelFactor(LUs, ctx)))
+            small[s_] = 0
+        self.dims_small = up(small, I32)
+        self.any_small = bool(np.any(small > 0))
 
         # ---- high-order per-cell factors (solvers.py:225-243) ------------
         self.has_high = self.m < N
@@ -197,10 +213,14 @@ class PmgPlan:
         """z = sum_S PMG_S(b) ./ damping   (or the single-set PMG)."""
         ctx, D, lib, st = self.ctx, self.D, self.ctx.lib, self.ctx.stream
         xlo = z if (self.direct and not self.has_high) else self.xlo
-        nat.check(lib.xdg_lu_solve_batched(
-            self.nsys, self.lu_off.data_ptr(), self.dims.data_ptr(),
-            self.vec_off.data_ptr(), self.LU.data_ptr(), self.src.data_ptr(),
-            b.data_ptr(), xlo.data_ptr(), st), "lu_solve_batched")
+        if self.any_small:
+            nat.check(lib.xdg_lu_solve_batched(
+                self.nsys, self.lu_off.data_ptr(), self.dims_small.data_ptr(),
+                self.vec_off.data_ptr(), self.LU.data_ptr(), self.src.data_ptr(),
+                b.data_ptr(), xlo.data_ptr(), st), "lu_solve_batched")
+        for lo, vo, pf in self.panels:
+            pf.solve(self.LU.data_ptr() + 8 * lo, self.src.data_ptr() + 4 * vo, b,
+                     xlo.data_ptr() + 8 * vo)
         if self.has_high:
             out = z if self.direct else self.out
             nat.check(lib.xdg_pmg_high(
