@@ -175,6 +175,140 @@ int xdg_pmg_combine(int nbr, int N, const int* cptr, const int64_t* cpos,
                     const double* out, const double* damping, double* z,
                     xdg_stream_t stream);
 
+/* ======================================================================
+ * Native solver driver (the reference's control loops, solvers.py:559-846,
+ * run in C++ over device data: one host sync per rm_step / GMRES inner
+ * iteration, no Python in the iteration loop).  Plain-pointer structs; the
+ * host layer fills them from its device buffers.  All device pointers.
+ * ====================================================================== */
+typedef struct xdg_bsr {
+  int32_t nbr, nbc, N, pad0;
+  int64_t nnzb;
+  const int* row_ptr;
+  const int* col;
+  const double* val_t;
+} xdg_bsr;
+
+typedef struct xdg_panel {     /* one large system solved by panels */
+  int32_t n, pad0;
+  int64_t lu_off, vec_off;
+  const double* Linv;
+  const double* Uinv;
+  int* counters;
+} xdg_panel;
+
+typedef struct xdg_pmg {       /* PmgPlan of paper_2003_02431_b200/pmg.py */
+  int32_t nsys, nwork, N, m, has_high, direct, any_small, npanels;
+  const int64_t* lu_off;
+  const int* dims_small;
+  const int64_t* vec_off;
+  const double* LU;
+  const int* src;
+  double* xlo;
+  const int* wi_ptr;
+  const int* wi_blk;
+  const int* wi_lcol;
+  const int* wi_cell;
+  const int* wi_lrow;
+  const int64_t* wi_xlo;
+  const int* wi_hidx;
+  const int64_t* wi_out;
+  const double* HLU;
+  const int* hperm;
+  double* out;
+  const int* cptr;
+  const int64_t* cpos;
+  const double* damping;
+  const xdg_panel* panels;     /* HOST array of npanels */
+} xdg_pmg;
+
+typedef struct xdg_direct {    /* dense LU of one system (coarsest level) */
+  int32_t n, pad0;
+  const double* LU;
+  const int* perm;
+  const int64_t* zero_off;     /* device {0} */
+  const int* dims;             /* device {n} */
+  const xdg_panel* panel;      /* HOST pointer or NULL (one-CTA solve) */
+} xdg_direct;
+
+typedef struct xdg_rm {        /* RmState (solvers.py:485-556) */
+  int64_t n;
+  int32_t max_columns, ncols;
+  int32_t last_dependent, dependent_count, rejected_count, restart_count;
+  double best_norm;
+  double* W;                   /* [max_columns][n] */
+  double* Z;                   /* [max_columns][n] */
+  double* x0;
+  double* r0;
+  double* y;
+  double* My;
+  double* My_new;              /* swapped with My on accept */
+  double* Mz;
+  double* coeff;               /* [max_columns] */
+  double* sc;                  /* >= 8 device scalars */
+  double* alpha_host;          /* HOST [max_columns] */
+  double* x;                   /* current() outputs */
+  double* r;
+  void* ws;                    /* reduction workspace */
+  void* gemv_ws;               /* xdg_gemv_t_workspace_bytes(max_columns) */
+} xdg_rm;
+
+typedef struct xdg_omg_level { /* one level of ortho_mg_solve */
+  xdg_bsr M;
+  xdg_bsr R;                   /* prolongation (fine rows x coarse cols) */
+  xdg_bsr Rt;                  /* restriction */
+  int32_t has_restriction, pad0;
+  xdg_pmg schwarz;
+  xdg_direct direct;           /* used when coarsest */
+  xdg_rm rm;
+  double* b;                   /* this level's right-hand side buffer */
+  double* z;                   /* smoother output */
+  double* xf;                  /* R x_c */
+} xdg_omg_level;
+
+/* One rm_step (solvers.py:559-625) on state `rm` with operator M and
+ * candidate z (device, length rm->n).  Updates rm (host counters too) and
+ * leaves the current point / true residual in rm->x, rm->r. */
+int xdg_rm_step(xdg_rm* rm, const xdg_bsr* M, const double* z,
+                xdg_stream_t stream);
+/* RmState(x0, r0): copies x0, r0, zeroes y / My, best_norm = ||r0||. */
+int xdg_rm_init(xdg_rm* rm, const double* x0, const double* r0,
+                xdg_stream_t stream);
+/* RmState.restart() (solvers.py:548-556); also leaves x = x0, r = r0. */
+int xdg_rm_restart(xdg_rm* rm, xdg_stream_t stream);
+/* x = x0 + y, r = r0 - My  (RmState.current()). */
+int xdg_rm_current(xdg_rm* rm, xdg_stream_t stream);
+/* z = PMG / Schwarz application of a plan over operator M
+ * (pmg.PmgPlan.apply; solvers.py:245-265, 460-478). */
+int xdg_pmg_apply_op(const xdg_pmg* plan, const xdg_bsr* M, const double* b,
+                     double* z, xdg_stream_t stream);
+/* ortho_mg_solve (solvers.py:669-749) entered at level index `entry`
+ * (0-based) of `levels` (nlevels total).  x (device, entry level size) holds
+ * the initial guess if has_x0, else is zeroed.  history: HOST array of
+ * capacity max_iterations+1; *iterations, *hist_len, *final_residual set. */
+int xdg_omg_solve(xdg_omg_level* levels, int nlevels, int entry,
+                  double tolerance, int max_iterations,
+                  int coarse_cycle_iterations, const double* b, double* x,
+                  int has_x0, int* iterations, double* history, int* hist_len,
+                  double* final_residual, xdg_stream_t stream);
+/* Restarted GMRES with PMG on the right (solvers.py:756-846).  V: device
+ * [restart+1][n], Zb: [restart][n], w: [n], r: [n], sc: device
+ * [restart+8], ycoef: device [restart].  history: HOST, capacity
+ * max_iterations+1.  Returns XDG_ERR_SINGULAR on a zero Givens column. */
+int xdg_gmres_solve(const xdg_bsr* M, const xdg_pmg* pmg, int restart,
+                    double tolerance, int max_iterations, const double* b,
+                    double* x, int has_x0, double* V, double* Zb, double* w,
+                    double* r, double* sc, double* ycoef, void* ws,
+                    void* gemv_ws, int* iterations, double* history,
+                    int* hist_len, double* final_residual,
+                    xdg_stream_t stream);
+/* Fused modified Gram-Schmidt of GMRES step j (solvers.py:802-807):
+ * for i <= j: h_i = V_i . w ; w -= h_i V_i ; then h_{j+1} = ||w|| and
+ * V_{j+1} = w / h_{j+1} (zero if h_{j+1} == 0).  h (device) receives
+ * h_0..h_{j+1}.  One cooperative launch (grid-wide syncs between steps). */
+int xdg_mgs(int64_t n, int j, double* V, int64_t ldv, double* w, double* h,
+            void* ws, xdg_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

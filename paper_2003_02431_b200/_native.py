@@ -53,6 +53,16 @@ SIGNATURES = {
                                    _vp]),
     "xdg_pmg_high": (_i32, [_i32, _i32, _i32] + [_vp] * 15),
     "xdg_pmg_combine": (_i32, [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "xdg_rm_step": (_i32, [_vp, _vp, _vp, _vp]),
+    "xdg_rm_init": (_i32, [_vp, _vp, _vp, _vp]),
+    "xdg_rm_restart": (_i32, [_vp, _vp]),
+    "xdg_rm_current": (_i32, [_vp, _vp]),
+    "xdg_pmg_apply_op": (_i32, [_vp, _vp, _vp, _vp, _vp]),
+    "xdg_omg_solve": (_i32, [_vp, _i32, _i32, _f64, _i32, _i32, _vp, _vp, _i32,
+                             _vp, _vp, _vp, _vp, _vp]),
+    "xdg_gmres_solve": (_i32, [_vp, _vp, _i32, _f64, _i32, _vp, _vp, _i32]
+                        + [_vp] * 13),
+    "xdg_mgs": (_i32, [_i64, _i32, _vp, _i64, _vp, _vp, _vp, _vp]),
 }
 
 _lib = None

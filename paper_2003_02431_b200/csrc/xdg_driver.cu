@@ -1,0 +1,491 @@
+// Native solver driver: the control loops of the reference's residual
+// minimisation (solvers.py:559-625), orthonormalization multigrid
+// (solvers.py:669-749) and preconditioned GMRES (solvers.py:756-846), run
+// in C++ over device-resident data.  Scalar decisions (dependent candidate,
+// accept / reject, Givens rotations, convergence) stay on the host exactly
+// as in the reference; every vector operation is a kernel of this library.
+// Host syncs: one per rm_step (four scalars read back together), one per
+// GMRES inner iteration (the Hessenberg column), one per multigrid
+// iteration of the entry level is implied by the rm_step syncs.
+//
+// Fused kernels introduced here:
+//   mgs_kernel        cooperative: all j+1 MGS steps of one GMRES iteration,
+//                     one grid-wide sync per step (double-buffered partials),
+//                     the axpy of step i fused with the dot of step i+1
+//   rm_normalize      w /= ||w||, z /= ||w|| with ||w|| = sqrt(device dot)
+//   rm_commit         y += alpha z ; x = x0 + y ; r = r0 - My_new
+//   rm_restart        x0 += y ; r0 -= My ; y = My = 0 ; x = x0 ; r = r0
+//   rm_current        x = x0 + y ; r = r0 - My
+#include <cooperative_groups.h>
+#include <math.h>
+#include <string.h>
+
+#include <vector>
+
+#include "xdg_common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace xdg {
+namespace {
+
+constexpr int kT = 256;
+constexpr int kPerSm = 4;
+
+__global__ void __launch_bounds__(kT)
+rm_normalize_kernel(int64_t n, const double* __restrict__ nw2, double* w,
+                    double* z) {
+  const double d = sqrt(*nw2);
+  const int64_t stride = (int64_t)gridDim.x * kT;
+  for (int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x; i < n; i += stride) {
+    w[i] = __ddiv_rn(w[i], d);
+    z[i] = __ddiv_rn(z[i], d);
+  }
+}
+
+__global__ void __launch_bounds__(kT)
+rm_commit_kernel(int64_t n, const double* __restrict__ alpha,
+                 const double* __restrict__ z, double* __restrict__ y,
+                 const double* __restrict__ x0, const double* __restrict__ r0,
+                 const double* __restrict__ My_new, double* __restrict__ x,
+                 double* __restrict__ r) {
+  const double a = *alpha;
+  const int64_t stride = (int64_t)gridDim.x * kT;
+  for (int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x; i < n; i += stride) {
+    const double yi = __dadd_rn(y[i], __dmul_rn(a, z[i]));
+    y[i] = yi;
+    x[i] = __dadd_rn(x0[i], yi);
+    r[i] = __dadd_rn(r0[i], -My_new[i]);
+  }
+}
+
+__global__ void __launch_bounds__(kT)
+rm_restart_kernel(int64_t n, double* __restrict__ x0, double* __restrict__ r0,
+                  double* __restrict__ y, double* __restrict__ My,
+                  double* __restrict__ x, double* __restrict__ r) {
+  const int64_t stride = (int64_t)gridDim.x * kT;
+  for (int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x; i < n; i += stride) {
+    const double xn = __dadd_rn(x0[i], y[i]);
+    const double rn = __dadd_rn(r0[i], -My[i]);
+    x0[i] = xn;
+    r0[i] = rn;
+    y[i] = 0.0;
+    My[i] = 0.0;
+    x[i] = xn;
+    r[i] = rn;
+  }
+}
+
+__global__ void __launch_bounds__(kT)
+rm_current_kernel(int64_t n, const double* __restrict__ x0,
+                  const double* __restrict__ y, const double* __restrict__ r0,
+                  const double* __restrict__ My, double* __restrict__ x,
+                  double* __restrict__ r) {
+  const int64_t stride = (int64_t)gridDim.x * kT;
+  for (int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x; i < n; i += stride) {
+    x[i] = __dadd_rn(x0[i], y[i]);
+    r[i] = __dadd_rn(r0[i], -My[i]);
+  }
+}
+
+// ---- fused modified Gram-Schmidt (cooperative) ----------------------------
+__global__ void __launch_bounds__(kT)
+mgs_kernel(int64_t n, int j, double* __restrict__ V, int64_t ldv,
+           double* __restrict__ w, double* __restrict__ h,
+           double* __restrict__ parts) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double red[kT / 32];
+  const int G = gridDim.x;
+  const int64_t stride = (int64_t)G * kT;
+  const int64_t i0 = (int64_t)blockIdx.x * kT + threadIdx.x;
+  // step 0 dot: V_0 . w
+  double s = 0.0;
+  for (int64_t e = i0; e < n; e += stride) s = fma(V[e], w[e], s);
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) parts[blockIdx.x] = s;
+  grid.sync();
+  for (int i = 0; i <= j; ++i) {
+    const double* P = parts + (int64_t)(i & 1) * G;
+    double hi = 0.0;
+    for (int g = 0; g < G; ++g) hi += P[g];  // same order in every CTA
+    if (blockIdx.x == 0 && threadIdx.x == 0) h[i] = hi;
+    const double* Vi = V + (int64_t)i * ldv;
+    const double* Vn = V + (int64_t)(i + 1) * ldv;
+    double t = 0.0;
+    for (int64_t e = i0; e < n; e += stride) {
+      const double we = __dadd_rn(w[e], -__dmul_rn(hi, Vi[e]));
+      w[e] = we;
+      t = (i < j) ? fma(Vn[e], we, t) : fma(we, we, t);
+    }
+    t = block_sum(t, red);
+    if (threadIdx.x == 0) parts[(int64_t)((i + 1) & 1) * G + blockIdx.x] = t;
+    grid.sync();
+  }
+  const double* P = parts + (int64_t)((j + 1) & 1) * G;
+  double nrm2 = 0.0;
+  for (int g = 0; g < G; ++g) nrm2 += P[g];
+  const double hn = sqrt(nrm2);
+  if (blockIdx.x == 0 && threadIdx.x == 0) h[j + 1] = hn;
+  double* Vj1 = V + (int64_t)(j + 1) * ldv;
+  for (int64_t e = i0; e < n; e += stride)
+    Vj1[e] = hn > 0.0 ? __ddiv_rn(w[e], hn) : 0.0;
+}
+
+// ---------------------------------------------------------------------------
+// host helpers
+
+cudaError_t sync_read(double* host, const double* dev, int count, cudaStream_t s) {
+  cudaError_t e = cudaMemcpyAsync(host, dev, sizeof(double) * count,
+                                  cudaMemcpyDeviceToHost, s);
+  if (e != cudaSuccess) return e;
+  return cudaStreamSynchronize(s);
+}
+
+#define XDG_TRY(expr)                 \
+  do {                                \
+    int _st = (expr);                 \
+    if (_st != XDG_OK) return _st;    \
+  } while (0)
+
+int spmv(const xdg_bsr* M, const double* x, double* y, const double* b,
+         double* nrm, void* ws, cudaStream_t s) {
+  return xdg_bsr_spmv(0, M->nbr, M->N, M->row_ptr, M->col, M->val_t, x, y, 1.0,
+                      0.0, b, nrm, ws, reinterpret_cast<xdg_stream_t>(s));
+}
+
+}  // namespace
+}  // namespace xdg
+
+using namespace xdg;
+
+// ---------------------------------------------------------------------------
+// The plan struct is operator-agnostic; the operator's blocks come in M.
+static int pmg_apply_op(const xdg_pmg* P, const xdg_bsr* M, const double* b,
+                        double* z, cudaStream_t s) {
+  xdg_stream_t st = reinterpret_cast<xdg_stream_t>(s);
+  double* xlo = (P->direct && !P->has_high) ? z : P->xlo;
+  if (P->any_small)
+    XDG_TRY(xdg_lu_solve_batched(P->nsys, P->lu_off, P->dims_small, P->vec_off,
+                                 P->LU, P->src, b, xlo, st));
+  for (int k = 0; k < P->npanels; ++k) {
+    const xdg_panel& q = P->panels[k];
+    XDG_TRY(xdg_lu_solve_panels(q.n, P->LU + q.lu_off, q.Linv, q.Uinv,
+                                P->src + q.vec_off, b, xlo + q.vec_off,
+                                q.counters, st));
+  }
+  if (P->has_high) {
+    double* out = P->direct ? z : P->out;
+    XDG_TRY(xdg_pmg_high(P->nwork, P->N, P->m, P->wi_ptr, P->wi_blk, P->wi_lcol,
+                         P->wi_cell, P->wi_lrow, P->wi_xlo, P->wi_hidx,
+                         P->wi_out, M->val_t, P->HLU, P->hperm, b, xlo, out, st));
+  }
+  if (!P->direct)
+    XDG_TRY(xdg_pmg_combine(M->nbr, P->N, P->cptr, P->cpos, P->out, P->damping,
+                            z, st));
+  return XDG_OK;
+}
+
+extern "C" int xdg_pmg_apply_op(const xdg_pmg* P, const xdg_bsr* M,
+                                const double* b, double* z,
+                                xdg_stream_t stream) {
+  return pmg_apply_op(P, M, b, z, reinterpret_cast<cudaStream_t>(stream));
+}
+
+// ---------------------------------------------------------------------------
+extern "C" int xdg_rm_current(xdg_rm* rm, xdg_stream_t stream) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  rm_current_kernel<<<grid_for(rm->n, kT, kPerSm), kT, 0, s>>>(
+      rm->n, rm->x0, rm->y, rm->r0, rm->My, rm->x, rm->r);
+  XDG_CHECK_LAUNCH();
+  return XDG_OK;
+}
+
+extern "C" int xdg_rm_init(xdg_rm* rm, const double* x0, const double* r0,
+                           xdg_stream_t stream) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const size_t bytes = sizeof(double) * rm->n;
+  if (x0 != rm->x0) XDG_TRY_CUDA(cudaMemcpyAsync(rm->x0, x0, bytes, cudaMemcpyDeviceToDevice, s));
+  if (r0 != rm->r0) XDG_TRY_CUDA(cudaMemcpyAsync(rm->r0, r0, bytes, cudaMemcpyDeviceToDevice, s));
+  XDG_TRY_CUDA(cudaMemsetAsync(rm->y, 0, bytes, s));
+  XDG_TRY_CUDA(cudaMemsetAsync(rm->My, 0, bytes, s));
+  XDG_TRY(xdg_dot(rm->n, rm->r0, rm->r0, rm->sc + 7, rm->ws, stream));
+  double v;
+  XDG_TRY_CUDA(sync_read(&v, rm->sc + 7, 1, s));
+  rm->best_norm = sqrt(v);
+  rm->ncols = 0;
+  rm->last_dependent = 0;
+  rm->dependent_count = rm->rejected_count = rm->restart_count = 0;
+  return XDG_OK;
+}
+
+static int rm_restart(xdg_rm* rm, cudaStream_t s) {
+  // best_norm is unchanged: it already is || r0 - My || of the very vector
+  // that becomes the new r0 (same kernel, same data -> same bits), which is
+  // what solvers.py:554 recomputes.
+  rm_restart_kernel<<<grid_for(rm->n, kT, kPerSm), kT, 0, s>>>(
+      rm->n, rm->x0, rm->r0, rm->y, rm->My, rm->x, rm->r);
+  XDG_CHECK_LAUNCH();
+  rm->ncols = 0;
+  rm->restart_count += 1;
+  return XDG_OK;
+}
+
+extern "C" int xdg_rm_step(xdg_rm* rm, const xdg_bsr* M, const double* zc,
+                           xdg_stream_t stream) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t n = rm->n;
+  if (rm->ncols >= rm->max_columns) XDG_TRY(rm_restart(rm, s));
+  const int col = rm->ncols;
+  double* z = rm->Z + (int64_t)col * n;  // candidate lives in its would-be column
+  double* w = rm->W + (int64_t)col * n;
+  if (zc != z)
+    XDG_TRY_CUDA(cudaMemcpyAsync(z, zc, sizeof(double) * n,
+                                 cudaMemcpyDeviceToDevice, s));
+  double* sc = rm->sc;
+  XDG_TRY(spmv(M, z, w, nullptr, sc + 0, rm->ws, s));          // w = M z
+  if (col > 0) {
+    for (int pass = 0; pass < 2; ++pass) {                    // CGS x2
+      XDG_TRY(xdg_gemv_t(n, col, rm->W, n, w, rm->coeff, rm->gemv_ws, stream));
+      XDG_TRY(xdg_gemv_update2(n, col, rm->W, rm->Z, n, rm->coeff, w, z, stream));
+    }
+  }
+  XDG_TRY(xdg_dot(n, w, w, sc + 1, rm->ws, stream));          // ||w||^2
+  // speculative tail (discarded when the candidate is dependent)
+  rm_normalize_kernel<<<grid_for(n, kT, kPerSm), kT, 0, s>>>(n, sc + 1, w, z);
+  XDG_CHECK_LAUNCH();
+  XDG_TRY(xdg_dot(n, w, rm->r0, sc + 2, rm->ws, stream));     // alpha = w . r0
+  XDG_TRY(spmv(M, z, rm->Mz, nullptr, nullptr, nullptr, s));  // exact image
+  XDG_TRY(xdg_rm_update(n, rm->r0, rm->My, rm->Mz, sc + 2, rm->My_new, sc + 3,
+                        rm->ws, stream));
+  double h[4];
+  XDG_TRY_CUDA(sync_read(h, sc, 4, s));
+  const double scale = sqrt(h[0]), norm_w = sqrt(h[1]);
+  if (scale == 0.0 || norm_w <= 1e-13 * scale) {               // solvers.py:594-599
+    rm->last_dependent = 1;
+    rm->dependent_count += 1;
+    return xdg_rm_current(rm, stream);
+  }
+  const double alpha = h[2], rho = sqrt(h[3]);
+  rm->last_dependent = 0;
+  if (rho > rm->best_norm) {                                   // solvers.py:609-615
+    rm->rejected_count += 1;
+    return rm_restart(rm, s);
+  }
+  rm->alpha_host[col] = alpha;
+  rm_commit_kernel<<<grid_for(n, kT, kPerSm), kT, 0, s>>>(
+      n, sc + 2, z, rm->y, rm->x0, rm->r0, rm->My_new, rm->x, rm->r);
+  XDG_CHECK_LAUNCH();
+  double* t = rm->My;
+  rm->My = rm->My_new;
+  rm->My_new = t;
+  rm->best_norm = rho;
+  rm->ncols = col + 1;
+  return XDG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// ortho_mg_solve
+
+namespace {
+
+struct OmgRun {
+  xdg_omg_level* L;
+  int nlevels, entry;
+  double tol;
+  int max_it, coarse_it;
+  cudaStream_t s;
+};
+
+// Solves level `lam` (0-based) for rhs b_dev into x_dev.  Returns status;
+// iterations / history only recorded for the entry level.
+int omg_level(OmgRun& R, int lam, const double* b, double* x, int has_x0,
+              int* iters, double* hist, int* hist_len, double* final_res) {
+  xdg_omg_level& lv = R.L[lam];
+  xdg_stream_t st = reinterpret_cast<xdg_stream_t>(R.s);
+  xdg_rm& rm = lv.rm;
+  const int64_t n = (int64_t)lv.M.nbr * lv.M.N;
+  if (lam == R.nlevels - 1 || !lv.has_restriction) {           // solvers.py:698-710
+    const xdg_direct& D = lv.direct;
+    if (D.panel != nullptr)
+      XDG_TRY(xdg_lu_solve_panels(D.n, D.LU, D.panel->Linv, D.panel->Uinv, D.perm,
+                                  b, x, D.panel->counters, st));
+    else
+      XDG_TRY(xdg_lu_solve_batched(1, D.zero_off, D.dims, D.zero_off, D.LU, D.perm,
+                                   b, x, st));
+    if (lam == R.entry) {
+      XDG_TRY(spmv(&lv.M, x, rm.r, b, rm.sc + 6, rm.ws, R.s));
+      double v;
+      XDG_TRY_CUDA(sync_read(&v, rm.sc + 6, 1, R.s));
+      *final_res = sqrt(v);
+      hist[0] = *final_res;
+      *hist_len = 1;
+      *iters = 0;
+    }
+    return XDG_OK;
+  }
+  if (!has_x0) XDG_TRY_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, R.s));
+  // r = b - M x ; RmState(x, r)
+  XDG_TRY(spmv(&lv.M, x, rm.r, b, nullptr, nullptr, R.s));
+  XDG_TRY(xdg_rm_init(&rm, x, rm.r, st));
+  double* H = (lam == R.entry) ? hist : nullptr;
+  int hl = 0;
+  double last = rm.best_norm;
+  if (H) H[hl] = last;
+  ++hl;
+  const int budget = (lam == R.entry) ? R.max_it : R.coarse_it;
+  int it = 0;
+  xdg_omg_level& nx = R.L[lam + 1];
+  while (last > R.tol && it < budget) {
+    ++it;
+    XDG_TRY(pmg_apply_op(&lv.schwarz, &lv.M, rm.r, lv.z, R.s));
+    XDG_TRY(xdg_rm_step(&rm, &lv.M, lv.z, st));
+    XDG_TRY(spmv(&lv.Rt, rm.r, nx.b, nullptr, nullptr, nullptr, R.s));  // r_c = R^T r
+    XDG_TRY(omg_level(R, lam + 1, nx.b, nx.rm.x, 0, nullptr, nullptr, nullptr, nullptr));
+    // the coarse solution sits in nx.rm.x (for the coarsest: written there)
+    XDG_TRY(spmv(&lv.R, nx.rm.x, lv.xf, nullptr, nullptr, nullptr, R.s));
+    XDG_TRY(xdg_rm_step(&rm, &lv.M, lv.xf, st));
+    XDG_TRY(pmg_apply_op(&lv.schwarz, &lv.M, rm.r, lv.z, R.s));
+    XDG_TRY(xdg_rm_step(&rm, &lv.M, lv.z, st));
+    // ||r|| of the returned residual == best_norm (every rm_step exit leaves
+    // r = r0 - My whose norm is best_norm)
+    last = rm.best_norm;
+    if (H) H[hl] = last;
+    ++hl;
+  }
+  if (it > 0 && x != rm.x)
+    XDG_TRY_CUDA(cudaMemcpyAsync(x, rm.x, sizeof(double) * n,
+                                 cudaMemcpyDeviceToDevice, R.s));
+  if (lam == R.entry) {
+    *iters = it;
+    *hist_len = hl;
+    *final_res = last;
+  }
+  return XDG_OK;
+}
+
+}  // namespace
+
+extern "C" int xdg_omg_solve(xdg_omg_level* levels, int nlevels, int entry,
+                             double tolerance, int max_iterations,
+                             int coarse_cycle_iterations, const double* b,
+                             double* x, int has_x0, int* iterations,
+                             double* history, int* hist_len,
+                             double* final_residual, xdg_stream_t stream) {
+  XDG_REQUIRE(nlevels >= 1 && entry >= 0 && entry < nlevels, XDG_ERR_ARG,
+              "bad level range");
+  OmgRun R{levels, nlevels, entry, tolerance, max_iterations,
+           coarse_cycle_iterations, reinterpret_cast<cudaStream_t>(stream)};
+  int st = omg_level(R, entry, b, x, has_x0, iterations, history, hist_len,
+                     final_residual);
+  if (st != XDG_OK) return st;
+  XDG_TRY_CUDA(cudaStreamSynchronize(R.s));
+  return XDG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// GMRES
+
+extern "C" int xdg_mgs(int64_t n, int j, double* V, int64_t ldv, double* w,
+                       double* h, void* ws, xdg_stream_t stream) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  static thread_local int per_sm = 0;
+  if (per_sm == 0) {
+    XDG_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mgs_kernel,
+                                                               kT, 0));
+    if (per_sm < 1) per_sm = 1;
+  }
+  int64_t need = (n + kT - 1) / kT;
+  int64_t cap = (int64_t)sm_count() * (per_sm < 2 ? per_sm : 2);
+  int grid = (int)(need < cap ? (need < 1 ? 1 : need) : cap);
+  // partials: 2 x grid doubles after the reduction counter slot
+  double* parts = static_cast<double*>(ws) + 1;
+  void* args[] = {&n, &j, &V, &ldv, &w, &h, &parts};
+  XDG_TRY_CUDA(cudaLaunchCooperativeKernel((const void*)mgs_kernel, dim3(grid),
+                                           dim3(kT), args, 0, s));
+  return XDG_OK;
+}
+
+extern "C" int xdg_gmres_solve(const xdg_bsr* M, const xdg_pmg* pmg,
+                               int restart, double tolerance,
+                               int max_iterations, const double* b, double* x,
+                               int has_x0, double* V, double* Zb, double* w,
+                               double* r, double* sc, double* ycoef, void* ws,
+                               void* gemv_ws, int* iterations, double* history,
+                               int* hist_len, double* final_residual,
+                               xdg_stream_t stream) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int m = restart;
+  const int64_t n = (int64_t)M->nbr * M->N;
+  (void)gemv_ws;
+  if (!has_x0) XDG_TRY_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, s));
+  XDG_TRY(spmv(M, x, r, b, sc, ws, s));
+  double v;
+  XDG_TRY_CUDA(sync_read(&v, sc, 1, s));
+  double beta = sqrt(v);
+  int hl = 0, total = 0;
+  history[hl++] = beta;
+  std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), g(m + 1), hc(m + 2),
+      y(m);
+  auto Hc = [&](int i, int jj) -> double& { return H[(size_t)i * m + jj]; };
+  while (beta > tolerance && total < max_iterations) {
+    std::fill(H.begin(), H.end(), 0.0);
+    std::fill(cs.begin(), cs.end(), 0.0);
+    std::fill(sn.begin(), sn.end(), 0.0);
+    std::fill(g.begin(), g.end(), 0.0);
+    g[0] = beta;
+    XDG_TRY(xdg_scale(n, beta, nullptr, 1, r, V, stream));      // V_0 = r / beta
+    int j = 0;
+    while (j < m && total < max_iterations) {
+      ++total;
+      double* Vj = V + (int64_t)j * n;
+      double* Zj = Zb + (int64_t)j * n;
+      XDG_TRY(pmg_apply_op(pmg, M, Vj, Zj, s));
+      XDG_TRY(spmv(M, Zj, w, nullptr, nullptr, nullptr, s));
+      XDG_TRY(xdg_mgs(n, j, V, n, w, sc, ws, stream));
+      XDG_TRY_CUDA(sync_read(hc.data(), sc, j + 2, s));
+      for (int i = 0; i <= j + 1; ++i) Hc(i, j) = hc[i];
+      for (int i = 0; i < j; ++i) {                               // rotations
+        const double hij = cs[i] * Hc(i, j) + sn[i] * Hc(i + 1, j);
+        Hc(i + 1, j) = -sn[i] * Hc(i, j) + cs[i] * Hc(i + 1, j);
+        Hc(i, j) = hij;
+      }
+      const double denom = hypot(Hc(j, j), Hc(j + 1, j));
+      if (denom == 0.0) {
+        set_error("preconditioned operator produced a zero column");
+        return XDG_ERR_SINGULAR;
+      }
+      cs[j] = Hc(j, j) / denom;
+      sn[j] = Hc(j + 1, j) / denom;
+      Hc(j, j) = cs[j] * Hc(j, j) + sn[j] * Hc(j + 1, j);
+      g[j + 1] = -sn[j] * g[j];
+      g[j] = cs[j] * g[j];
+      Hc(j + 1, j) = 0.0;
+      const double est = fabs(g[j + 1]);
+      history[hl++] = est;
+      ++j;
+      if (est <= tolerance) break;
+    }
+    // y = H[:j,:j]^-1 g[:j] (upper triangular back substitution)
+    for (int i = j - 1; i >= 0; --i) {
+      double t = g[i];
+      for (int k = i + 1; k < j; ++k) t -= Hc(i, k) * y[k];
+      y[i] = t / Hc(i, i);
+    }
+    for (int i = 0; i < j; ++i) y[i] = -y[i];                     // x -= Z (-y)
+    XDG_TRY_CUDA(cudaMemcpyAsync(ycoef, y.data(), sizeof(double) * j,
+                                 cudaMemcpyHostToDevice, s));
+    XDG_TRY(xdg_gemv_update2(n, j, Zb, nullptr, n, ycoef, x, nullptr, stream));
+    XDG_TRY(spmv(M, x, r, b, sc, ws, s));
+    XDG_TRY_CUDA(sync_read(&v, sc, 1, s));
+    beta = sqrt(v);
+    history[hl - 1] = beta;
+  }
+  *iterations = total;
+  *hist_len = hl;
+  *final_residual = beta;
+  return XDG_OK;
+}
+
+extern "C" int xdg_rm_restart(xdg_rm* rm, xdg_stream_t stream) {
+  return rm_restart(rm, reinterpret_cast<cudaStream_t>(stream));
+}

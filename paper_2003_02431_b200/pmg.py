@@ -210,33 +210,18 @@ class PmgPlan:
 
     # ------------------------------------------------------------------
     def apply(self, b: torch.Tensor, z: torch.Tensor) -> torch.Tensor:
-        """z = sum_S PMG_S(b) ./ damping   (or the single-set PMG)."""
-        ctx, D, lib, st = self.ctx, self.D, self.ctx.lib, self.ctx.stream
-        xlo = z if (self.direct and not self.has_high) else self.xlo
-        if self.any_small:
-            nat.check(lib.xdg_lu_solve_batched(
-                self.nsys, self.lu_off.data_ptr(), self.dims_small.data_ptr(),
-                self.vec_off.data_ptr(), self.LU.data_ptr(), self.src.data_ptr(),
-                b.data_ptr(), xlo.data_ptr(), st), "lu_solve_batched")
-        for lo, vo, pf in self.panels:
-            pf.solve(self.LU.data_ptr() + 8 * lo, self.src.data_ptr() + 4 * vo, b,
-                     xlo.data_ptr() + 8 * vo)
-        if self.has_high:
-            out = z if self.direct else self.out
-            nat.check(lib.xdg_pmg_high(
-                self.nwork, self.N, self.m, self.wi_ptr.data_ptr(),
-                self.wi_blk.data_ptr(), self.wi_lcol.data_ptr(),
-                self.wi_cell.data_ptr(), self.wi_lrow.data_ptr(),
-                self.wi_xlo.data_ptr(), self.wi_hidx.data_ptr(),
-                self.wi_out.data_ptr(), D.val_t.data_ptr(), self.HLU.data_ptr(),
-                self.hperm.data_ptr(), b.data_ptr(), xlo.data_ptr(),
-                out.data_ptr(), st), "pmg_high")
-        if not self.direct:
-            nat.check(lib.xdg_pmg_combine(
-                D.nbr, self.N, self.cptr.data_ptr(), self.cpos.data_ptr(),
-                self.out.data_ptr(),
-                None if self.damping is None else self.damping.data_ptr(),
-                z.data_ptr(), st), "pmg_combine")
+        """z = sum_S PMG_S(b) ./ damping   (or the single-set PMG), through
+        the native xdg_pmg_apply_op."""
+        import ctypes as C
+
+        from .driver import bsr_struct, pmg_struct
+
+        if getattr(self, "_struct", None) is None:
+            self._struct = pmg_struct(self)
+        Ms = bsr_struct(self.D)
+        nat.check(self.ctx.lib.xdg_pmg_apply_op(
+            C.byref(self._struct[0]), C.byref(Ms), b.data_ptr(), z.data_ptr(),
+            self.ctx.stream), "pmg_apply")
         return z
 
     def algorithmic_bytes(self) -> int:

@@ -21,6 +21,7 @@ or CUDA tensors (returning CUDA tensors, zero-copy for device callers).
 from __future__ import annotations
 
 import csv
+import ctypes as C
 import math
 from dataclasses import dataclass
 from math import comb
@@ -33,6 +34,7 @@ import torch
 from .blockmatrix import as_block_sparse
 from .device import Context, DeviceBSR
 from .direct import DirectFactorization, direct_factor
+from .driver import RmBuffers, XdgOmgLevel, bsr_struct, direct_struct, pmg_struct
 from .errors import (
     DimensionMismatchError,
     InvalidConfigError,
@@ -293,14 +295,14 @@ def schwarz_apply(M, residual, partition: SchwarzPartition, k_lo):
 
 
 # ---------------------------------------------------------------------------
-# residual minimization (solvers.py:485-625)
+# residual minimization (solvers.py:485-625) -- native driver (xdg_rm_*)
 
 
 class RmState:
     """Growing orthonormal search space (solvers.py:485-556), device
-    resident: W, Z are (max_columns, L) row-per-column buffers in HBM.
-    `W`, `Z`, `alpha`, `x0`, `r0`, `current()` return host copies for
-    inspection; the solvers use the `_dev` views."""
+    resident: W, Z are (max_columns, L) buffers in HBM, counters live in the
+    native `xdg_rm` struct that xdg_rm_step updates.  `W`, `Z`, `alpha`,
+    `x0`, `r0`, `current()` return host copies for inspection."""
 
     def __init__(self, x0, r0, max_columns: int = DEFAULT_RM_MAX_COLUMNS):
         if _length(x0) != _length(r0):
@@ -309,62 +311,45 @@ class RmState:
             raise InvalidConfigError("max_columns must be >= 1")
         ctx = Context.get()
         self._ctx = ctx
-        self._host = not (_is_dev(x0) or _is_dev(r0))
-        self._x0 = _to_dev(x0, ctx)
-        self._r0 = _to_dev(r0, ctx)
-        n = self._x0.numel()
-        self.n = n
+        xd, rd = _to_dev(x0, ctx), _to_dev(r0, ctx)
+        self.n = xd.numel()
         self.max_columns = int(max_columns)
-        dev = ctx.device
-        self._W = torch.empty(self.max_columns, n, dtype=F64, device=dev)
-        self._Z = torch.empty(self.max_columns, n, dtype=F64, device=dev)
-        self._alpha = np.zeros(self.max_columns)
-        self._y = torch.zeros(n, dtype=F64, device=dev)
-        self._My = torch.zeros(n, dtype=F64, device=dev)
-        self._Mz = torch.empty(n, dtype=F64, device=dev)
-        self._My_new = torch.empty(n, dtype=F64, device=dev)
-        self._coeff = torch.zeros(self.max_columns, dtype=F64, device=dev)
-        self._sc = torch.zeros(8, dtype=F64, device=dev)
-        self.best_norm = self._norm(self._r0)
-        self.ncols = 0
-        self.last_dependent = False
-        self.dependent_count = 0
-        self.rejected_count = 0
-        self.restart_count = 0
+        self._buf = RmBuffers(ctx, self.n, self.max_columns)
+        nat_check(ctx.lib.xdg_rm_init(C.byref(self._buf.s), xd.data_ptr(),
+                                      rd.data_ptr(), ctx.stream), "rm_init")
 
-    def _norm(self, v: torch.Tensor) -> float:
-        self._ctx.dot(v, v, self._sc[7:8])
-        return math.sqrt(float(_sync_read(self._sc[7:8])[0]))
+    # counters / scalars of the native state (reference attribute names)
+    ncols = property(lambda self: self._buf.s.ncols)
+    best_norm = property(lambda self: self._buf.s.best_norm)
+    last_dependent = property(lambda self: bool(self._buf.s.last_dependent))
+    dependent_count = property(lambda self: self._buf.s.dependent_count)
+    rejected_count = property(lambda self: self._buf.s.rejected_count)
+    restart_count = property(lambda self: self._buf.s.restart_count)
 
-    # host views (reference attribute semantics)
     @property
     def x0(self):
-        return self._x0.cpu().numpy()
+        return self._buf.x0.cpu().numpy()
 
     @property
     def r0(self):
-        return self._r0.cpu().numpy()
+        return self._buf.r0.cpu().numpy()
 
     @property
     def W(self):
-        return self._W[: self.ncols].T.cpu().numpy()
+        return self._buf.W[: self.ncols].T.cpu().numpy()
 
     @property
     def Z(self):
-        return self._Z[: self.ncols].T.cpu().numpy()
+        return self._buf.Z[: self.ncols].T.cpu().numpy()
 
     @property
     def alpha(self):
-        return self._alpha[: self.ncols].copy()
+        return self._buf.alpha_host[: self.ncols].copy()
 
     def current_dev(self) -> tuple:
-        ctx = self._ctx
-        x = torch.empty_like(self._x0)
-        r = torch.empty_like(self._r0)
-        ctx.lib.xdg_add(self.n, self._x0.data_ptr(), self._y.data_ptr(),
-                        x.data_ptr(), ctx.stream)
-        ctx.sub(self._r0, self._My, r)
-        return x, r
+        nat_check(self._ctx.lib.xdg_rm_current(C.byref(self._buf.s), self._ctx.stream),
+                  "rm_current")
+        return self._buf.x.clone(), self._buf.r.clone()
 
     def current(self) -> tuple:
         x, r = self.current_dev()
@@ -372,59 +357,8 @@ class RmState:
 
     def restart(self) -> None:
         """Collapse the space onto the current point (solvers.py:548-556)."""
-        x, r = self.current_dev()
-        self._x0, self._r0 = x, r
-        self._y.zero_()
-        self._My.zero_()
-        self.best_norm = self._norm(self._r0)
-        self.ncols = 0
-        self.restart_count += 1
-
-
-def _rm_step_dev(state: RmState, z_cand: torch.Tensor, D: DeviceBSR):
-    """Device rm_step; returns (x, r) device tensors (solvers.py:559-625)."""
-    ctx = state._ctx
-    if state.ncols >= state.max_columns:
-        state.restart()
-    col = state.ncols
-    z = state._Z[col]          # candidate lives in its would-be column
-    w = state._W[col]
-    z.copy_(z_cand)
-    sc = state._sc
-    D.spmv(z, w, norm_out=sc[0:1])                  # w = M z, ||w||^2
-    if col > 0:
-        Wv, Zv, coeff = state._W, state._Z, state._coeff
-        for _ in range(2):   # two classical Gram-Schmidt passes
-            ctx.gemv_t(Wv[:col], col, w, coeff)
-            ctx.gemv_update2(Wv, Zv, col, coeff, w, z)
-    ctx.dot(w, w, sc[1:2])
-    s01 = _sync_read(sc[0:2])
-    scale, norm_w = math.sqrt(s01[0]), math.sqrt(s01[1])
-    if scale == 0.0 or norm_w <= DEPENDENT_CANDIDATE_RTOL * scale:
-        state.last_dependent = True
-        state.dependent_count += 1
-        return state.current_dev()
-    ctx.scale(norm_w, w, w, invert=True)
-    ctx.scale(norm_w, z, z, invert=True)
-    ctx.dot(w, state._r0, sc[2:3])                  # alpha = w . r0
-    D.spmv(z, state._Mz)                            # exact image M z
-    nat_check(ctx.lib.xdg_rm_update(
-        state.n, state._r0.data_ptr(), state._My.data_ptr(),
-        state._Mz.data_ptr(), sc[2:3].data_ptr(), state._My_new.data_ptr(),
-        sc[3:4].data_ptr(), ctx.ws, ctx.stream), "rm_update")
-    s23 = _sync_read(sc[2:4])
-    alpha, rho = float(s23[0]), math.sqrt(s23[1])
-    state.last_dependent = False
-    if rho > state.best_norm:
-        state.rejected_count += 1
-        state.restart()
-        return state.current_dev()
-    state._alpha[col] = alpha
-    ctx.axpy(1.0, z, state._y, a_dev=sc[2:3])       # y += alpha z
-    state._My, state._My_new = state._My_new, state._My
-    state.best_norm = rho
-    state.ncols = col + 1
-    return state.current_dev()
+        nat_check(self._ctx.lib.xdg_rm_restart(C.byref(self._buf.s), self._ctx.stream),
+                  "rm_restart")
 
 
 def nat_check(status, what):
@@ -440,7 +374,11 @@ def rm_step(state: RmState, z_candidate, M) -> tuple:
         raise DimensionMismatchError("candidate length mismatch")
     ctx = state._ctx
     D = _device_operator(M, ctx)
-    x, r = _rm_step_dev(state, _to_dev(z_candidate, ctx, copy=False), D)
+    zd = _to_dev(z_candidate, ctx, copy=False)
+    Ms = bsr_struct(D)
+    nat_check(ctx.lib.xdg_rm_step(C.byref(state._buf.s), C.byref(Ms), zd.data_ptr(),
+                                  ctx.stream), "rm_step")
+    x, r = state._buf.x.clone(), state._buf.r.clone()
     host = not _is_dev(z_candidate)
     return _out(x, not host), _out(r, not host), state
 
@@ -450,7 +388,7 @@ def rm_step(state: RmState, z_candidate, M) -> tuple:
 
 
 class _OmgContext:
-    """Per-solve caches (solvers.py:632-666) plus their device twins."""
+    """Per-solve caches (solvers.py:632-666) plus the native level structs."""
 
     def __init__(self, config: SolverConfig, entry_level: int = 1):
         self.config = config
@@ -459,6 +397,7 @@ class _OmgContext:
         self.transposes = {}
         self.coarse_factorization = {}
         self._dev = Context.get()
+        self._native = None
 
     def partition(self, hierarchy, level: int) -> SchwarzPartition:
         part = self.partitions.get(level)
@@ -483,82 +422,81 @@ class _OmgContext:
             self.coarse_factorization[level] = fact
         return fact
 
-
-def _dev_norm(ctx: Context, v: torch.Tensor, slot: torch.Tensor) -> float:
-    ctx.dot(v, v, slot)
-    return math.sqrt(float(_sync_read(slot)[0]))
-
-
-def _omg_dev(hierarchy, b: torch.Tensor, x0, config: SolverConfig, level: int,
-             ctx_omg: _OmgContext):
-    ctx = ctx_omg._dev
-    lv = hierarchy.level(level)
-    M = lv.matrix
-    config.check_degree(lv.data.basis.degree)
-    t_start = perf_counter()
-    D = as_block_sparse(M).device(ctx)
-    scal = torch.zeros(1, dtype=F64, device=ctx.device)
-    n = M.shape[0]
-
-    if level == hierarchy.num_levels or lv.restriction is None:
-        x = ctx_omg.coarse_solver(hierarchy, level).apply_device(b)
-        r = torch.empty_like(b)
-        D.spmv(x, r, b=b, norm_out=scal)
-        res = math.sqrt(float(_sync_read(scal)[0]))
-        torch.cuda.synchronize(ctx.device)
-        return x, SolverReport(solver="omg", iterations=0,
-                               converged=res <= config.tolerance,
-                               final_residual=res, residual_history=[res],
-                               time_iterations=perf_counter() - t_start, dofs=n)
-
-    x = torch.zeros_like(b) if x0 is None else _to_dev(x0, ctx)
-    r = torch.empty_like(b)
-    D.spmv(x, r, b=b)
-    state = RmState(x, r, config.rm_max_columns)
-    history = [state.best_norm]          # == ||r|| (same kernel, same data)
-    partition = ctx_omg.partition(hierarchy, level)
-    k_lo = config.k_lo_scalar
-    R = as_block_sparse(lv.restriction)
-    Rd = R.device(ctx)
-    Rtd = ctx_omg.restriction_transpose(hierarchy, level).device(ctx)
-    budget = (config.max_iterations if level == ctx_omg.entry_level
-              else config.coarse_cycle_iterations)
-    z = torch.empty_like(b)
-    xf = torch.empty_like(b)
-    rc = torch.empty(Rtd.nbr * Rtd.N, dtype=F64, device=ctx.device)
-    it = 0
-    while history[-1] > config.tolerance and it < budget:
-        it += 1
-        _schwarz_dev(M, D, r, partition, k_lo, ctx, z)
-        x, r = _rm_step_dev(state, z, D)
-        Rtd.spmv(r, rc)                                   # r_c = R^T r
-        xc, _ = _omg_dev(hierarchy, rc, None, config, level + 1, ctx_omg)
-        Rd.spmv(xc, xf)                                   # R x_c
-        x, r = _rm_step_dev(state, xf, D)
-        _schwarz_dev(M, D, r, partition, k_lo, ctx, z)
-        x, r = _rm_step_dev(state, z, D)
-        # ||r0 - My|| of the returned residual equals state.best_norm: every
-        # exit of rm_step leaves r = r0 - My with best_norm its norm.
-        history.append(state.best_norm)
-    torch.cuda.synchronize(ctx.device)
-    return x, SolverReport(solver="omg", iterations=it,
-                           converged=history[-1] <= config.tolerance,
-                           final_residual=history[-1], residual_history=history,
-                           time_iterations=perf_counter() - t_start, dofs=n)
+    def native_levels(self, hierarchy, entry: int):
+        """XdgOmgLevel array for levels entry..last visited (built once)."""
+        if self._native is not None:
+            return self._native
+        ctx = self._dev
+        cfg = self.config
+        nl = hierarchy.num_levels
+        arr = (XdgOmgLevel * nl)()
+        keep = []
+        k_lo = cfg.k_lo_scalar
+        for lam in range(entry, nl + 1):
+            lv = hierarchy.level(lam)
+            cfg.check_degree(lv.data.basis.degree)
+            M = as_block_sparse(lv.matrix)
+            D = M.device(ctx)
+            n = D.nbr * D.N
+            L = arr[lam - 1]
+            L.M = bsr_struct(D)
+            coarsest = lam == nl or lv.restriction is None
+            rm = RmBuffers(ctx, n, cfg.rm_max_columns, allocate_space=not coarsest)
+            keep.append(rm)
+            L.rm = rm.s
+            bufs = torch.zeros(3, n, dtype=F64, device=ctx.device)
+            keep.append(bufs)
+            L.b, L.z, L.xf = (bufs[i].data_ptr() for i in range(3))
+            if coarsest:
+                dd = self.coarse_solver(hierarchy, lam)._dev
+                L.direct, k = direct_struct(dd)
+                keep += [dd, k]
+                L.has_restriction = 0
+                break
+            part = self.partition(hierarchy, lam)
+            modes_low = min(space_dimension(k_lo, part.dim), _uniform_block_size(M))
+            plan = _schwarz_plan(M, D, part, modes_low, ctx)
+            L.schwarz, k = pmg_struct(plan)
+            keep += [plan, k]
+            Rd = as_block_sparse(lv.restriction).device(ctx)
+            Rtd = self.restriction_transpose(hierarchy, lam).device(ctx)
+            L.R, L.Rt = bsr_struct(Rd), bsr_struct(Rtd)
+            keep += [Rd, Rtd]
+            L.has_restriction = 1
+        self._native = (arr, keep)
+        return self._native
 
 
 def ortho_mg_solve(hierarchy, b, x0=None, config: Optional[SolverConfig] = None,
                    level: int = 1, _context: Optional[_OmgContext] = None) -> tuple:
     """Orthonormalization multigrid (Alg. 4) on `level`; returns
-    (solution, SolverReport); non-convergence is reported, not raised."""
+    (solution, SolverReport); non-convergence is reported, not raised.
+    The iteration loop runs in the native driver (xdg_omg_solve)."""
     config = config or SolverConfig()
     ctx_omg = _context or _OmgContext(config, entry_level=level)
     lv = hierarchy.level(level)
     if _length(b) != (lv.matrix.shape[0],):
         raise DimensionMismatchError(
             f"rhs of length {_length(b)} against matrix {lv.matrix.shape}")
-    bd = _to_dev(b, ctx_omg._dev)
-    x, rep = _omg_dev(hierarchy, bd, x0, config, level, ctx_omg)
+    config.check_degree(lv.data.basis.degree)
+    ctx = ctx_omg._dev
+    bd = _to_dev(b, ctx)
+    t_start = perf_counter()
+    arr, _keep = ctx_omg.native_levels(hierarchy, level)
+    n = bd.numel()
+    x = torch.zeros_like(bd) if x0 is None else _to_dev(x0, ctx)
+    hist = np.zeros(config.max_iterations + 2)
+    it, hl, fin = C.c_int(0), C.c_int(0), C.c_double(0.0)
+    nat_check(ctx.lib.xdg_omg_solve(
+        arr, hierarchy.num_levels, level - 1, float(config.tolerance),
+        int(config.max_iterations), int(config.coarse_cycle_iterations),
+        bd.data_ptr(), x.data_ptr(), int(x0 is not None), C.byref(it),
+        hist.ctypes.data, C.byref(hl), C.byref(fin), ctx.stream), "omg_solve")
+    history = [float(v) for v in hist[: hl.value]]
+    rep = SolverReport(solver="omg", iterations=it.value,
+                       converged=fin.value <= config.tolerance,
+                       final_residual=fin.value, residual_history=history,
+                       time_iterations=perf_counter() - t_start, dofs=n)
     return _out(x, _is_dev(b)), rep
 
 
@@ -570,88 +508,47 @@ def gmres_pmg_solve(M, b, config: Optional[SolverConfig] = None,
                     factorization_cache: Optional[dict] = None, *, dim: int,
                     x0=None) -> tuple:
     """Restarted GMRES, degree-separated preconditioner on the right, MGS
-    orthogonalisation, Givens rotations; stops on the true residual."""
-    from scipy.linalg import solve_triangular
-
+    orthogonalisation, Givens rotations; stops on the true residual.  The
+    iteration loop runs in the native driver (xdg_gmres_solve)."""
     config = config or SolverConfig()
     cache = factorization_cache if factorization_cache is not None else {}
     if _length(b) != (M.shape[0],):
         raise DimensionMismatchError(f"rhs of length {_length(b)} against matrix {M.shape}")
     nb = M.row_layout.num_blocks
     all_cells = tuple(range(nb))
-    k_lo = config.k_lo_scalar
     m = config.gmres_restart
     ctx = Context.get()
+    bd = _to_dev(b, ctx)
     t_start = perf_counter()
     D = _device_operator(M, ctx)
-    modes_low = min(space_dimension(_normalize_k_lo(k_lo), dim), _uniform_block_size(M))
+    modes_low = min(space_dimension(_normalize_k_lo(config.k_lo_scalar), dim),
+                    _uniform_block_size(M))
     plan = _pmg_plan(M, D, all_cells, modes_low, cache)
-    bd = _to_dev(b, ctx)
     n = bd.numel()
     dev = ctx.device
     x = torch.zeros_like(bd) if x0 is None else _to_dev(x0, ctx)
-    r = torch.empty_like(bd)
-    sc = torch.zeros(m + 2, dtype=F64, device=dev)
-    D.spmv(x, r, b=bd, norm_out=sc[0:1])
-    beta = math.sqrt(float(_sync_read(sc[0:1])[0]))
-    history = [beta]
-    total = 0
     V = torch.empty(m + 1, n, dtype=F64, device=dev)
     Z = torch.empty(m, n, dtype=F64, device=dev)
     w = torch.empty(n, dtype=F64, device=dev)
-    ycoef = torch.empty(m, dtype=F64, device=dev)
-
-    while beta > config.tolerance and total < config.max_iterations:
-        H = np.zeros((m + 1, m))
-        cs = np.zeros(m)
-        sn = np.zeros(m)
-        g = np.zeros(m + 1)
-        g[0] = beta
-        ctx.scale(beta, r, V[0], invert=True)
-        j = 0
-        while j < m and total < config.max_iterations:
-            total += 1
-            plan.apply(V[j], Z[j])
-            D.spmv(Z[j], w)
-            for i in range(j + 1):                    # modified Gram-Schmidt
-                ctx.dot(V[i], w, sc[i:i + 1])
-                ctx.axpy(-1.0, V[i], w, a_dev=sc[i:i + 1])
-            ctx.dot(w, w, sc[j + 1:j + 2])
-            col = _sync_read(sc[: j + 2])
-            H[: j + 1, j] = col[: j + 1]
-            H[j + 1, j] = math.sqrt(col[j + 1])
-            if H[j + 1, j] > 0.0:
-                ctx.scale(H[j + 1, j], w, V[j + 1], invert=True)
-            else:
-                V[j + 1].zero_()
-            for i in range(j):                        # stored rotations
-                h_i = cs[i] * H[i, j] + sn[i] * H[i + 1, j]
-                H[i + 1, j] = -sn[i] * H[i, j] + cs[i] * H[i + 1, j]
-                H[i, j] = h_i
-            denom = float(np.hypot(H[j, j], H[j + 1, j]))
-            if denom == 0.0:
-                raise SingularSystemError("preconditioned operator produced a zero column")
-            cs[j] = H[j, j] / denom
-            sn[j] = H[j + 1, j] / denom
-            H[j, j] = cs[j] * H[j, j] + sn[j] * H[j + 1, j]
-            g[j + 1] = -sn[j] * g[j]
-            g[j] = cs[j] * g[j]
-            H[j + 1, j] = 0.0
-            estimate = abs(float(g[j + 1]))
-            history.append(estimate)
-            j += 1
-            if estimate <= config.tolerance:
-                break
-        yv = solve_triangular(H[:j, :j], g[:j], check_finite=False)
-        ycoef[:j].copy_(torch.from_numpy(-yv))
-        # x = x + Z y   (as x -= Z (-y); negation is exact)
-        ctx.gemv_update2(Z, None, j, ycoef, x, None)
-        D.spmv(x, r, b=bd, norm_out=sc[0:1])
-        beta = math.sqrt(float(_sync_read(sc[0:1])[0]))
-        history[-1] = beta
+    r = torch.empty(n, dtype=F64, device=dev)
+    sc = torch.zeros(m + 8, dtype=F64, device=dev)
+    ycoef = torch.zeros(m, dtype=F64, device=dev)
+    ws = torch.zeros((int(ctx.lib.xdg_reduce_workspace_bytes()) + 7) // 8, dtype=F64,
+                     device=dev)
+    hist = np.zeros(config.max_iterations + 2)
+    it, hl, fin = C.c_int(0), C.c_int(0), C.c_double(0.0)
+    Ms = bsr_struct(D)
+    Ps, _k = pmg_struct(plan)
+    nat_check(ctx.lib.xdg_gmres_solve(
+        C.byref(Ms), C.byref(Ps), m, float(config.tolerance), int(config.max_iterations),
+        bd.data_ptr(), x.data_ptr(), int(x0 is not None), V.data_ptr(), Z.data_ptr(),
+        w.data_ptr(), r.data_ptr(), sc.data_ptr(), ycoef.data_ptr(), ws.data_ptr(),
+        None, C.byref(it), hist.ctypes.data, C.byref(hl), C.byref(fin), ctx.stream),
+        "gmres_solve")
     torch.cuda.synchronize(dev)
-    rep = SolverReport(solver="gmres-pmg", iterations=total,
-                       converged=beta <= config.tolerance, final_residual=beta,
+    history = [float(v) for v in hist[: hl.value]]
+    rep = SolverReport(solver="gmres-pmg", iterations=it.value,
+                       converged=fin.value <= config.tolerance, final_residual=fin.value,
                        residual_history=history,
                        time_iterations=perf_counter() - t_start, dofs=M.shape[0])
     return _out(x, _is_dev(b)), rep
