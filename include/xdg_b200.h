@@ -120,24 +120,27 @@ int xdg_gemv_update2(int64_t L, int ncols, const double* W, const double* Z,
 
 
 /* ---- dense LU solves (batched, variable size) --------------------------- */
-/* For s < nsys: n = dims[s]; LU + lu_off[s] is the packed row-major n x n
- * factor of a partial-pivoting LU (A = P L U, unit L); x + vec_off[s]
- * receives the solution of A x = b_s where b_s[i] = b[src[vec_off[s]+i]]
- * (pivot permutation pre-composed with the gather).  One CTA per system.
- * Replaces SuperLU solve (blockmatrix.py:224) for the low-order PMG
- * systems (solvers.py:249-251) and the coarsest-level direct solve
- * (solvers.py:699). */
-int xdg_lu_solve_batched(int nsys, const int64_t* lu_off, const int* dims,
-                         const int64_t* vec_off, const double* LU,
-                         const int* src, const double* b, double* x,
-                         xdg_stream_t stream);
-/* One large system: x = U^-1 L^-1 (b[src[i]])_i with one CTA per 64-row
- * panel chained through counters (4 ints of device scratch, zeroed by the
- * call).  Linv / Uinv: inverses of the 64x64 diagonal blocks of L (unit) and
- * U, (ceil(n/64), 64, 64) row-major, identity-padded past n.  Deterministic. */
-int xdg_lu_solve_panels(int n, const double* LU, const double* Linv,
-                        const double* Uinv, const int* src, const double* b,
-                        double* x, int* counters, xdg_stream_t stream);
+/* Factors: a partial-pivoting LU (A = P L U, L unit lower) stored as its
+ * TRIANGULAR INVERSES, INV (row-major n x n per system): L^-1 strictly below
+ * the diagonal (unit diagonal implicit), U^-1 on and above it.  A solve
+ * x = U^-1 L^-1 P^T b is two triangular GEMVs (8 n^2 bytes, the same as
+ * forward/backward substitution, without the sequential chain).
+ * Replaces SuperLU solve (blockmatrix.py:224) for the low-order PMG systems
+ * (solvers.py:249-251) and the coarsest-level direct solve (solvers.py:699).
+ *
+ * Batched: for s < nsys, n = dims[s] (0: skipped), INV + off[s], and
+ * x + vec_off[s] = A_s^-1 (b[src[vec_off[s]+i]])_i -- pivot permutation
+ * pre-composed with the gather.  One CTA per system; max_n = max dims
+ * (2 max_n doubles of shared memory, max_n <= 12800). */
+int xdg_lu_inv_apply_batched(int nsys, const int64_t* off, const int* dims,
+                             const int64_t* vec_off, const double* INV,
+                             const int* src, const double* b, double* x,
+                             int max_n, xdg_stream_t stream);
+/* One large system over the whole GPU (warp per row, 3 launches);
+ * scratch: 2 n doubles. */
+int xdg_lu_inv_apply_large(int n, const double* INV, const int* src,
+                           const double* b, double* x, double* scratch,
+                           xdg_stream_t stream);
 /* LAPACK ipiv (1-based sequential swaps) -> permutation perm with
  * (P^T b)[i] = b[perm[i]], per system (setup). */
 int xdg_ipiv_to_perm(int nsys, const int* dims, const int64_t* vec_off,
@@ -189,20 +192,19 @@ typedef struct xdg_bsr {
   const double* val_t;
 } xdg_bsr;
 
-typedef struct xdg_panel {     /* one large system solved by panels */
+typedef struct xdg_large {     /* one large system: xdg_lu_inv_apply_large */
   int32_t n, pad0;
-  int64_t lu_off, vec_off;
-  const double* Linv;
-  const double* Uinv;
-  int* counters;
-} xdg_panel;
+  int64_t off, vec_off;
+  double* scratch;             /* 2 n doubles */
+} xdg_large;
 
 typedef struct xdg_pmg {       /* PmgPlan of paper_2003_02431_b200/pmg.py */
-  int32_t nsys, nwork, N, m, has_high, direct, any_small, npanels;
+  int32_t nsys, nwork, N, m, has_high, direct, any_small, nlarge;
+  int32_t max_n_small, pad0;
   const int64_t* lu_off;
   const int* dims_small;
   const int64_t* vec_off;
-  const double* LU;
+  const double* LU;            /* triangular-inverse factors (INV) */
   const int* src;
   double* xlo;
   const int* wi_ptr;
@@ -219,16 +221,16 @@ typedef struct xdg_pmg {       /* PmgPlan of paper_2003_02431_b200/pmg.py */
   const int* cptr;
   const int64_t* cpos;
   const double* damping;
-  const xdg_panel* panels;     /* HOST array of npanels */
+  const xdg_large* large;      /* HOST array of nlarge */
 } xdg_pmg;
 
 typedef struct xdg_direct {    /* dense LU of one system (coarsest level) */
-  int32_t n, pad0;
-  const double* LU;
+  int32_t n, large;            /* large: whole-GPU apply, else one CTA */
+  const double* LU;            /* triangular-inverse factors (INV) */
   const int* perm;
   const int64_t* zero_off;     /* device {0} */
   const int* dims;             /* device {n} */
-  const xdg_panel* panel;      /* HOST pointer or NULL (one-CTA solve) */
+  double* scratch;             /* 2 n doubles (large) */
 } xdg_direct;
 
 typedef struct xdg_rm {        /* RmState (solvers.py:485-556) */

@@ -165,13 +165,13 @@ static int pmg_apply_op(const xdg_pmg* P, const xdg_bsr* M, const double* b,
   xdg_stream_t st = reinterpret_cast<xdg_stream_t>(s);
   double* xlo = (P->direct && !P->has_high) ? z : P->xlo;
   if (P->any_small)
-    XDG_TRY(xdg_lu_solve_batched(P->nsys, P->lu_off, P->dims_small, P->vec_off,
-                                 P->LU, P->src, b, xlo, st));
-  for (int k = 0; k < P->npanels; ++k) {
-    const xdg_panel& q = P->panels[k];
-    XDG_TRY(xdg_lu_solve_panels(q.n, P->LU + q.lu_off, q.Linv, q.Uinv,
-                                P->src + q.vec_off, b, xlo + q.vec_off,
-                                q.counters, st));
+    XDG_TRY(xdg_lu_inv_apply_batched(P->nsys, P->lu_off, P->dims_small,
+                                     P->vec_off, P->LU, P->src, b, xlo,
+                                     P->max_n_small, st));
+  for (int k = 0; k < P->nlarge; ++k) {
+    const xdg_large& q = P->large[k];
+    XDG_TRY(xdg_lu_inv_apply_large(q.n, P->LU + q.off, P->src + q.vec_off, b,
+                                   xlo + q.vec_off, q.scratch, st));
   }
   if (P->has_high) {
     double* out = P->direct ? z : P->out;
@@ -306,12 +306,11 @@ int omg_level(OmgRun& R, int lam, const double* b, double* x, int has_x0,
   const int64_t n = (int64_t)lv.M.nbr * lv.M.N;
   if (lam == R.nlevels - 1 || !lv.has_restriction) {           // solvers.py:698-710
     const xdg_direct& D = lv.direct;
-    if (D.panel != nullptr)
-      XDG_TRY(xdg_lu_solve_panels(D.n, D.LU, D.panel->Linv, D.panel->Uinv, D.perm,
-                                  b, x, D.panel->counters, st));
+    if (D.large)
+      XDG_TRY(xdg_lu_inv_apply_large(D.n, D.LU, D.perm, b, x, D.scratch, st));
     else
-      XDG_TRY(xdg_lu_solve_batched(1, D.zero_off, D.dims, D.zero_off, D.LU, D.perm,
-                                   b, x, st));
+      XDG_TRY(xdg_lu_inv_apply_batched(1, D.zero_off, D.dims, D.zero_off, D.LU,
+                                       D.perm, b, x, D.n, st));
     if (lam == R.entry) {
       XDG_TRY(spmv(&lv.M, x, rm.r, b, rm.sc + 6, rm.ws, R.s));
       double v;

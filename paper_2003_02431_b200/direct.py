@@ -5,9 +5,9 @@ blockmatrix.py:203-243).
 The reference factors with SuperLU (COLAMD + partial pivoting) and solves
 on the host.  Here the matrix is assembled dense on the device
 (xdg_pmg_build_low with every block), factored once with a partial-pivoting
-LU (setup; torch.linalg.lu_factor_ex -> cuSOLVER getrf, plumbing), and every
-`apply` runs the hand-written pivoted forward/backward substitution kernel
-(xdg_lu_solve_batched).  Dense storage bounds the size
+LU (setup; torch.linalg.lu_factor_ex -> cuSOLVER getrf, plumbing) whose
+triangular factors are inverted once (setup), and every `apply` runs the
+hand-written pivoted triangular-GEMV kernels (xdg_lu_inv_apply_*).  Dense storage bounds the size
 (MAX_DENSE_DIRECT unknowns); the coarsest multigrid levels and the
 low-order PMG systems it serves are small.
 """
@@ -68,77 +68,70 @@ def dense_from_device_bsr(D) -> torch.Tensor:
     return A.view(n, n)
 
 
-PANEL = 64          # rows per panel of xdg_lu_solve_panels
-PANEL_MIN_N = 2048  # systems at least this large use the multi-CTA solve
+SMEM_MAX_N = 12800   # one-CTA batched apply keeps 2 n doubles in smem
+LARGE_MIN_N = 512    # a lone system this large is applied over the whole GPU
 
 
-class PanelFactor:
-    """Extra setup for the multi-CTA solve of one large factored system:
-    inverses of the 64x64 diagonal blocks of L (unit lower) and U."""
-
-    def __init__(self, LU: torch.Tensor, ctx):
-        n = LU.shape[0]
-        self.n, self.ctx = n, ctx
-        npan = (n + PANEL - 1) // PANEL
-        pad = npan * PANEL - n
-        dev = LU.device
-        eye = torch.eye(PANEL, dtype=F64, device=dev)
-        Lb = torch.empty(npan, PANEL, PANEL, dtype=F64, device=dev)
-        Ub = torch.empty_like(Lb)
-        for p in range(npan):
-            r0, r1 = p * PANEL, min((p + 1) * PANEL, n)
-            blk = eye.clone()
-            blk[: r1 - r0, : r1 - r0] = LU[r0:r1, r0:r1]
-            Lb[p] = torch.tril(blk, -1) + eye
-            Ub[p] = torch.triu(blk)
-            if r1 - r0 < PANEL:
-                Ub[p, r1 - r0:, r1 - r0:] = eye[: pad, : pad]
-        self.Linv = torch.linalg.solve_triangular(
-            Lb, eye.expand_as(Lb), upper=False, unitriangular=True).contiguous()
-        self.Uinv = torch.linalg.solve_triangular(
-            Ub, eye.expand_as(Ub), upper=True).contiguous()
-        self.counters = torch.zeros(4, dtype=I32, device=dev)
-
-    def solve(self, LU_ptr: int, src_ptr: int, b: torch.Tensor, x_ptr: int):
-        nat.check(self.ctx.lib.xdg_lu_solve_panels(
-            self.n, LU_ptr, self.Linv.data_ptr(), self.Uinv.data_ptr(), src_ptr,
-            b.data_ptr(), x_ptr, self.counters.data_ptr(), self.ctx.stream),
-            "lu_solve_panels")
+def triangular_inverses(LU: torch.Tensor, chunk_bytes: int = 2 << 30) -> torch.Tensor:
+    """INV of a packed LU (n, n) or batch (b, n, n): L^-1 strictly below the
+    diagonal (unit diagonal implicit), U^-1 on and above it (setup; the
+    inverses of triangular matrices via torch.linalg.solve_triangular)."""
+    if LU.dim() == 2:
+        return triangular_inverses(LU.unsqueeze(0), chunk_bytes)[0]
+    nb, n, _ = LU.shape
+    out = torch.empty_like(LU)
+    eye = torch.eye(n, dtype=LU.dtype, device=LU.device)
+    step = max(1, chunk_bytes // max(1, 8 * n * n * 4))
+    for s in range(0, nb, step):
+        blk = LU[s:s + step]
+        Linv = torch.linalg.solve_triangular(torch.tril(blk, -1) + eye, eye.expand_as(blk),
+                                             upper=False, unitriangular=True)
+        Uinv = torch.linalg.solve_triangular(torch.triu(blk), eye.expand_as(blk),
+                                             upper=True)
+        out[s:s + step] = torch.tril(Linv, -1) + torch.triu(Uinv)
+    return out
 
 
 class DeviceDirect:
     """Device-side factor of one dense system: apply(b_dev) -> x_dev."""
 
-    def __init__(self, A: torch.Tensor, ctx, what="matrix"):
+    def __init__(self, A: torch.Tensor, ctx, what="matrix", large=None):
         n = A.shape[0]
         self.n = n
         self.ctx = ctx
         dev = ctx.device
         if n == 0:
-            self.LU = torch.zeros(0, dtype=F64, device=dev)
+            self.INV = torch.zeros(0, dtype=F64, device=dev)
+            self.large = False
             return
         LU, piv = lu_factor_dense(A, what)
-        self.LU = LU.contiguous()
+        self.INV = triangular_inverses(LU).contiguous()
+        del LU
         self.lu_off = torch.zeros(1, dtype=torch.int64, device=dev)
         self.vec_off = torch.zeros(1, dtype=torch.int64, device=dev)
         self.dims = torch.tensor([n], dtype=I32, device=dev)
         self.perm = ipiv_to_perm(ctx, piv.to(I32).contiguous(), self.dims,
                                  self.vec_off)
-        self.panel = PanelFactor(self.LU, ctx) if n >= PANEL_MIN_N else None
+        self.large = (n >= LARGE_MIN_N or n > SMEM_MAX_N) if large is None else bool(large)
+        if n > SMEM_MAX_N:
+            self.large = True
+        self.scratch = torch.empty(2 * n, dtype=F64, device=dev)
 
     def apply(self, b: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         if out is None:
             out = torch.empty(self.n, dtype=F64, device=b.device)
         if self.n == 0:
             return out
-        if self.panel is not None:
-            self.panel.solve(self.LU.data_ptr(), self.perm.data_ptr(), b,
-                             out.data_ptr())
+        if self.large:
+            nat.check(self.ctx.lib.xdg_lu_inv_apply_large(
+                self.n, self.INV.data_ptr(), self.perm.data_ptr(), b.data_ptr(),
+                out.data_ptr(), self.scratch.data_ptr(), self.ctx.stream),
+                "lu_inv_apply_large")
             return out
-        nat.check(self.ctx.lib.xdg_lu_solve_batched(
-            1, self.lu_off.data_ptr(), self.dims.data_ptr(),
-            self.vec_off.data_ptr(), self.LU.data_ptr(), self.perm.data_ptr(),
-            b.data_ptr(), out.data_ptr(), self.ctx.stream), "lu_solve")
+        nat.check(self.ctx.lib.xdg_lu_inv_apply_batched(
+            1, self.lu_off.data_ptr(), self.dims.data_ptr(), self.vec_off.data_ptr(),
+            self.INV.data_ptr(), self.perm.data_ptr(), b.data_ptr(), out.data_ptr(),
+            self.n, self.ctx.stream), "lu_inv_apply")
         return out
 
 

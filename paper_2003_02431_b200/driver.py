@@ -24,24 +24,24 @@ class XdgBsr(C.Structure):
                 ("col", _vp), ("val_t", _vp)]
 
 
-class XdgPanel(C.Structure):
-    _fields_ = [("n", C.c_int32), ("pad0", C.c_int32), ("lu_off", C.c_int64),
-                ("vec_off", C.c_int64), ("Linv", _vp), ("Uinv", _vp),
-                ("counters", _vp)]
+class XdgLarge(C.Structure):
+    _fields_ = [("n", C.c_int32), ("pad0", C.c_int32), ("off", C.c_int64),
+                ("vec_off", C.c_int64), ("scratch", _vp)]
 
 
 class XdgPmg(C.Structure):
     _fields_ = [(f, C.c_int32) for f in ("nsys", "nwork", "N", "m", "has_high",
-                                         "direct", "any_small", "npanels")] + \
+                                         "direct", "any_small", "nlarge",
+                                         "max_n_small", "pad0")] + \
         [(f, _vp) for f in ("lu_off", "dims_small", "vec_off", "LU", "src", "xlo",
                             "wi_ptr", "wi_blk", "wi_lcol", "wi_cell", "wi_lrow",
                             "wi_xlo", "wi_hidx", "wi_out", "HLU", "hperm", "out",
-                            "cptr", "cpos", "damping", "panels")]
+                            "cptr", "cpos", "damping", "large")]
 
 
 class XdgDirect(C.Structure):
-    _fields_ = [("n", C.c_int32), ("pad0", C.c_int32), ("LU", _vp), ("perm", _vp),
-                ("zero_off", _vp), ("dims", _vp), ("panel", _vp)]
+    _fields_ = [("n", C.c_int32), ("large", C.c_int32), ("LU", _vp), ("perm", _vp),
+                ("zero_off", _vp), ("dims", _vp), ("scratch", _vp)]
 
 
 class XdgRm(C.Structure):
@@ -69,24 +69,24 @@ def bsr_struct(D) -> XdgBsr:
                   D.col.data_ptr(), D.val_t.data_ptr())
 
 
-def panel_structs(items):
-    """items: list of (lu_off, vec_off, PanelFactor) -> (array, count)."""
+def large_structs(items):
+    """items: list of (n, off, vec_off, scratch) -> (ctypes array, count)."""
     if not items:
         return None, 0
-    arr = (XdgPanel * len(items))()
-    for i, (lo, vo, pf) in enumerate(items):
-        arr[i] = XdgPanel(pf.n, 0, lo, vo, pf.Linv.data_ptr(), pf.Uinv.data_ptr(),
-                          pf.counters.data_ptr())
+    arr = (XdgLarge * len(items))()
+    for i, (n, off, vo, scratch) in enumerate(items):
+        arr[i] = XdgLarge(n, 0, off, vo, scratch.data_ptr())
     return arr, len(items)
 
 
 def pmg_struct(plan):
     """(XdgPmg, keepalive) for a pmg.PmgPlan."""
-    panels, npan = panel_structs(plan.panels)
+    large, nlarge = large_structs(plan.large)
     s = XdgPmg()
     s.nsys, s.nwork, s.N, s.m = plan.nsys, plan.nwork, plan.N, plan.m
-    s.has_high, s.direct, s.any_small, s.npanels = (int(plan.has_high), int(plan.direct),
-                                                     int(plan.any_small), npan)
+    s.has_high, s.direct, s.any_small, s.nlarge = (int(plan.has_high), int(plan.direct),
+                                                   int(plan.any_small), nlarge)
+    s.max_n_small = plan.max_n_small
     s.lu_off, s.dims_small, s.vec_off = _p(plan.lu_off), _p(plan.dims_small), _p(plan.vec_off)
     s.LU, s.src, s.xlo = _p(plan.LU), _p(plan.src), _p(plan.xlo)
     for f in ("wi_ptr", "wi_blk", "wi_lcol", "wi_cell", "wi_lrow"):
@@ -98,24 +98,20 @@ def pmg_struct(plan):
     if not plan.direct:
         s.out, s.cptr, s.cpos = _p(plan.out), _p(plan.cptr), _p(plan.cpos)
         s.damping = _p(plan.damping)
-    s.panels = C.cast(panels, _vp) if panels is not None else None
-    return s, [panels]
+    s.large = C.cast(large, _vp) if large is not None else None
+    return s, [large]
 
 
 def direct_struct(dd):
     """XdgDirect for a direct.DeviceDirect."""
-    keep = []
     s = XdgDirect()
     s.n = dd.n
     if dd.n:
-        s.LU, s.perm = _p(dd.LU), _p(dd.perm)
+        s.large = int(dd.large)
+        s.LU, s.perm = _p(dd.INV), _p(dd.perm)
         s.zero_off, s.dims = _p(dd.lu_off), _p(dd.dims)
-        if dd.panel is not None:
-            pa = XdgPanel(dd.panel.n, 0, 0, 0, dd.panel.Linv.data_ptr(),
-                          dd.panel.Uinv.data_ptr(), dd.panel.counters.data_ptr())
-            keep.append(pa)
-            s.panel = C.cast(C.pointer(pa), _vp)
-    return s, keep
+        s.scratch = _p(dd.scratch)
+    return s, []
 
 
 class RmBuffers:

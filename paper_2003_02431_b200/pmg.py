@@ -11,7 +11,7 @@ solvers.py:300-305):
   * per cell: pivoted LU of the high-order diagonal block H_c, shared by
     every set containing the cell (H_c depends only on M[c, c]).
 Apply (3 launches, all sets at once):
-  xdg_lu_solve_batched  -> x_lo of every set (one CTA per set)
+  xdg_lu_inv_apply_*    -> x_lo of every set (triangular-inverse GEMVs)
   xdg_pmg_high          -> residual on the high rows + per-cell H_c solves
   xdg_pmg_combine       -> ordered sum over sets / damping (or scatter)
 """
@@ -21,7 +21,8 @@ import numpy as np
 import torch
 
 from . import _native as nat
-from .direct import PANEL_MIN_N, PanelFactor, ipiv_to_perm, lu_factor_dense
+from .direct import (LARGE_MIN_N, SMEM_MAX_N, ipiv_to_perm, lu_factor_dense,
+                     triangular_inverses)
 from .errors import SingularSystemError
 
 F64 = torch.float64
@@ -127,6 +128,7 @@ class PmgPlan:
                 cells = tuple(int(c) for c in sets[idx[0]][:8])
                 raise SingularSystemError(
                     f"low-order system on cells {cells}... is singular") from exc
+            LU = triangular_inverses(LU)
             for q, s in enumerate(idx):
                 A[lu_off[s]:lu_off[s] + n * n] = LU[q].reshape(-1)
                 piv[vec_off[s]:vec_off[s] + n] = pv[q].to(I32)
@@ -139,18 +141,18 @@ class PmgPlan:
         base = torch.from_numpy(np.repeat(vec_off[:-1], dims)).to(dev)
         # perm is local to each system: global position = base + local index
         self.src = gidx[base + perm].to(I32) if perm.numel() else perm.to(I32)
-        # large systems: multi-CTA panel solve; the batched kernel skips them
-        self.panels = []
+        # a few large systems: whole-GPU apply each; the batched one-CTA
+        # kernel (which fills the GPU when there are many systems) skips them
+        self.large = []
         small = dims.copy()
-        # (only when the systems are few: many systems already fill the GPU
-        # one CTA each)
-        big = np.flatnonzero(dims >= PANEL_MIN_N) if self.nsys <= 4 else []
-        for s_ in big:
+        for s_ in range(self.nsys):
             n = int(dims[s_])
-            LUs = A[lu_off[s_]:lu_off[s_] + n * n].view(n, n)
-            self.panels.append((int(lu_off[s_]), int(vec_off[s_]), PanelFactor(LUs, ctx)))
-            small[s_] = 0
+            if n > SMEM_MAX_N or (self.nsys <= 4 and n >= LARGE_MIN_N):
+                scratch = torch.empty(2 * n, dtype=F64, device=dev)
+                self.large.append((n, int(lu_off[s_]), int(vec_off[s_]), scratch))
+                small[s_] = 0
         self.dims_small = up(small, I32)
+        self.max_n_small = int(small.max()) if len(small) else 0
         self.any_small = bool(np.any(small > 0))
 
         # ---- high-order per-cell factors (solvers.py:225-243) ------------

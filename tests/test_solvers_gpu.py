@@ -106,19 +106,21 @@ def test_direct_factorization_matches_reference():
             assert F.factor_count == 1
 
 
-def test_panel_lu_solve_large_random_system():
-    """Multi-CTA panel triangular solves (n >= 2048) against numpy."""
+@pytest.mark.parametrize("large", [False, True])
+def test_dense_lu_inverse_apply_random_systems(large):
+    """Triangular-inverse LU applies (one-CTA batched and whole-GPU) vs numpy."""
     import torch
 
     from paper_2003_02431_b200.device import Context
     from paper_2003_02431_b200.direct import DeviceDirect
 
     rng = np.random.default_rng(11)
-    for n in (2048, 3001, 5000):
+    for n in (1, 37, 600, 2048, 5000):
+        if n > 12800 and not large:
+            continue
         A = rng.standard_normal((n, n)) + n ** 0.5 * np.eye(n)
         b = rng.standard_normal(n)
-        F = DeviceDirect(torch.from_numpy(A).cuda(), Context.get())
-        assert F.panel is not None
+        F = DeviceDirect(torch.from_numpy(A).cuda(), Context.get(), large=large)
         x1 = F.apply(torch.from_numpy(b).cuda()).cpu().numpy()
         x2 = F.apply(torch.from_numpy(b).cuda()).cpu().numpy()
         assert np.array_equal(x1, x2)  # deterministic
