@@ -179,7 +179,7 @@ def time_solves(torch, budget_s: float):
 
     out = []
     t_start = time.perf_counter()
-    for case in ("cfg1", "sphere8p3"):
+    for case in ("cfg1", "sphere8p3", "large/s16p3", "large/cfg2"):
         path = os.path.join(ROOT, "tests", "golden", f"{case}.npz")
         if not os.path.exists(path):
             continue
@@ -196,8 +196,11 @@ def time_solves(torch, budget_s: float):
                 x, rep = ortho_mg_solve(hier, lv.rhs, None, cfg, 1)
             else:
                 x, rep = gmres_pmg_solve(lv.matrix, lv.rhs, cfg, dim=meta["dim"])
-            ref_x = z[f"{solver}_x"]
-            rel = float(np.linalg.norm(x - ref_x) / np.linalg.norm(ref_x))
+            if f"{solver}_x" in z:
+                ref_x = z[f"{solver}_x"]
+                rel = float(np.linalg.norm(x - ref_x) / np.linalg.norm(ref_x))
+            else:  # large fixtures: no reference solve (hours on the CPU)
+                rel = None
             ref_s = meta.get(f"{solver}_seconds")
             cpu_here = None
             if case == "cfg1":  # bounded: ~10 s of CPU per solver
@@ -208,8 +211,9 @@ def time_solves(torch, budget_s: float):
                 "case": case, "solver": "omg" if solver == "omg" else "gmres-pmg",
                 "config": meta[solver], "dofs_raw": meta["dofs_raw"],
                 "dofs_agglomerated": lv.num_dofs, "iterations": rep.iterations,
-                "ref_iterations_envelope": [int(z[f"{solver}_envelope"].min()),
-                                            int(z[f"{solver}_envelope"].max())],
+                "ref_iterations_envelope": ([int(z[f"{solver}_envelope"].min()),
+                                             int(z[f"{solver}_envelope"].max())]
+                                            if f"{solver}_envelope" in z else None),
                 "converged": rep.converged, "solve_s": rep.time_iterations,
                 "dof_per_s": meta["dofs_raw"] / rep.time_iterations,
                 "ms_per_iteration": 1e3 * rep.time_iterations / max(rep.iterations, 1),
