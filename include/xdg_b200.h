@@ -128,19 +128,17 @@ int xdg_gemv_update2(int64_t L, int ncols, const double* W, const double* Z,
  * Replaces SuperLU solve (blockmatrix.py:224) for the low-order PMG systems
  * (solvers.py:249-251) and the coarsest-level direct solve (solvers.py:699).
  *
- * Batched: for s < nsys, n = dims[s] (0: skipped), INV + off[s], and
- * x + vec_off[s] = A_s^-1 (b[src[vec_off[s]+i]])_i -- pivot permutation
- * pre-composed with the gather.  One CTA per system; max_n = max dims
- * (2 max_n doubles of shared memory, max_n <= 12800). */
-int xdg_lu_inv_apply_batched(int nsys, const int64_t* off, const int* dims,
-                             const int64_t* vec_off, const double* INV,
-                             const int* src, const double* b, double* x,
-                             int max_n, xdg_stream_t stream);
-/* One large system over the whole GPU (warp per row, 3 launches);
- * scratch: 2 n doubles. */
-int xdg_lu_inv_apply_large(int n, const double* INV, const int* src,
-                           const double* b, double* x, double* scratch,
-                           xdg_stream_t stream);
+ * For s < nsys: n = dims[s], INV + off[s], and x + vec_off[s] receives
+ * A_s^-1 (b[src[vec_off[s]+i]])_i -- pivot permutation pre-composed with the
+ * gather.  Systems are packed back to back (vec_off[s+1] = vec_off[s] +
+ * dims[s]), total = sum of dims, row_sys[g] = system of packed row g.  All
+ * systems at once, warp per row over the whole GPU (3 launches: gather,
+ * L^-1 rows, U^-1 rows); scratch: 2 total doubles. */
+int xdg_lu_inv_apply(int nsys, int64_t total, const int* row_sys,
+                     const int64_t* off, const int* dims,
+                     const int64_t* vec_off, const double* INV, const int* src,
+                     const double* b, double* x, double* scratch,
+                     xdg_stream_t stream);
 /* LAPACK ipiv (1-based sequential swaps) -> permutation perm with
  * (P^T b)[i] = b[perm[i]], per system (setup). */
 int xdg_ipiv_to_perm(int nsys, const int* dims, const int64_t* vec_off,
@@ -192,17 +190,13 @@ typedef struct xdg_bsr {
   const double* val_t;
 } xdg_bsr;
 
-typedef struct xdg_large {     /* one large system: xdg_lu_inv_apply_large */
-  int32_t n, pad0;
-  int64_t off, vec_off;
-  double* scratch;             /* 2 n doubles */
-} xdg_large;
-
 typedef struct xdg_pmg {       /* PmgPlan of paper_2003_02431_b200/pmg.py */
-  int32_t nsys, nwork, N, m, has_high, direct, any_small, nlarge;
-  int32_t max_n_small, pad0;
+  int32_t nsys, nwork, N, m, has_high, direct;
+  int64_t total;               /* sum of the low-order system sizes */
+  const int* row_sys;
+  double* scratch;             /* 2 total doubles */
   const int64_t* lu_off;
-  const int* dims_small;
+  const int* dims;
   const int64_t* vec_off;
   const double* LU;            /* triangular-inverse factors (INV) */
   const int* src;
@@ -221,16 +215,16 @@ typedef struct xdg_pmg {       /* PmgPlan of paper_2003_02431_b200/pmg.py */
   const int* cptr;
   const int64_t* cpos;
   const double* damping;
-  const xdg_large* large;      /* HOST array of nlarge */
 } xdg_pmg;
 
 typedef struct xdg_direct {    /* dense LU of one system (coarsest level) */
-  int32_t n, large;            /* large: whole-GPU apply, else one CTA */
+  int32_t n, pad0;
   const double* LU;            /* triangular-inverse factors (INV) */
   const int* perm;
   const int64_t* zero_off;     /* device {0} */
   const int* dims;             /* device {n} */
-  double* scratch;             /* 2 n doubles (large) */
+  const int* row_sys;          /* device zeros[n] */
+  double* scratch;             /* 2 n doubles */
 } xdg_direct;
 
 typedef struct xdg_rm {        /* RmState (solvers.py:485-556) */

@@ -43,9 +43,7 @@ SIGNATURES = {
     "xdg_gemv_t": (_i32, [_i64, _i32, _vp, _i64, _vp, _vp, _vp, _vp]),
     "xdg_gemv_update2": (_i32, [_i64, _i32, _vp, _vp, _i64, _vp, _vp, _vp,
                                 _vp]),
-    "xdg_lu_inv_apply_batched": (_i32, [_i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
-                                        _i32, _vp]),
-    "xdg_lu_inv_apply_large": (_i32, [_i32, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "xdg_lu_inv_apply": (_i32, [_i32, _i64] + [_vp] * 10),
     "xdg_ipiv_to_perm": (_i32, [_i32, _vp, _vp, _vp, _vp, _vp]),
     "xdg_pmg_build_low": (_i32, [_i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp,
                                  _vp, _vp, _vp, _vp, _vp]),

@@ -60,7 +60,6 @@ extern "C" int xdg_ipiv_to_perm(int nsys, const int* dims,
 namespace xdg {
 namespace {
 
-constexpr int kIT = 512;  // threads per CTA (16 warps)
 
 template <bool LOWER>
 __device__ __forceinline__ double tri_row_dot(const double* __restrict__ row,
@@ -92,101 +91,58 @@ __device__ __forceinline__ double tri_row_dot(const double* __restrict__ row,
   return warp_sum((a0 + a1) + (a2 + a3));
 }
 
-// one CTA per system, vectors staged in shared memory (2 n doubles)
-__global__ void __launch_bounds__(kIT)
-inv_apply_batched_kernel(const int64_t* __restrict__ off,
-                         const int* __restrict__ dims,
-                         const int64_t* __restrict__ vec_off,
-                         const double* __restrict__ INV,
-                         const int* __restrict__ src,
-                         const double* __restrict__ b, double* __restrict__ xout) {
-  extern __shared__ double sm[];
-  const int s = blockIdx.x;
-  const int n = dims[s];
-  if (n == 0) return;
-  const double* A = INV + off[s];
-  const int* sidx = src + vec_off[s];
-  double* x = xout + vec_off[s];
-  double* t = sm;       // P^T b
-  double* y = sm + n;   // L^-1 t
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  constexpr int nw = kIT / 32;
-  for (int i = threadIdx.x; i < n; i += kIT) t[i] = b[sidx[i]];
-  __syncthreads();
-  for (int i = warp; i < n; i += nw) {
-    const double d = tri_row_dot<true>(A + (int64_t)i * n, t, i, n, lane);
-    if (lane == 0) y[i] = __dadd_rn(t[i], d);
-  }
-  __syncthreads();
-  for (int i = warp; i < n; i += nw) {
-    const double d = tri_row_dot<false>(A + (int64_t)i * n, y, i, n, lane);
-    if (lane == 0) x[i] = d;
-  }
-}
-
-// one large system: warp per row over the whole GPU, rows interleaved so
-// long and short triangle rows mix on every SM
+// All systems at once, warp per row over the whole GPU.  Global row g of
+// the batch belongs to system row_sys[g] (rows of a system are contiguous,
+// starting at vec_off[s]); rows are visited in an interleaved order so long
+// and short triangle rows mix on every SM.
 __global__ void __launch_bounds__(256)
-gather_kernel(int n, const int* __restrict__ src, const double* __restrict__ b,
-              double* __restrict__ t) {
-  for (int i = blockIdx.x * 256 + threadIdx.x; i < n; i += gridDim.x * 256)
+gather_kernel(int64_t total, const int* __restrict__ src,
+              const double* __restrict__ b, double* __restrict__ t) {
+  for (int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * 256)
     t[i] = b[src[i]];
 }
 
 template <bool LOWER>
 __global__ void __launch_bounds__(256)
-inv_apply_rows_kernel(int n, const double* __restrict__ A,
-                      const double* __restrict__ v, double* __restrict__ out) {
+inv_rows_kernel(int64_t total, const int* __restrict__ row_sys,
+                const int64_t* __restrict__ off, const int* __restrict__ dims,
+                const int64_t* __restrict__ vec_off, const double* __restrict__ INV,
+                const double* __restrict__ v, double* __restrict__ out) {
   const int lane = threadIdx.x & 31;
-  const int nw = gridDim.x * 8;
-  for (int w = blockIdx.x * 8 + (threadIdx.x >> 5); w < n; w += nw) {
-    // pair long and short rows: w -> rows alternate from both ends
-    const int i = (w & 1) ? n - 1 - (w >> 1) : (w >> 1);
-    const double d = tri_row_dot<LOWER>(A + (int64_t)i * n, v, i, n, lane);
-    if (lane == 0) out[i] = LOWER ? __dadd_rn(v[i], d) : d;
+  const int64_t nw = (int64_t)gridDim.x * 8;
+  for (int64_t w = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); w < total; w += nw) {
+    const int64_t g = (w & 1) ? total - 1 - (w >> 1) : (w >> 1);
+    const int s = row_sys[g];
+    const int64_t base = vec_off[s];
+    const int n = dims[s];
+    const int i = (int)(g - base);
+    const double* vs = v + base;
+    const double d = tri_row_dot<LOWER>(INV + off[s] + (int64_t)i * n, vs, i, n, lane);
+    if (lane == 0) out[g] = LOWER ? __dadd_rn(vs[i], d) : d;
   }
 }
 
 }  // namespace
 }  // namespace xdg
 
-extern "C" int xdg_lu_inv_apply_batched(int nsys, const int64_t* off,
-                                        const int* dims, const int64_t* vec_off,
-                                        const double* INV, const int* src,
-                                        const double* b, double* x,
-                                        int max_n, xdg_stream_t stream) {
+extern "C" int xdg_lu_inv_apply(int nsys, int64_t total, const int* row_sys,
+                                const int64_t* off, const int* dims,
+                                const int64_t* vec_off, const double* INV,
+                                const int* src, const double* b, double* x,
+                                double* scratch, xdg_stream_t stream) {
   using namespace xdg;
-  if (nsys <= 0) return XDG_OK;
-  const size_t smem = (size_t)2 * max_n * sizeof(double);
-  XDG_REQUIRE(smem <= 200 * 1024, XDG_ERR_ARG,
-              "batched inverse apply: system of %d unknowns exceeds shared memory", max_n);
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  static thread_local bool attr = false;
-  if (!attr) {
-    XDG_TRY_CUDA(cudaFuncSetAttribute(inv_apply_batched_kernel,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      200 * 1024));
-    attr = true;
-  }
-  inv_apply_batched_kernel<<<nsys, kIT, smem, s>>>(off, dims, vec_off, INV, src, b, x);
-  XDG_CHECK_LAUNCH();
-  return XDG_OK;
-}
-
-extern "C" int xdg_lu_inv_apply_large(int n, const double* INV, const int* src,
-                                      const double* b, double* x,
-                                      double* scratch, xdg_stream_t stream) {
-  using namespace xdg;
-  if (n <= 0) return XDG_OK;
+  XDG_REQUIRE(nsys >= 0 && total >= 0, XDG_ERR_ARG, "bad batch");
+  if (nsys == 0 || total == 0) return XDG_OK;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   double* t = scratch;
-  double* y = scratch + n;
-  gather_kernel<<<grid_for(n, 256, 4), 256, 0, s>>>(n, src, b, t);
+  double* y = scratch + total;
+  gather_kernel<<<grid_for(total, 256, 4), 256, 0, s>>>(total, src, b, t);
   XDG_CHECK_LAUNCH();
-  const int g = resident_grid(inv_apply_rows_kernel<true>, 256, 0, (int64_t)n * 32);
-  inv_apply_rows_kernel<true><<<g, 256, 0, s>>>(n, INV, t, y);
+  const int g = resident_grid(inv_rows_kernel<true>, 256, 0, total * 32);
+  inv_rows_kernel<true><<<g, 256, 0, s>>>(total, row_sys, off, dims, vec_off, INV, t, y);
   XDG_CHECK_LAUNCH();
-  inv_apply_rows_kernel<false><<<g, 256, 0, s>>>(n, INV, y, x);
+  inv_rows_kernel<false><<<g, 256, 0, s>>>(total, row_sys, off, dims, vec_off, INV, y, x);
   XDG_CHECK_LAUNCH();
   return XDG_OK;
 }

@@ -164,15 +164,8 @@ static int pmg_apply_op(const xdg_pmg* P, const xdg_bsr* M, const double* b,
                         double* z, cudaStream_t s) {
   xdg_stream_t st = reinterpret_cast<xdg_stream_t>(s);
   double* xlo = (P->direct && !P->has_high) ? z : P->xlo;
-  if (P->any_small)
-    XDG_TRY(xdg_lu_inv_apply_batched(P->nsys, P->lu_off, P->dims_small,
-                                     P->vec_off, P->LU, P->src, b, xlo,
-                                     P->max_n_small, st));
-  for (int k = 0; k < P->nlarge; ++k) {
-    const xdg_large& q = P->large[k];
-    XDG_TRY(xdg_lu_inv_apply_large(q.n, P->LU + q.off, P->src + q.vec_off, b,
-                                   xlo + q.vec_off, q.scratch, st));
-  }
+  XDG_TRY(xdg_lu_inv_apply(P->nsys, P->total, P->row_sys, P->lu_off, P->dims,
+                           P->vec_off, P->LU, P->src, b, xlo, P->scratch, st));
   if (P->has_high) {
     double* out = P->direct ? z : P->out;
     XDG_TRY(xdg_pmg_high(P->nwork, P->N, P->m, P->wi_ptr, P->wi_blk, P->wi_lcol,
@@ -306,11 +299,8 @@ int omg_level(OmgRun& R, int lam, const double* b, double* x, int has_x0,
   const int64_t n = (int64_t)lv.M.nbr * lv.M.N;
   if (lam == R.nlevels - 1 || !lv.has_restriction) {           // solvers.py:698-710
     const xdg_direct& D = lv.direct;
-    if (D.large)
-      XDG_TRY(xdg_lu_inv_apply_large(D.n, D.LU, D.perm, b, x, D.scratch, st));
-    else
-      XDG_TRY(xdg_lu_inv_apply_batched(1, D.zero_off, D.dims, D.zero_off, D.LU,
-                                       D.perm, b, x, D.n, st));
+    XDG_TRY(xdg_lu_inv_apply(1, D.n, D.row_sys, D.zero_off, D.dims, D.zero_off,
+                             D.LU, D.perm, b, x, D.scratch, st));
     if (lam == R.entry) {
       XDG_TRY(spmv(&lv.M, x, rm.r, b, rm.sc + 6, rm.ws, R.s));
       double v;

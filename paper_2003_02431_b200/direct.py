@@ -68,10 +68,6 @@ def dense_from_device_bsr(D) -> torch.Tensor:
     return A.view(n, n)
 
 
-SMEM_MAX_N = 12800   # one-CTA batched apply keeps 2 n doubles in smem
-LARGE_MIN_N = 512    # a lone system this large is applied over the whole GPU
-
-
 def triangular_inverses(LU: torch.Tensor, chunk_bytes: int = 2 << 30) -> torch.Tensor:
     """INV of a packed LU (n, n) or batch (b, n, n): L^-1 strictly below the
     diagonal (unit diagonal implicit), U^-1 on and above it (setup; the
@@ -95,26 +91,21 @@ def triangular_inverses(LU: torch.Tensor, chunk_bytes: int = 2 << 30) -> torch.T
 class DeviceDirect:
     """Device-side factor of one dense system: apply(b_dev) -> x_dev."""
 
-    def __init__(self, A: torch.Tensor, ctx, what="matrix", large=None):
+    def __init__(self, A: torch.Tensor, ctx, what="matrix"):
         n = A.shape[0]
         self.n = n
         self.ctx = ctx
         dev = ctx.device
         if n == 0:
             self.INV = torch.zeros(0, dtype=F64, device=dev)
-            self.large = False
             return
         LU, piv = lu_factor_dense(A, what)
         self.INV = triangular_inverses(LU).contiguous()
         del LU
         self.lu_off = torch.zeros(1, dtype=torch.int64, device=dev)
-        self.vec_off = torch.zeros(1, dtype=torch.int64, device=dev)
         self.dims = torch.tensor([n], dtype=I32, device=dev)
-        self.perm = ipiv_to_perm(ctx, piv.to(I32).contiguous(), self.dims,
-                                 self.vec_off)
-        self.large = (n >= LARGE_MIN_N or n > SMEM_MAX_N) if large is None else bool(large)
-        if n > SMEM_MAX_N:
-            self.large = True
+        self.perm = ipiv_to_perm(ctx, piv.to(I32).contiguous(), self.dims, self.lu_off)
+        self.row_sys = torch.zeros(n, dtype=I32, device=dev)
         self.scratch = torch.empty(2 * n, dtype=F64, device=dev)
 
     def apply(self, b: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
@@ -122,16 +113,11 @@ class DeviceDirect:
             out = torch.empty(self.n, dtype=F64, device=b.device)
         if self.n == 0:
             return out
-        if self.large:
-            nat.check(self.ctx.lib.xdg_lu_inv_apply_large(
-                self.n, self.INV.data_ptr(), self.perm.data_ptr(), b.data_ptr(),
-                out.data_ptr(), self.scratch.data_ptr(), self.ctx.stream),
-                "lu_inv_apply_large")
-            return out
-        nat.check(self.ctx.lib.xdg_lu_inv_apply_batched(
-            1, self.lu_off.data_ptr(), self.dims.data_ptr(), self.vec_off.data_ptr(),
-            self.INV.data_ptr(), self.perm.data_ptr(), b.data_ptr(), out.data_ptr(),
-            self.n, self.ctx.stream), "lu_inv_apply")
+        nat.check(self.ctx.lib.xdg_lu_inv_apply(
+            1, self.n, self.row_sys.data_ptr(), self.lu_off.data_ptr(),
+            self.dims.data_ptr(), self.lu_off.data_ptr(), self.INV.data_ptr(),
+            self.perm.data_ptr(), b.data_ptr(), out.data_ptr(),
+            self.scratch.data_ptr(), self.ctx.stream), "lu_inv_apply")
         return out
 
 

@@ -24,24 +24,19 @@ class XdgBsr(C.Structure):
                 ("col", _vp), ("val_t", _vp)]
 
 
-class XdgLarge(C.Structure):
-    _fields_ = [("n", C.c_int32), ("pad0", C.c_int32), ("off", C.c_int64),
-                ("vec_off", C.c_int64), ("scratch", _vp)]
-
-
 class XdgPmg(C.Structure):
     _fields_ = [(f, C.c_int32) for f in ("nsys", "nwork", "N", "m", "has_high",
-                                         "direct", "any_small", "nlarge",
-                                         "max_n_small", "pad0")] + \
-        [(f, _vp) for f in ("lu_off", "dims_small", "vec_off", "LU", "src", "xlo",
+                                         "direct")] + [("total", C.c_int64)] + \
+        [(f, _vp) for f in ("row_sys", "scratch", "lu_off", "dims", "vec_off", "LU",
+                            "src", "xlo",
                             "wi_ptr", "wi_blk", "wi_lcol", "wi_cell", "wi_lrow",
                             "wi_xlo", "wi_hidx", "wi_out", "HLU", "hperm", "out",
-                            "cptr", "cpos", "damping", "large")]
+                            "cptr", "cpos", "damping")]
 
 
 class XdgDirect(C.Structure):
-    _fields_ = [("n", C.c_int32), ("large", C.c_int32), ("LU", _vp), ("perm", _vp),
-                ("zero_off", _vp), ("dims", _vp), ("scratch", _vp)]
+    _fields_ = [("n", C.c_int32), ("pad0", C.c_int32), ("LU", _vp), ("perm", _vp),
+                ("zero_off", _vp), ("dims", _vp), ("row_sys", _vp), ("scratch", _vp)]
 
 
 class XdgRm(C.Structure):
@@ -69,25 +64,13 @@ def bsr_struct(D) -> XdgBsr:
                   D.col.data_ptr(), D.val_t.data_ptr())
 
 
-def large_structs(items):
-    """items: list of (n, off, vec_off, scratch) -> (ctypes array, count)."""
-    if not items:
-        return None, 0
-    arr = (XdgLarge * len(items))()
-    for i, (n, off, vo, scratch) in enumerate(items):
-        arr[i] = XdgLarge(n, 0, off, vo, scratch.data_ptr())
-    return arr, len(items)
-
-
 def pmg_struct(plan):
     """(XdgPmg, keepalive) for a pmg.PmgPlan."""
-    large, nlarge = large_structs(plan.large)
     s = XdgPmg()
     s.nsys, s.nwork, s.N, s.m = plan.nsys, plan.nwork, plan.N, plan.m
-    s.has_high, s.direct, s.any_small, s.nlarge = (int(plan.has_high), int(plan.direct),
-                                                   int(plan.any_small), nlarge)
-    s.max_n_small = plan.max_n_small
-    s.lu_off, s.dims_small, s.vec_off = _p(plan.lu_off), _p(plan.dims_small), _p(plan.vec_off)
+    s.has_high, s.direct, s.total = int(plan.has_high), int(plan.direct), plan.total
+    s.row_sys, s.scratch = _p(plan.row_sys), _p(plan.lu_scratch)
+    s.lu_off, s.dims, s.vec_off = _p(plan.lu_off), _p(plan.dims), _p(plan.vec_off)
     s.LU, s.src, s.xlo = _p(plan.LU), _p(plan.src), _p(plan.xlo)
     for f in ("wi_ptr", "wi_blk", "wi_lcol", "wi_cell", "wi_lrow"):
         setattr(s, f, _p(getattr(plan, f)))
@@ -98,8 +81,7 @@ def pmg_struct(plan):
     if not plan.direct:
         s.out, s.cptr, s.cpos = _p(plan.out), _p(plan.cptr), _p(plan.cpos)
         s.damping = _p(plan.damping)
-    s.large = C.cast(large, _vp) if large is not None else None
-    return s, [large]
+    return s, []
 
 
 def direct_struct(dd):
@@ -107,10 +89,9 @@ def direct_struct(dd):
     s = XdgDirect()
     s.n = dd.n
     if dd.n:
-        s.large = int(dd.large)
         s.LU, s.perm = _p(dd.INV), _p(dd.perm)
         s.zero_off, s.dims = _p(dd.lu_off), _p(dd.dims)
-        s.scratch = _p(dd.scratch)
+        s.row_sys, s.scratch = _p(dd.row_sys), _p(dd.scratch)
     return s, []
 
 

@@ -21,8 +21,7 @@ import numpy as np
 import torch
 
 from . import _native as nat
-from .direct import (LARGE_MIN_N, SMEM_MAX_N, ipiv_to_perm, lu_factor_dense,
-                     triangular_inverses)
+from .direct import ipiv_to_perm, lu_factor_dense, triangular_inverses
 from .errors import SingularSystemError
 
 F64 = torch.float64
@@ -141,19 +140,10 @@ class PmgPlan:
         base = torch.from_numpy(np.repeat(vec_off[:-1], dims)).to(dev)
         # perm is local to each system: global position = base + local index
         self.src = gidx[base + perm].to(I32) if perm.numel() else perm.to(I32)
-        # a few large systems: whole-GPU apply each; the batched one-CTA
-        # kernel (which fills the GPU when there are many systems) skips them
-        self.large = []
-        small = dims.copy()
-        for s_ in range(self.nsys):
-            n = int(dims[s_])
-            if n > SMEM_MAX_N or (self.nsys <= 4 and n >= LARGE_MIN_N):
-                scratch = torch.empty(2 * n, dtype=F64, device=dev)
-                self.large.append((n, int(lu_off[s_]), int(vec_off[s_]), scratch))
-                small[s_] = 0
-        self.dims_small = up(small, I32)
-        self.max_n_small = int(small.max()) if len(small) else 0
-        self.any_small = bool(np.any(small > 0))
+        # packed-row -> system map for the warp-per-row inverse apply
+        self.total = int(vec_off[-1])
+        self.row_sys = up(np.repeat(np.arange(self.nsys), dims), I32)
+        self.lu_scratch = torch.empty(2 * max(self.total, 1), dtype=F64, device=dev)
 
         # ---- high-order per-cell factors (solvers.py:225-243) ------------
         self.has_high = self.m < N
