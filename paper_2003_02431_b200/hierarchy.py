@@ -95,6 +95,18 @@ def _graph(ptr: np.ndarray, adj: np.ndarray) -> MeshGraph:
     return MeshGraph(num_cells=n, edges=edges, adjacency=adjacency)
 
 
+def fixture_array(z, key: str) -> np.ndarray:
+    """z[key], reassembling block arrays stored deduplicated
+    (key__uniq[key__idx], tests/golden/dedup_fixture.py)."""
+    if key in z.files:
+        return z[key]
+    return z[key + "__uniq"][z[key + "__idx"]]
+
+
+def fixture_has(z, key: str) -> bool:
+    return key in z.files or (key + "__uniq") in z.files
+
+
 def load_hierarchy(path_or_npz, num_levels: Optional[int] = None) -> MultigridHierarchy:
     """Rebuild a hierarchy from a fixture written by make_golden.py."""
     z = np.load(path_or_npz) if isinstance(path_or_npz, str) else path_or_npz
@@ -105,15 +117,16 @@ def load_hierarchy(path_or_npz, num_levels: Optional[int] = None) -> MultigridHi
     for lam in range(1, L + 1):
         p = f"L{lam}_"
         N = int(z[p + "N"])
-        rp, col, val = z[p + "row_ptr"], z[p + "col"], z[p + "val"]
+        rp, col, val = z[p + "row_ptr"], z[p + "col"], fixture_array(z, p + "val")
         nb = len(rp) - 1
         lay = uniform_layout(nb, N)
         M = BlockSparseMatrix.from_bsr(rp, col, val, lay, lay)
         R = None
-        if lam < L and (p + "R_row_ptr") in z:
+        if lam < L and (p + "R_row_ptr") in z.files:
             nc = int(z[p + "R_ncols"])
             R = BlockSparseMatrix.from_bsr(z[p + "R_row_ptr"], z[p + "R_col"],
-                                           z[p + "R_val"], lay, uniform_layout(nc, N))
+                                           fixture_array(z, p + "R_val"), lay,
+                                           uniform_layout(nc, N))
         info = LevelInfo(basis=_Basis(int(z[p + "degree"]), dim), num_blocks=nb)
         levels.append(HierarchyLevel(data=info, matrix=M, rhs=np.array(z[p + "rhs"]),
                                      restriction=R,
