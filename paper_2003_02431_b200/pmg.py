@@ -102,6 +102,13 @@ class PmgPlan:
         self.xlo = torch.zeros(int(vec_off[-1]), dtype=F64, device=dev)
 
         # ---- low-order dense factors (solvers.py:208-221) ----------------
+        need = 8 * int(lu_off[-1])
+        free, _ = torch.cuda.mem_get_info(dev)
+        if 3 * need > free:  # factor + LU + inverse temporaries
+            raise NotImplementedError(
+                f"dense low-order factors need {need / 1e9:.1f} GB (largest system "
+                f"{int(dims.max())} unknowns; {free / 1e9:.0f} GB free): the sparse "
+                "low-order factorisation is not implemented yet (DESIGN.md section 7)")
         A = torch.zeros(int(lu_off[-1]), dtype=F64, device=dev)
         nat.check(ctx.lib.xdg_pmg_build_low(
             self.nwork, N, self.m, self.wi_ptr.data_ptr(),
