@@ -112,11 +112,14 @@ int xdg_div(int64_t n, const double* x, const double* d, double* y,
 int64_t xdg_gemv_t_workspace_bytes(int ncols);
 int xdg_gemv_t(int64_t L, int ncols, const double* W, int64_t ldw,
                const double* w, double* coeff, void* ws, xdg_stream_t stream);
-/* w -= W coeff ; z -= Z coeff  (Z may be NULL): the fused update pair of
- * the classical Gram-Schmidt pass, solvers.py:591-592. */
+/* w -= W coeff ; z -= Z coeff_z (coeff_z NULL: coeff; Z may be NULL): the
+ * update pair of a classical Gram-Schmidt pass, solvers.py:591-592. */
 int xdg_gemv_update2(int64_t L, int ncols, const double* W, const double* Z,
-                     int64_t ld, const double* coeff, double* w, double* z,
-                     xdg_stream_t stream);
+                     int64_t ld, const double* coeff, const double* coeff_z,
+                     double* w, double* z, xdg_stream_t stream);
+/* out = a + b for short device vectors (coefficient sums). */
+int xdg_add_small(int n, const double* a, const double* b, double* out,
+                  xdg_stream_t stream);
 
 
 /* ---- dense LU solves (batched, variable size) --------------------------- */
@@ -240,7 +243,7 @@ typedef struct xdg_rm {        /* RmState (solvers.py:485-556) */
   double* My;
   double* My_new;              /* swapped with My on accept */
   double* Mz;
-  double* coeff;               /* [max_columns] */
+  double* coeff;               /* [3 * max_columns]: c1, c2, c1 + c2 */
   double* sc;                  /* >= 8 device scalars */
   double* alpha_host;          /* HOST [max_columns] */
   double* x;                   /* current() outputs */

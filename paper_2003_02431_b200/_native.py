@@ -41,8 +41,9 @@ SIGNATURES = {
     "xdg_div": (_i32, [_i64, _vp, _vp, _vp, _vp]),
     "xdg_gemv_t_workspace_bytes": (_i64, [_i32]),
     "xdg_gemv_t": (_i32, [_i64, _i32, _vp, _i64, _vp, _vp, _vp, _vp]),
-    "xdg_gemv_update2": (_i32, [_i64, _i32, _vp, _vp, _i64, _vp, _vp, _vp,
+    "xdg_gemv_update2": (_i32, [_i64, _i32, _vp, _vp, _i64, _vp, _vp, _vp, _vp,
                                 _vp]),
+    "xdg_add_small": (_i32, [_i32, _vp, _vp, _vp, _vp]),
     "xdg_lu_inv_apply": (_i32, [_i32, _i64] + [_vp] * 10),
     "xdg_ipiv_to_perm": (_i32, [_i32, _vp, _vp, _vp, _vp, _vp]),
     "xdg_pmg_build_low": (_i32, [_i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp,

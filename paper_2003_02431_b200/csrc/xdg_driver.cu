@@ -237,10 +237,19 @@ extern "C" int xdg_rm_step(xdg_rm* rm, const xdg_bsr* M, const double* zc,
   double* sc = rm->sc;
   XDG_TRY(spmv(M, z, w, nullptr, sc + 0, rm->ws, s));          // w = M z
   if (col > 0) {
-    for (int pass = 0; pass < 2; ++pass) {                    // CGS x2
-      XDG_TRY(xdg_gemv_t(n, col, rm->W, n, w, rm->coeff, rm->gemv_ws, stream));
-      XDG_TRY(xdg_gemv_update2(n, col, rm->W, rm->Z, n, rm->coeff, w, z, stream));
-    }
+    // two classical Gram-Schmidt passes (solvers.py:589-592).  The two z
+    // updates are merged into z -= Z (c1 + c2): one pass over Z instead of
+    // two (a roundoff-level reassociation of (z - Z c1) - Z c2); w is
+    // updated exactly as in the reference.
+    double* c1 = rm->coeff;
+    double* c2 = rm->coeff + rm->max_columns;
+    double* cs = rm->coeff + 2 * (int64_t)rm->max_columns;
+    XDG_TRY(xdg_gemv_t(n, col, rm->W, n, w, c1, rm->gemv_ws, stream));
+    XDG_TRY(xdg_gemv_update2(n, col, rm->W, nullptr, n, c1, nullptr, w, nullptr,
+                             stream));
+    XDG_TRY(xdg_gemv_t(n, col, rm->W, n, w, c2, rm->gemv_ws, stream));
+    XDG_TRY(xdg_add_small(col, c1, c2, cs, stream));
+    XDG_TRY(xdg_gemv_update2(n, col, rm->W, rm->Z, n, c2, cs, w, z, stream));
   }
   XDG_TRY(xdg_dot(n, w, w, sc + 1, rm->ws, stream));          // ||w||^2
   // speculative tail (discarded when the candidate is dependent)
@@ -463,7 +472,8 @@ extern "C" int xdg_gmres_solve(const xdg_bsr* M, const xdg_pmg* pmg,
     for (int i = 0; i < j; ++i) y[i] = -y[i];                     // x -= Z (-y)
     XDG_TRY_CUDA(cudaMemcpyAsync(ycoef, y.data(), sizeof(double) * j,
                                  cudaMemcpyHostToDevice, s));
-    XDG_TRY(xdg_gemv_update2(n, j, Zb, nullptr, n, ycoef, x, nullptr, stream));
+    XDG_TRY(xdg_gemv_update2(n, j, Zb, nullptr, n, ycoef, nullptr, x, nullptr,
+                             stream));
     XDG_TRY(spmv(M, x, r, b, sc, ws, s));
     XDG_TRY_CUDA(sync_read(&v, sc, 1, s));
     beta = sqrt(v);

@@ -124,43 +124,50 @@ div_kernel(int64_t n, const double* __restrict__ x,
     y[i] = __ddiv_rn(x[i], d[i]);
 }
 
-// ---- W^T w over up to kCols columns per pass ------------------------------
-// Each CTA streams a contiguous slice of the L rows; per column it forms a
-// partial dot with a fixed shuffle tree and writes partial[c][cta].  A
-// second, tiny kernel sums the partials per column in CTA order.
-constexpr int kCols = 8;
+// ---- W^T w -------------------------------------------------------------------
+// Each CTA owns a tile of kTile rows: w's tile is staged in shared memory,
+// warp j handles columns j, j+8, ...; for a column every lane issues
+// kTile/32 independent coalesced loads, reduces them in a fixed order and
+// the warp tree writes partial[c][tile].  gemv_t_final sums the tile
+// partials per column in tile order (deterministic).
+constexpr int kTile = 1024;
+constexpr int kMaxTiles = 4096;
 
 __global__ void __launch_bounds__(kT)
 gemv_t_partial(int64_t L, int ncols, const double* __restrict__ W, int64_t ldw,
                const double* __restrict__ w, double* __restrict__ partial) {
-  const int64_t per = (L + gridDim.x - 1) / gridDim.x;
-  const int64_t lo = (int64_t)blockIdx.x * per;
-  const int64_t hi = lo + per < L ? lo + per : L;
-  __shared__ double red[kCols][kT / 32];
-  for (int c0 = 0; c0 < ncols; c0 += kCols) {
-    double acc[kCols];
-#pragma unroll
-    for (int q = 0; q < kCols; ++q) acc[q] = 0.0;
-    for (int64_t i = lo + threadIdx.x; i < hi; i += kT) {
-      const double wi = __ldg(w + i);
-#pragma unroll
-      for (int q = 0; q < kCols; ++q)
-        if (c0 + q < ncols)
-          acc[q] = fma(__ldg(W + (int64_t)(c0 + q) * ldw + i), wi, acc[q]);
-    }
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-    for (int q = 0; q < kCols; ++q) {
-      const double v = warp_sum(acc[q]);
-      if (lane == 0) red[q][warp] = v;
-    }
+  __shared__ double ws[kTile];
+  const int ntiles = gridDim.x;
+  const int64_t rows_per = ((L + ntiles - 1) / ntiles + 31) / 32 * 32;
+  const int64_t lo = (int64_t)blockIdx.x * rows_per;
+  const int64_t hi = lo + rows_per < L ? lo + rows_per : L;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int64_t t0 = lo; t0 < hi; t0 += kTile) {
+    const int len = (int)((hi - t0) < kTile ? (hi - t0) : kTile);
     __syncthreads();
-    if (threadIdx.x < kCols && c0 + (int)threadIdx.x < ncols) {
-      double s = 0.0;
-      for (int q = 0; q < kT / 32; ++q) s += red[threadIdx.x][q];
-      partial[(int64_t)(c0 + threadIdx.x) * gridDim.x + blockIdx.x] = s;
-    }
+    for (int i = threadIdx.x; i < kTile; i += kT) ws[i] = i < len ? w[t0 + i] : 0.0;
     __syncthreads();
+    for (int c = warp; c < ncols; c += kT / 32) {
+      const double* Wc = W + (int64_t)c * ldw + t0;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      if (len == kTile) {
+#pragma unroll 8
+        for (int k = 0; k < kTile / 32; k += 4) {
+          const int i = lane + 32 * k;
+          a0 = fma(__ldg(Wc + i), ws[i], a0);
+          a1 = fma(__ldg(Wc + i + 32), ws[i + 32], a1);
+          a2 = fma(__ldg(Wc + i + 64), ws[i + 64], a2);
+          a3 = fma(__ldg(Wc + i + 96), ws[i + 96], a3);
+        }
+      } else {
+        for (int i = lane; i < len; i += 32) a0 = fma(__ldg(Wc + i), ws[i], a0);
+      }
+      const double v = warp_sum((a0 + a1) + (a2 + a3));
+      if (lane == 0) {
+        double* pc = partial + (int64_t)c * ntiles + blockIdx.x;
+        *pc = (t0 == lo) ? v : *pc + v;
+      }
+    }
   }
 }
 
@@ -177,29 +184,58 @@ __global__ void gemv_t_final(int ncols, int nparts,
   if (lane == 0) coeff[c] = s;
 }
 
-// w -= W coeff ; z -= Z coeff.  Per element the column sum is formed in
-// column order, then subtracted (numpy: tmp = W @ coeff; w -= tmp).
+// w -= W cw ; z -= Z cz.  Per element the column sum is formed in column
+// order (4 columns' loads issued together), then subtracted
+// (numpy: tmp = W @ coeff; w -= tmp).
 __global__ void __launch_bounds__(kT)
 gemv_update2_kernel(int64_t L, int ncols, const double* __restrict__ W,
                     const double* __restrict__ Z, int64_t ld,
-                    const double* __restrict__ coeff, double* __restrict__ w,
-                    double* __restrict__ z) {
+                    const double* __restrict__ cw, const double* __restrict__ cz,
+                    double* __restrict__ w, double* __restrict__ z) {
   extern __shared__ double sc[];
-  for (int c = threadIdx.x; c < ncols; c += kT) sc[c] = coeff[c];
+  double* scw = sc;
+  double* scz = sc + ncols;
+  for (int c = threadIdx.x; c < ncols; c += kT) {
+    scw[c] = cw[c];
+    scz[c] = cz[c];
+  }
   __syncthreads();
   const int64_t stride = (int64_t)gridDim.x * kT;
   for (int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x; i < L; i += stride) {
     double tw = 0.0, tz = 0.0;
-    for (int c = 0; c < ncols; ++c) {
-      tw = fma(__ldg(W + (int64_t)c * ld + i), sc[c], tw);
-      if (Z) tz = fma(__ldg(Z + (int64_t)c * ld + i), sc[c], tz);
+    int c = 0;
+    for (; c + 4 <= ncols; c += 4) {
+      double a[4], b[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a[u] = __ldg(W + (int64_t)(c + u) * ld + i);
+        b[u] = Z ? __ldg(Z + (int64_t)(c + u) * ld + i) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        tw = fma(a[u], scw[c + u], tw);
+        if (Z) tz = fma(b[u], scz[c + u], tz);
+      }
+    }
+    for (; c < ncols; ++c) {
+      tw = fma(__ldg(W + (int64_t)c * ld + i), scw[c], tw);
+      if (Z) tz = fma(__ldg(Z + (int64_t)c * ld + i), scz[c], tz);
     }
     w[i] = __dadd_rn(w[i], -tw);
     if (Z) z[i] = __dadd_rn(z[i], -tz);
   }
 }
 
-int gemv_t_parts() { return sm_count() * 2; }
+__global__ void add_small_kernel(int n, const double* a, const double* b, double* out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out[i] = a[i] + b[i];
+}
+
+int gemv_t_parts(int64_t L) {
+  int64_t t = (L + kTile - 1) / kTile;
+  if (t > kMaxTiles) t = kMaxTiles;
+  return t < 1 ? 1 : (int)t;
+}
 
 }  // namespace
 }  // namespace xdg
@@ -284,7 +320,7 @@ extern "C" int xdg_div(int64_t n, const double* x, const double* d, double* y,
 }
 
 extern "C" int64_t xdg_gemv_t_workspace_bytes(int ncols) {
-  return 8 * (int64_t)(ncols > 0 ? ncols : 1) * gemv_t_parts();
+  return 8 * (int64_t)(ncols > 0 ? ncols : 1) * kMaxTiles;
 }
 
 extern "C" int xdg_gemv_t(int64_t L, int ncols, const double* W, int64_t ldw,
@@ -295,9 +331,7 @@ extern "C" int xdg_gemv_t(int64_t L, int ncols, const double* W, int64_t ldw,
               (long long)ldw);
   if (ncols == 0) return XDG_OK;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  int parts = gemv_t_parts();
-  if (L < (int64_t)parts * kT) parts = (int)((L + kT - 1) / kT);
-  if (parts < 1) parts = 1;
+  const int parts = gemv_t_parts(L);
   double* partial = static_cast<double*>(ws);
   gemv_t_partial<<<parts, kT, 0, s>>>(L, ncols, W, ldw, w, partial);
   XDG_CHECK_LAUNCH();
@@ -308,16 +342,30 @@ extern "C" int xdg_gemv_t(int64_t L, int ncols, const double* W, int64_t ldw,
 
 extern "C" int xdg_gemv_update2(int64_t L, int ncols, const double* W,
                                 const double* Z, int64_t ld,
-                                const double* coeff, double* w, double* z,
-                                xdg_stream_t stream) {
+                                const double* coeff, const double* coeff_z,
+                                double* w, double* z, xdg_stream_t stream) {
   XDG_REQUIRE(L >= 0 && ncols >= 0 && ld >= L, XDG_ERR_ARG,
               "gemv_update2: bad shape");
   if (ncols == 0 || L == 0) return XDG_OK;
   XDG_REQUIRE(ncols <= 6000, XDG_ERR_ARG, "gemv_update2: ncols %d too large",
               ncols);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  gemv_update2_kernel<<<grid_for(L, kT, kPerSm), kT, ncols * sizeof(double),
-                        s>>>(L, ncols, W, Z, ld, coeff, w, z);
+  const size_t smem = 2 * ncols * sizeof(double);
+  if (smem > 48 * 1024)
+    XDG_TRY_CUDA(cudaFuncSetAttribute(gemv_update2_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+  gemv_update2_kernel<<<grid_for(L, kT, kPerSm), kT, smem, s>>>(
+      L, ncols, W, Z, ld, coeff, coeff_z ? coeff_z : coeff, w, z);
+  XDG_CHECK_LAUNCH();
+  return XDG_OK;
+}
+
+extern "C" int xdg_add_small(int n, const double* a, const double* b,
+                             double* out, xdg_stream_t stream) {
+  if (n <= 0) return XDG_OK;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  add_small_kernel<<<(n + 255) / 256, 256, 0, s>>>(n, a, b, out);
   XDG_CHECK_LAUNCH();
   return XDG_OK;
 }

@@ -108,7 +108,7 @@ class Context:
         L = w.numel()
         ld = W.stride(0)
         nat.check(self.lib.xdg_gemv_update2(
-            L, int(ncols), W.data_ptr(), _ptr(Z), ld, coeff.data_ptr(),
+            L, int(ncols), W.data_ptr(), _ptr(Z), ld, coeff.data_ptr(), None,
             w.data_ptr(), _ptr(z), self.stream), "gemv_update2")
 
 

@@ -106,7 +106,7 @@ class RmBuffers:
         self.W = torch.empty(cols, n, dtype=F64, device=dev)
         self.Z = torch.empty(cols, n, dtype=F64, device=dev)
         self.vec = torch.zeros(8, n, dtype=F64, device=dev)  # x0 r0 y My My_new Mz x r
-        self.coeff = torch.zeros(max(max_columns, 1), dtype=F64, device=dev)
+        self.coeff = torch.zeros(3 * max(max_columns, 1), dtype=F64, device=dev)
         self.sc = torch.zeros(16, dtype=F64, device=dev)
         self.alpha_host = np.zeros(max(max_columns, 1))
         self.ws = torch.zeros((int(ctx.lib.xdg_reduce_workspace_bytes()) + 7) // 8,
