@@ -26,7 +26,7 @@ from cutdg.solvers import SolverConfig, gmres_pmg_solve, ortho_mg_solve  # noqa:
 from make_golden import CASES, build_case, perturbed  # noqa: E402
 
 PLAN = {
-    "cfg1": {1e-10: 20, 1e-9: 6, 1e-8: 6},
+    "cfg1": {1e-10: 20, 1e-9: 20, 1e-8: 40},
     "bench4": {1e-10: 10, 1e-9: 5, 1e-8: 5},
     "sphere8p3": {1e-8: 10},
 }
