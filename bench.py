@@ -174,8 +174,11 @@ def run_reference(args):
 
 def time_solves(torch, budget_s: float):
     """XDG solves on the serialized reference hierarchies: DOF/s per solve."""
+    from paper_2003_02431_b200 import solvers as S
     from paper_2003_02431_b200.hierarchy import load_hierarchy
     from paper_2003_02431_b200.solvers import SolverConfig, gmres_pmg_solve, ortho_mg_solve
+
+    peak, peak_kind = measured_peak()
 
     out = []
     t_start = time.perf_counter()
@@ -194,9 +197,12 @@ def time_solves(torch, budget_s: float):
             torch.cuda.synchronize()
             try:
                 if solver == "omg":
-                    x, rep = ortho_mg_solve(hier, lv.rhs, None, cfg, 1)
+                    octx = S._OmgContext(cfg, 1)
+                    x, rep = ortho_mg_solve(hier, lv.rhs, None, cfg, 1, octx)
+                    loop = dict(octx.last_loop)
                 else:
                     x, rep = gmres_pmg_solve(lv.matrix, lv.rhs, cfg, dim=meta["dim"])
+                    loop = dict(S.LAST_LOOP)
             except NotImplementedError as exc:
                 out.append({"case": case, "solver": solver, "unsupported": str(exc)})
                 continue
@@ -221,6 +227,11 @@ def time_solves(torch, budget_s: float):
                 "converged": rep.converged, "solve_s": rep.time_iterations,
                 "dof_per_s": meta["dofs_raw"] / rep.time_iterations,
                 "ms_per_iteration": 1e3 * rep.time_iterations / max(rep.iterations, 1),
+                "setup_s": loop["setup_seconds"], "loop_s": loop["seconds"],
+                "loop_algorithmic_bytes": loop["bytes"],
+                "loop_GBs": loop["bytes"] / max(loop["seconds"], 1e-12) / 1e9,
+                "loop_frac_of_hbm_peak": loop["bytes"] / max(loop["seconds"], 1e-12)
+                / 1e9 / peak,
                 "rel_err_vs_reference": rel,
                 "reference_cpu_s_build_container": ref_s,
                 "cpu_oracle_s_this_host": cpu_here,

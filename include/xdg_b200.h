@@ -218,6 +218,7 @@ typedef struct xdg_pmg {       /* PmgPlan of paper_2003_02431_b200/pmg.py */
   const int* cptr;
   const int64_t* cpos;
   const double* damping;
+  double apply_bytes;          /* algorithmic bytes of one apply (accounting) */
 } xdg_pmg;
 
 typedef struct xdg_direct {    /* dense LU of one system (coarsest level) */
@@ -284,12 +285,14 @@ int xdg_pmg_apply_op(const xdg_pmg* plan, const xdg_bsr* M, const double* b,
 /* ortho_mg_solve (solvers.py:669-749) entered at level index `entry`
  * (0-based) of `levels` (nlevels total).  x (device, entry level size) holds
  * the initial guess if has_x0, else is zeroed.  history: HOST array of
- * capacity max_iterations+1; *iterations, *hist_len, *final_residual set. */
+ * capacity max_iterations+1; *iterations, *hist_len, *final_residual set;
+ * *bytes_out (if not NULL) = algorithmic bytes of all kernels launched. */
 int xdg_omg_solve(xdg_omg_level* levels, int nlevels, int entry,
                   double tolerance, int max_iterations,
                   int coarse_cycle_iterations, const double* b, double* x,
                   int has_x0, int* iterations, double* history, int* hist_len,
-                  double* final_residual, xdg_stream_t stream);
+                  double* final_residual, double* bytes_out,
+                  xdg_stream_t stream);
 /* Restarted GMRES with PMG on the right (solvers.py:756-846).  V: device
  * [restart+1][n], Zb: [restart][n], w: [n], r: [n], sc: device
  * [restart+8], ycoef: device [restart].  history: HOST, capacity
@@ -299,7 +302,7 @@ int xdg_gmres_solve(const xdg_bsr* M, const xdg_pmg* pmg, int restart,
                     double* x, int has_x0, double* V, double* Zb, double* w,
                     double* r, double* sc, double* ycoef, void* ws,
                     void* gemv_ws, int* iterations, double* history,
-                    int* hist_len, double* final_residual,
+                    int* hist_len, double* final_residual, double* bytes_out,
                     xdg_stream_t stream);
 /* Fused modified Gram-Schmidt of GMRES step j (solvers.py:802-807):
  * for i <= j: h_i = V_i . w ; w -= h_i V_i ; then h_{j+1} = ||w|| and

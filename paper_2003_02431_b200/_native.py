@@ -58,9 +58,9 @@ SIGNATURES = {
     "xdg_rm_current": (_i32, [_vp, _vp]),
     "xdg_pmg_apply_op": (_i32, [_vp, _vp, _vp, _vp, _vp]),
     "xdg_omg_solve": (_i32, [_vp, _i32, _i32, _f64, _i32, _i32, _vp, _vp, _i32,
-                             _vp, _vp, _vp, _vp, _vp]),
+                             _vp, _vp, _vp, _vp, _vp, _vp]),
     "xdg_gmres_solve": (_i32, [_vp, _vp, _i32, _f64, _i32, _vp, _vp, _i32]
-                        + [_vp] * 13),
+                        + [_vp] * 14),
     "xdg_mgs": (_i32, [_i64, _i32, _vp, _i64, _vp, _vp, _vp, _vp]),
 }
 

@@ -134,6 +134,17 @@ mgs_kernel(int64_t n, int j, double* __restrict__ V, int64_t ldv,
 // ---------------------------------------------------------------------------
 // host helpers
 
+// Algorithmic bytes of every kernel the driver launches (minimal traffic of
+// each op: SURVEY 8(d) formulas), accumulated per solve so a solve can
+// report achieved bandwidth = bytes / time against the HBM roofline.
+thread_local double g_bytes = 0.0;
+inline void count(double b) { g_bytes += b; }
+inline double spmv_bytes(const xdg_bsr* M, bool fused_b) {
+  const double N = M->N;
+  return 8.0 * N * N * M->nnzb + 4.0 * M->nnzb + 4.0 * (M->nbr + 1) +
+         8.0 * N * (M->nbc + M->nbr) + (fused_b ? 8.0 * N * M->nbr : 0.0);
+}
+
 cudaError_t sync_read(double* host, const double* dev, int count, cudaStream_t s) {
   cudaError_t e = cudaMemcpyAsync(host, dev, sizeof(double) * count,
                                   cudaMemcpyDeviceToHost, s);
@@ -149,6 +160,7 @@ cudaError_t sync_read(double* host, const double* dev, int count, cudaStream_t s
 
 int spmv(const xdg_bsr* M, const double* x, double* y, const double* b,
          double* nrm, void* ws, cudaStream_t s) {
+  count(spmv_bytes(M, b != nullptr));
   return xdg_bsr_spmv(0, M->nbr, M->N, M->row_ptr, M->col, M->val_t, x, y, 1.0,
                       0.0, b, nrm, ws, reinterpret_cast<xdg_stream_t>(s));
 }
@@ -163,6 +175,7 @@ using namespace xdg;
 static int pmg_apply_op(const xdg_pmg* P, const xdg_bsr* M, const double* b,
                         double* z, cudaStream_t s) {
   xdg_stream_t st = reinterpret_cast<xdg_stream_t>(s);
+  count(P->apply_bytes);
   double* xlo = (P->direct && !P->has_high) ? z : P->xlo;
   XDG_TRY(xdg_lu_inv_apply(P->nsys, P->total, P->row_sys, P->lu_off, P->dims,
                            P->vec_off, P->LU, P->src, b, xlo, P->scratch, st));
@@ -187,6 +200,7 @@ extern "C" int xdg_pmg_apply_op(const xdg_pmg* P, const xdg_bsr* M,
 // ---------------------------------------------------------------------------
 extern "C" int xdg_rm_current(xdg_rm* rm, xdg_stream_t stream) {
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  count(48.0 * rm->n);
   rm_current_kernel<<<grid_for(rm->n, kT, kPerSm), kT, 0, s>>>(
       rm->n, rm->x0, rm->y, rm->r0, rm->My, rm->x, rm->r);
   XDG_CHECK_LAUNCH();
@@ -215,6 +229,7 @@ static int rm_restart(xdg_rm* rm, cudaStream_t s) {
   // best_norm is unchanged: it already is || r0 - My || of the very vector
   // that becomes the new r0 (same kernel, same data -> same bits), which is
   // what solvers.py:554 recomputes.
+  count(80.0 * rm->n);
   rm_restart_kernel<<<grid_for(rm->n, kT, kPerSm), kT, 0, s>>>(
       rm->n, rm->x0, rm->r0, rm->y, rm->My, rm->x, rm->r);
   XDG_CHECK_LAUNCH();
@@ -231,9 +246,11 @@ extern "C" int xdg_rm_step(xdg_rm* rm, const xdg_bsr* M, const double* zc,
   const int col = rm->ncols;
   double* z = rm->Z + (int64_t)col * n;  // candidate lives in its would-be column
   double* w = rm->W + (int64_t)col * n;
-  if (zc != z)
+  if (zc != z) {
+    count(16.0 * n);
     XDG_TRY_CUDA(cudaMemcpyAsync(z, zc, sizeof(double) * n,
                                  cudaMemcpyDeviceToDevice, s));
+  }
   double* sc = rm->sc;
   XDG_TRY(spmv(M, z, w, nullptr, sc + 0, rm->ws, s));          // w = M z
   if (col > 0) {
@@ -244,6 +261,8 @@ extern "C" int xdg_rm_step(xdg_rm* rm, const xdg_bsr* M, const double* zc,
     double* c1 = rm->coeff;
     double* c2 = rm->coeff + rm->max_columns;
     double* cs = rm->coeff + 2 * (int64_t)rm->max_columns;
+    // W read 3x (two W^T w, one w-only update), W+Z once, vectors
+    count(8.0 * col * n * 5 + 8.0 * n * 10);
     XDG_TRY(xdg_gemv_t(n, col, rm->W, n, w, c1, rm->gemv_ws, stream));
     XDG_TRY(xdg_gemv_update2(n, col, rm->W, nullptr, n, c1, nullptr, w, nullptr,
                              stream));
@@ -251,6 +270,7 @@ extern "C" int xdg_rm_step(xdg_rm* rm, const xdg_bsr* M, const double* zc,
     XDG_TRY(xdg_add_small(col, c1, c2, cs, stream));
     XDG_TRY(xdg_gemv_update2(n, col, rm->W, rm->Z, n, c2, cs, w, z, stream));
   }
+  count(16.0 * n + 32.0 * n + 16.0 * n + 32.0 * n);  // dot, normalize, dot, update
   XDG_TRY(xdg_dot(n, w, w, sc + 1, rm->ws, stream));          // ||w||^2
   // speculative tail (discarded when the candidate is dependent)
   rm_normalize_kernel<<<grid_for(n, kT, kPerSm), kT, 0, s>>>(n, sc + 1, w, z);
@@ -274,6 +294,7 @@ extern "C" int xdg_rm_step(xdg_rm* rm, const xdg_bsr* M, const double* zc,
     return rm_restart(rm, s);
   }
   rm->alpha_host[col] = alpha;
+  count(64.0 * n);
   rm_commit_kernel<<<grid_for(n, kT, kPerSm), kT, 0, s>>>(
       n, sc + 2, z, rm->y, rm->x0, rm->r0, rm->My_new, rm->x, rm->r);
   XDG_CHECK_LAUNCH();
@@ -308,6 +329,7 @@ int omg_level(OmgRun& R, int lam, const double* b, double* x, int has_x0,
   const int64_t n = (int64_t)lv.M.nbr * lv.M.N;
   if (lam == R.nlevels - 1 || !lv.has_restriction) {           // solvers.py:698-710
     const xdg_direct& D = lv.direct;
+    count(8.0 * D.n * (double)D.n + 32.0 * D.n);
     XDG_TRY(xdg_lu_inv_apply(1, D.n, D.row_sys, D.zero_off, D.dims, D.zero_off,
                              D.LU, D.perm, b, x, D.scratch, st));
     if (lam == R.entry) {
@@ -368,7 +390,9 @@ extern "C" int xdg_omg_solve(xdg_omg_level* levels, int nlevels, int entry,
                              int coarse_cycle_iterations, const double* b,
                              double* x, int has_x0, int* iterations,
                              double* history, int* hist_len,
-                             double* final_residual, xdg_stream_t stream) {
+                             double* final_residual, double* bytes_out,
+                             xdg_stream_t stream) {
+  g_bytes = 0.0;
   XDG_REQUIRE(nlevels >= 1 && entry >= 0 && entry < nlevels, XDG_ERR_ARG,
               "bad level range");
   OmgRun R{levels, nlevels, entry, tolerance, max_iterations,
@@ -377,6 +401,7 @@ extern "C" int xdg_omg_solve(xdg_omg_level* levels, int nlevels, int entry,
                      final_residual);
   if (st != XDG_OK) return st;
   XDG_TRY_CUDA(cudaStreamSynchronize(R.s));
+  if (bytes_out) *bytes_out = g_bytes;
   return XDG_OK;
 }
 
@@ -410,8 +435,9 @@ extern "C" int xdg_gmres_solve(const xdg_bsr* M, const xdg_pmg* pmg,
                                double* r, double* sc, double* ycoef, void* ws,
                                void* gemv_ws, int* iterations, double* history,
                                int* hist_len, double* final_residual,
-                               xdg_stream_t stream) {
+                               double* bytes_out, xdg_stream_t stream) {
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  g_bytes = 0.0;
   const int m = restart;
   const int64_t n = (int64_t)M->nbr * M->N;
   (void)gemv_ws;
@@ -431,6 +457,7 @@ extern "C" int xdg_gmres_solve(const xdg_bsr* M, const xdg_pmg* pmg,
     std::fill(sn.begin(), sn.end(), 0.0);
     std::fill(g.begin(), g.end(), 0.0);
     g[0] = beta;
+    count(16.0 * n);
     XDG_TRY(xdg_scale(n, beta, nullptr, 1, r, V, stream));      // V_0 = r / beta
     int j = 0;
     while (j < m && total < max_iterations) {
@@ -439,6 +466,7 @@ extern "C" int xdg_gmres_solve(const xdg_bsr* M, const xdg_pmg* pmg,
       double* Zj = Zb + (int64_t)j * n;
       XDG_TRY(pmg_apply_op(pmg, M, Vj, Zj, s));
       XDG_TRY(spmv(M, Zj, w, nullptr, nullptr, nullptr, s));
+      count(8.0 * n * (3.0 * (j + 1) + 3.0));
       XDG_TRY(xdg_mgs(n, j, V, n, w, sc, ws, stream));
       XDG_TRY_CUDA(sync_read(hc.data(), sc, j + 2, s));
       for (int i = 0; i <= j + 1; ++i) Hc(i, j) = hc[i];
@@ -472,6 +500,7 @@ extern "C" int xdg_gmres_solve(const xdg_bsr* M, const xdg_pmg* pmg,
     for (int i = 0; i < j; ++i) y[i] = -y[i];                     // x -= Z (-y)
     XDG_TRY_CUDA(cudaMemcpyAsync(ycoef, y.data(), sizeof(double) * j,
                                  cudaMemcpyHostToDevice, s));
+    count(8.0 * j * n + 16.0 * n);
     XDG_TRY(xdg_gemv_update2(n, j, Zb, nullptr, n, ycoef, nullptr, x, nullptr,
                              stream));
     XDG_TRY(spmv(M, x, r, b, sc, ws, s));
@@ -482,6 +511,7 @@ extern "C" int xdg_gmres_solve(const xdg_bsr* M, const xdg_pmg* pmg,
   *iterations = total;
   *hist_len = hl;
   *final_residual = beta;
+  if (bytes_out) *bytes_out = g_bytes;
   return XDG_OK;
 }
 

@@ -31,7 +31,7 @@ class XdgPmg(C.Structure):
                             "src", "xlo",
                             "wi_ptr", "wi_blk", "wi_lcol", "wi_cell", "wi_lrow",
                             "wi_xlo", "wi_hidx", "wi_out", "HLU", "hperm", "out",
-                            "cptr", "cpos", "damping")]
+                            "cptr", "cpos", "damping")] + [("apply_bytes", C.c_double)]
 
 
 class XdgDirect(C.Structure):
@@ -81,6 +81,7 @@ def pmg_struct(plan):
     if not plan.direct:
         s.out, s.cptr, s.cpos = _p(plan.out), _p(plan.cptr), _p(plan.cpos)
         s.damping = _p(plan.damping)
+    s.apply_bytes = float(plan.algorithmic_bytes())
     return s, []
 
 

@@ -52,6 +52,7 @@ __all__ = [
 ]
 
 DEPENDENT_CANDIDATE_RTOL = 1e-13   # solvers.py:52
+LAST_LOOP: dict = {}               # last GMRES loop: seconds, algorithmic bytes
 DEFAULT_RM_MAX_COLUMNS = 200       # solvers.py:53
 F64 = torch.float64
 
@@ -486,12 +487,16 @@ def ortho_mg_solve(hierarchy, b, x0=None, config: Optional[SolverConfig] = None,
     n = bd.numel()
     x = torch.zeros_like(bd) if x0 is None else _to_dev(x0, ctx)
     hist = np.zeros(config.max_iterations + 2)
-    it, hl, fin = C.c_int(0), C.c_int(0), C.c_double(0.0)
+    it, hl, fin, nbytes = C.c_int(0), C.c_int(0), C.c_double(0.0), C.c_double(0.0)
+    t_iter = perf_counter()
     nat_check(ctx.lib.xdg_omg_solve(
         arr, hierarchy.num_levels, level - 1, float(config.tolerance),
         int(config.max_iterations), int(config.coarse_cycle_iterations),
         bd.data_ptr(), x.data_ptr(), int(x0 is not None), C.byref(it),
-        hist.ctypes.data, C.byref(hl), C.byref(fin), ctx.stream), "omg_solve")
+        hist.ctypes.data, C.byref(hl), C.byref(fin), C.byref(nbytes), ctx.stream),
+        "omg_solve")
+    ctx_omg.last_loop = dict(seconds=perf_counter() - t_iter, bytes=nbytes.value,
+                             setup_seconds=t_iter - t_start)
     history = [float(v) for v in hist[: hl.value]]
     rep = SolverReport(solver="omg", iterations=it.value,
                        converged=fin.value <= config.tolerance,
@@ -536,16 +541,19 @@ def gmres_pmg_solve(M, b, config: Optional[SolverConfig] = None,
     ws = torch.zeros((int(ctx.lib.xdg_reduce_workspace_bytes()) + 7) // 8, dtype=F64,
                      device=dev)
     hist = np.zeros(config.max_iterations + 2)
-    it, hl, fin = C.c_int(0), C.c_int(0), C.c_double(0.0)
+    it, hl, fin, nbytes = C.c_int(0), C.c_int(0), C.c_double(0.0), C.c_double(0.0)
     Ms = bsr_struct(D)
     Ps, _k = pmg_struct(plan)
+    t_iter = perf_counter()
     nat_check(ctx.lib.xdg_gmres_solve(
         C.byref(Ms), C.byref(Ps), m, float(config.tolerance), int(config.max_iterations),
         bd.data_ptr(), x.data_ptr(), int(x0 is not None), V.data_ptr(), Z.data_ptr(),
         w.data_ptr(), r.data_ptr(), sc.data_ptr(), ycoef.data_ptr(), ws.data_ptr(),
-        None, C.byref(it), hist.ctypes.data, C.byref(hl), C.byref(fin), ctx.stream),
-        "gmres_solve")
+        None, C.byref(it), hist.ctypes.data, C.byref(hl), C.byref(fin), C.byref(nbytes),
+        ctx.stream), "gmres_solve")
     torch.cuda.synchronize(dev)
+    LAST_LOOP.update(seconds=perf_counter() - t_iter, bytes=nbytes.value,
+                     setup_seconds=t_iter - t_start)
     history = [float(v) for v in hist[: hl.value]]
     rep = SolverReport(solver="gmres-pmg", iterations=it.value,
                        converged=fin.value <= config.tolerance, final_residual=fin.value,
