@@ -179,6 +179,14 @@ def time_solves(torch, budget_s: float):
     from paper_2003_02431_b200.solvers import SolverConfig, gmres_pmg_solve, ortho_mg_solve
 
     peak, peak_kind = measured_peak()
+    # one-time process warm-up (cuSOLVER handle, module loading) outside the
+    # timed solves -- the reference's scipy/LAPACK is likewise already loaded
+    from paper_2003_02431_b200.direct import lu_factor_dense
+
+    eye = torch.eye(64, dtype=torch.float64, device="cuda")
+    lu_factor_dense(eye)
+    torch.linalg.solve_triangular(eye, eye, upper=True)
+    torch.cuda.synchronize()
 
     out = []
     t_start = time.perf_counter()
