@@ -56,6 +56,11 @@ int xdg_blocks_transpose(int64_t nnzb, int N, const double* in, double* out,
 int xdg_gather_blocks(int64_t nidx, int N, const int* idx, const double* x,
                       double* out, xdg_stream_t stream);
 
+/* out[k*m + q] = x[k*N + q], q < m: the low-order modes of nblk blocks (the
+ * owned part of the distributed low-order right-hand side, solvers.py:250). */
+int xdg_gather_modes(int64_t nblk, int N, int m, const double* x, double* out,
+                     xdg_stream_t stream);
+
 /* ---- block-sparse matrix-vector product -------------------------------- */
 /* Block rows [row_begin, row_end) of
  *     b == NULL :  y = alpha * (M x) + beta * y   (beta == 0: y not read)

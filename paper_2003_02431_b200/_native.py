@@ -30,6 +30,7 @@ SIGNATURES = {
     "xdg_reduce_workspace_bytes": (_i64, []),
     "xdg_blocks_transpose": (_i32, [_i64, _i32, _vp, _vp, _vp]),
     "xdg_gather_blocks": (_i32, [_i64, _i32, _vp, _vp, _vp, _vp]),
+    "xdg_gather_modes": (_i32, [_i64, _i32, _i32, _vp, _vp, _vp]),
     "xdg_bsr_spmv": (_i32, [_i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _f64,
                             _f64, _vp, _vp, _vp, _vp]),
     "xdg_dot": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp]),

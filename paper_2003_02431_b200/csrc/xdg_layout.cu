@@ -41,8 +41,30 @@ gather_blocks_kernel(int64_t nidx, int N, const int* __restrict__ idx,
   }
 }
 
+__global__ void __launch_bounds__(kT)
+gather_modes_kernel(int64_t nblk, int N, int m, const double* __restrict__ x,
+                    double* __restrict__ out) {
+  const int64_t total = nblk * m;
+  for (int64_t t = (int64_t)blockIdx.x * kT + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * kT) {
+    const int64_t k = t / m;
+    out[t] = x[k * N + (t - k * m)];
+  }
+}
+
 }  // namespace
 }  // namespace xdg
+
+extern "C" int xdg_gather_modes(int64_t nblk, int N, int m, const double* x,
+                                double* out, xdg_stream_t stream) {
+  using namespace xdg;
+  if (nblk <= 0) return XDG_OK;
+  XDG_REQUIRE(m >= 1 && m <= N, XDG_ERR_ARG, "bad mode count %d of %d", m, N);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  gather_modes_kernel<<<grid_for(nblk * m, kT, 8), kT, 0, s>>>(nblk, N, m, x, out);
+  XDG_CHECK_LAUNCH();
+  return XDG_OK;
+}
 
 extern "C" int xdg_gather_blocks(int64_t nidx, int N, const int* idx,
                                  const double* x, double* out,

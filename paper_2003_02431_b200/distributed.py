@@ -84,24 +84,40 @@ class HaloPlan:
             for p, idx in self.sends.items():
                 self.sendbufs[p].copy_(xv[idx.long()].reshape(-1))
 
+    def _host_staged(self, x_ext) -> bool:
+        """gloo cannot move CUDA tensors point to point: stage through host
+        memory (the tests run several gloo ranks on one GPU)."""
+        return x_ext.is_cuda and dist.get_backend(self.group) == "gloo"
+
     def start(self, x_ext: torch.Tensor):
-        """Post the exchange; returns the request list (wait with `finish`)."""
+        """Post the exchange; returns a pending handle (wait with `finish`)."""
         if self.world == 1 or (not self.sends and not self.recvs):
             return []
         self._pack(x_ext)
-        ops = []
+        ops, post = [], []
         base = self.nloc * self.N
+        staged = self._host_staged(x_ext)
         for q, (lo, hi) in sorted(self.recvs.items()):
-            ops.append(dist.P2POp(dist.irecv, x_ext[base + lo * self.N: base + hi * self.N],
-                                  q, group=self.group))
+            dst = x_ext[base + lo * self.N: base + hi * self.N]
+            if staged:
+                buf = torch.empty(dst.numel(), dtype=dst.dtype)
+                post.append((dst, buf))
+                dst = buf
+            ops.append(dist.P2POp(dist.irecv, dst, q, group=self.group))
         for p, _ in sorted(self.sends.items()):
-            ops.append(dist.P2POp(dist.isend, self.sendbufs[p], p, group=self.group))
-        return dist.batch_isend_irecv(ops)
+            src = self.sendbufs[p].cpu() if staged else self.sendbufs[p]
+            ops.append(dist.P2POp(dist.isend, src, p, group=self.group))
+        return (dist.batch_isend_irecv(ops), post)
 
     @staticmethod
-    def finish(reqs):
+    def finish(pending):
+        if not pending:
+            return
+        reqs, post = pending
         for r in reqs:
             r.wait()
+        for dst, buf in post:
+            dst.copy_(buf)
 
     def exchange(self, x_ext: torch.Tensor):
         self.finish(self.start(x_ext))
