@@ -17,7 +17,7 @@ from .errors import (
 )
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libxdg_b200.so")
+LIB_PATH = os.environ.get("XDG_LIB", os.path.join(_PKG, "libxdg_b200.so"))
 
 XDG_OK, XDG_ERR_ARG, XDG_ERR_CUDA, XDG_ERR_SINGULAR, XDG_ERR_UNSUPPORTED = range(5)
 

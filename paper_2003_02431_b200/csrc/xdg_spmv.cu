@@ -28,6 +28,22 @@ namespace {
 
 constexpr int kThreads = 256;
 
+// Minimum resident CTAs per SM requested from ptxas for the warp-aligned
+// kernel (0: no hint).  A hint lets ptxas keep a whole block column of
+// loads in flight (measured with tools/tune_spmv.py; see profiles/).
+#ifndef XDG_SPMV_MINB_SMALL
+#define XDG_SPMV_MINB_SMALL 3  // N <= 12
+#endif
+#ifndef XDG_SPMV_MINB_LARGE
+#define XDG_SPMV_MINB_LARGE 3  // N > 12
+#endif
+template <int N>
+struct MinBlocks {
+  static constexpr int v = N <= 12 ? XDG_SPMV_MINB_SMALL : XDG_SPMV_MINB_LARGE;
+};
+#define XDG_LB(N) __launch_bounds__(kThreads, MinBlocks<N>::v > 0 ? MinBlocks<N>::v : 1)
+#define XDG_LB_HINTED(N) (MinBlocks<N>::v > 0)
+
 enum EpiMode { EPI_PLAIN = 0, EPI_AXPBY = 1, EPI_RESID = 2 };
 
 template <int MODE>
@@ -46,7 +62,7 @@ __device__ __forceinline__ double epilogue(double acc, int64_t gi,
 
 // ---- N <= 32: warp-aligned block rows, x exchanged through shuffles -------
 template <int N, int MODE, bool NORM>
-__global__ void __launch_bounds__(kThreads)
+__global__ void XDG_LB(N)
 spmv_warp_rows(int row_begin, int row_end, const int* __restrict__ row_ptr,
                const int* __restrict__ col, const double* __restrict__ val,
                const double* __restrict__ x, double* y, double alpha,
