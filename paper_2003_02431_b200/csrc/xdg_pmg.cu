@@ -160,6 +160,80 @@ pmg_high_kernel(int nwork, int N, int m, const int* __restrict__ wi_ptr,
   }
 }
 
+// nh <= 16: floor(32/nh) cells per warp, lane group g owns cell w_base + g,
+// lane i of the group owns high row i.  Same arithmetic order per row as
+// pmg_high_kernel (blocks in order, low columns in order, separate mul/add;
+// column-oriented LU substitutions).
+__global__ void __launch_bounds__(kT)
+pmg_high_packed_kernel(int nwork, int N, int m, const int* __restrict__ wi_ptr,
+                       const int* __restrict__ wi_blk, const int* __restrict__ wi_lcol,
+                       const int* __restrict__ wi_cell, const int* __restrict__ wi_lrow,
+                       const int64_t* __restrict__ wi_xlo,
+                       const int* __restrict__ wi_hidx,
+                       const int64_t* __restrict__ wi_out,
+                       const double* __restrict__ val_t,
+                       const double* __restrict__ HLU, const int* __restrict__ hperm,
+                       const double* __restrict__ b, const double* __restrict__ xlo_buf,
+                       double* __restrict__ out_buf) {
+  const int nh = N - m;
+  const int cpw = 32 / nh;
+  const int lane = threadIdx.x & 31;
+  const int grp = lane / nh;
+  const int i = lane - grp * nh;
+  const int base = grp * nh;
+  const bool lane_ok = grp < cpw;
+  const int warps = (gridDim.x * kT) >> 5;
+  for (int wb = ((blockIdx.x * kT + threadIdx.x) >> 5) * cpw; wb < nwork;
+       wb += warps * cpw) {
+    const int w = wb + grp;
+    const bool active = lane_ok && w < nwork;
+    int e0 = 0, e1 = 0;
+    const double* xlo = xlo_buf;
+    if (active) {
+      e0 = wi_ptr[w];
+      e1 = wi_ptr[w + 1];
+      xlo = xlo_buf + wi_xlo[w];
+    }
+    const int cnt = __reduce_max_sync(0xffffffffu, e1 - e0);
+    double acc = 0.0;
+    for (int t = 0; t < cnt; ++t) {
+      const int e = e0 + t;
+      if (active && e < e1) {
+        const int64_t k = wi_blk[e];
+        const double* v = val_t + k * N * N + m + i;
+        const double* xq = xlo + (int64_t)wi_lcol[e] * m;
+        for (int q = 0; q < m; ++q)
+          acc = __dadd_rn(acc, __dmul_rn(__ldg(v + q * N), __ldg(xq + q)));
+      }
+    }
+    double r = 0.0;
+    int c = 0, hi = 0;
+    if (active) {
+      c = wi_cell[w];
+      hi = wi_hidx[w];
+      r = __dadd_rn(b[(int64_t)c * N + m + i], -acc);
+    }
+    const double* F = HLU + (int64_t)hi * nh * nh;
+    const int pi = active ? hperm[(int64_t)hi * nh + i] : i;
+    double t = __shfl_sync(0xffffffffu, r, base + pi);
+    for (int j = 0; j < nh; ++j) {  // unit lower, column-oriented
+      const double yj = __shfl_sync(0xffffffffu, t, base + j);
+      if (active && i > j) t = __dadd_rn(t, -__dmul_rn(yj, F[(int64_t)j * nh + i]));
+    }
+    for (int j = nh - 1; j >= 0; --j) {  // upper, column-oriented
+      if (active && i == j) t = __ddiv_rn(t, F[(int64_t)j * nh + j]);
+      const double xj = __shfl_sync(0xffffffffu, t, base + j);
+      if (active && i < j) t = __dadd_rn(t, -__dmul_rn(xj, F[(int64_t)j * nh + i]));
+    }
+    if (active) {
+      double* o = out_buf + wi_out[w];
+      const double* self = xlo + (int64_t)wi_lrow[w] * m;
+      for (int q = i; q < m; q += nh) o[q] = self[q];
+      o[m + i] = t;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kT)
 combine_kernel(int nbr, int N, const int* __restrict__ cptr,
                const int64_t* __restrict__ cpos, const double* __restrict__ out,
@@ -222,6 +296,16 @@ extern "C" int xdg_pmg_high(int nwork, int N, int m, const int* wi_ptr,
               "high-order block size %d outside [1, 64]", nh);
   if (nwork <= 0) return XDG_OK;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (nh <= 16) {
+    const int cpw = 32 / nh;
+    const int64_t warps = ((int64_t)nwork + cpw - 1) / cpw;
+    const int g = resident_grid(pmg_high_packed_kernel, kT, 0, warps * 32);
+    pmg_high_packed_kernel<<<g, kT, 0, s>>>(nwork, N, m, wi_ptr, wi_blk, wi_lcol,
+                                            wi_cell, wi_lrow, wi_xlo, wi_hidx,
+                                            wi_out, val_t, HLU, hperm, b, xlo, out);
+    XDG_CHECK_LAUNCH();
+    return XDG_OK;
+  }
   const int grid = grid_for((int64_t)nwork * 32, kT, 8);
   if (nh <= 32)
     pmg_high_kernel<1><<<grid, kT, 0, s>>>(nwork, N, m, wi_ptr, wi_blk, wi_lcol,
