@@ -66,17 +66,20 @@ __device__ __forceinline__ double tri_row_dot(const double* __restrict__ row,
                                               const double* v, int i, int n,
                                               int lane) {
   // LOWER: sum_{j<i} row[j] v[j];  UPPER: sum_{j>=i} row[j] v[j].
-  // 8 independent loads per lane in flight (memory-level parallelism for a
-  // single SM streaming a whole factor), 4 accumulators, fixed order.
+  // Chunks of 256 columns: every lane issues its 8 loads of a chunk
+  // together (predicated past the end), so short rows and row tails keep
+  // the same memory-level parallelism as long rows.  4 accumulators, fixed
+  // order: deterministic.
   const int j0 = LOWER ? 0 : i, j1 = LOWER ? i : n;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-  int j = j0 + lane;
-  for (; j + 224 < j1; j += 256) {
+  for (int jb = j0; jb < j1; jb += 256) {
     double r[8], q[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      r[u] = __ldg(row + j + 32 * u);
-      q[u] = v[j + 32 * u];
+      const int j = jb + lane + 32 * u;
+      const bool in = j < j1;
+      r[u] = in ? __ldg(row + j) : 0.0;
+      q[u] = in ? v[j] : 0.0;
     }
     a0 = fma(r[0], q[0], a0);
     a1 = fma(r[1], q[1], a1);
@@ -87,7 +90,6 @@ __device__ __forceinline__ double tri_row_dot(const double* __restrict__ row,
     a2 = fma(r[6], q[6], a2);
     a3 = fma(r[7], q[7], a3);
   }
-  for (; j < j1; j += 32) a0 = fma(__ldg(row + j), v[j], a0);
   return warp_sum((a0 + a1) + (a2 + a3));
 }
 
