@@ -72,7 +72,24 @@ __device__ __forceinline__ double tri_row_dot(const double* __restrict__ row,
   // order: deterministic.
   const int j0 = LOWER ? 0 : i, j1 = LOWER ? i : n;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-  for (int jb = j0; jb < j1; jb += 256) {
+  int jb = j0;
+  for (; jb + 256 <= j1; jb += 256) {  // full chunks: no predicates
+    double r[8], q[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      r[u] = __ldg(row + jb + lane + 32 * u);
+      q[u] = v[jb + lane + 32 * u];
+    }
+    a0 = fma(r[0], q[0], a0);
+    a1 = fma(r[1], q[1], a1);
+    a2 = fma(r[2], q[2], a2);
+    a3 = fma(r[3], q[3], a3);
+    a0 = fma(r[4], q[4], a0);
+    a1 = fma(r[5], q[5], a1);
+    a2 = fma(r[6], q[6], a2);
+    a3 = fma(r[7], q[7], a3);
+  }
+  if (jb < j1) {  // one predicated chunk for the tail
     double r[8], q[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
