@@ -56,6 +56,10 @@ int xdg_blocks_transpose(int64_t nnzb, int N, const double* in, double* out,
 int xdg_gather_blocks(int64_t nidx, int N, const int* idx, const double* x,
                       double* out, xdg_stream_t stream);
 
+/* y[idx[i]*N + q] += src[i*N + q] (idx without duplicates): adds the
+ * partial Schwarz sums other ranks computed for this rank's cells. */
+int xdg_scatter_add_blocks(int64_t nidx, int N, const int* idx,
+                           const double* src, double* y, xdg_stream_t stream);
 /* out[k*m + q] = x[k*N + q], q < m: the low-order modes of nblk blocks (the
  * owned part of the distributed low-order right-hand side, solvers.py:250). */
 int xdg_gather_modes(int64_t nblk, int N, int m, const double* x, double* out,
@@ -279,6 +283,18 @@ int xdg_rm_step(xdg_rm* rm, const xdg_bsr* M, const double* z,
 /* RmState(x0, r0): copies x0, r0, zeroes y / My, best_norm = ||r0||. */
 int xdg_rm_init(xdg_rm* rm, const double* x0, const double* r0,
                 xdg_stream_t stream);
+/* rm_step pieces for the multi-GPU driver (it all-reduces in between):
+ * w /= sqrt(*nw2), z /= sqrt(*nw2)  (solvers.py:601-602);
+ * y += alpha z, x = x0 + y, r = r0 - My_new  (accept, solvers.py:617-624);
+ * x0 += y, r0 -= My, y = My = 0, x = x0, r = r0  (restart, 548-556). */
+int xdg_rm_normalize(int64_t n, const double* nw2_dev, double* w, double* z,
+                     xdg_stream_t stream);
+int xdg_rm_commit(int64_t n, const double* alpha_dev, const double* z,
+                  double* y, const double* x0, const double* r0,
+                  const double* My_new, double* x, double* r,
+                  xdg_stream_t stream);
+int xdg_rm_restart_vec(int64_t n, double* x0, double* r0, double* y, double* My,
+                       double* x, double* r, xdg_stream_t stream);
 /* RmState.restart() (solvers.py:548-556); also leaves x = x0, r = r0. */
 int xdg_rm_restart(xdg_rm* rm, xdg_stream_t stream);
 /* x = x0 + y, r = r0 - My  (RmState.current()). */

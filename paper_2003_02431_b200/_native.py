@@ -54,6 +54,10 @@ SIGNATURES = {
     "xdg_pmg_high": (_i32, [_i32, _i32, _i32] + [_vp] * 15),
     "xdg_pmg_combine": (_i32, [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp]),
     "xdg_rm_step": (_i32, [_vp, _vp, _vp, _vp]),
+    "xdg_rm_normalize": (_i32, [_i64, _vp, _vp, _vp, _vp]),
+    "xdg_rm_commit": (_i32, [_i64] + [_vp] * 9),
+    "xdg_rm_restart_vec": (_i32, [_i64] + [_vp] * 7),
+    "xdg_scatter_add_blocks": (_i32, [_i64, _i32, _vp, _vp, _vp, _vp]),
     "xdg_rm_init": (_i32, [_vp, _vp, _vp, _vp]),
     "xdg_rm_restart": (_i32, [_vp, _vp]),
     "xdg_rm_current": (_i32, [_vp, _vp]),

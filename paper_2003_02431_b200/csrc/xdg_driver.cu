@@ -515,6 +515,39 @@ extern "C" int xdg_gmres_solve(const xdg_bsr* M, const xdg_pmg* pmg,
   return XDG_OK;
 }
 
+// Exported pieces of rm_step for the multi-GPU driver (dist_solvers.py),
+// which interleaves them with all-reduces.
+extern "C" int xdg_rm_normalize(int64_t n, const double* nw2_dev, double* w,
+                                double* z, xdg_stream_t stream) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (n <= 0) return XDG_OK;
+  rm_normalize_kernel<<<grid_for(n, kT, kPerSm), kT, 0, s>>>(n, nw2_dev, w, z);
+  XDG_CHECK_LAUNCH();
+  return XDG_OK;
+}
+
+extern "C" int xdg_rm_commit(int64_t n, const double* alpha_dev, const double* z,
+                             double* y, const double* x0, const double* r0,
+                             const double* My_new, double* x, double* r,
+                             xdg_stream_t stream) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (n <= 0) return XDG_OK;
+  rm_commit_kernel<<<grid_for(n, kT, kPerSm), kT, 0, s>>>(n, alpha_dev, z, y, x0, r0,
+                                                          My_new, x, r);
+  XDG_CHECK_LAUNCH();
+  return XDG_OK;
+}
+
+extern "C" int xdg_rm_restart_vec(int64_t n, double* x0, double* r0, double* y,
+                                  double* My, double* x, double* r,
+                                  xdg_stream_t stream) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (n <= 0) return XDG_OK;
+  rm_restart_kernel<<<grid_for(n, kT, kPerSm), kT, 0, s>>>(n, x0, r0, y, My, x, r);
+  XDG_CHECK_LAUNCH();
+  return XDG_OK;
+}
+
 extern "C" int xdg_rm_restart(xdg_rm* rm, xdg_stream_t stream) {
   return rm_restart(rm, reinterpret_cast<cudaStream_t>(stream));
 }

@@ -122,6 +122,29 @@ class HaloPlan:
     def exchange(self, x_ext: torch.Tensor):
         self.finish(self.start(x_ext))
 
+    def reverse(self, ghost_vals: torch.Tensor) -> dict:
+        """Transpose of `exchange`: send the values this rank holds for its
+        ghost blocks (ghost_vals, (nghost * N,)) back to their owners;
+        returns {source rank: received values for self.sends[source]}."""
+        if self.world == 1:
+            return {}
+        staged = ghost_vals.is_cuda and dist.get_backend(self.group) == "gloo"
+        ops, bufs = [], {}
+        for p, idx in sorted(self.sends.items()):
+            buf = torch.empty(idx.numel() * self.N, dtype=ghost_vals.dtype,
+                              device="cpu" if staged else ghost_vals.device)
+            bufs[p] = buf
+            ops.append(dist.P2POp(dist.irecv, buf, p, group=self.group))
+        for q, (lo, hi) in sorted(self.recvs.items()):
+            src = ghost_vals[lo * self.N: hi * self.N]
+            ops.append(dist.P2POp(dist.isend, src.cpu() if staged else src, q,
+                                  group=self.group))
+        for r in dist.batch_isend_irecv(ops) if ops else []:
+            r.wait()
+        if staged:
+            bufs = {p: b.to(ghost_vals.device) for p, b in bufs.items()}
+        return bufs
+
 
 def split_interior(row_ptr: np.ndarray, col: np.ndarray, nloc: int):
     """(a, b): rows [a, b) reference no ghost column; rows outside are the

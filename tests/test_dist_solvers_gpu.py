@@ -24,7 +24,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, case, tol, q):
+def _worker(rank, world, port, case, tol, q, solver="gmres"):
     sys.path.insert(0, ROOT)
     import torch
     import torch.distributed as dist
@@ -33,26 +33,33 @@ def _worker(rank, world, port, case, tol, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         torch.cuda.set_device(0)
-        from paper_2003_02431_b200.dist_solvers import dist_gmres_pmg_solve
+        from paper_2003_02431_b200.dist_solvers import (dist_gmres_pmg_solve,
+                                                         dist_ortho_mg_solve)
+        from paper_2003_02431_b200.hierarchy import load_hierarchy
         from paper_2003_02431_b200.solvers import SolverConfig
 
         z = np.load(golden_path(case))
         meta = json.loads(bytes(z["meta"]).decode())
-        cfgd = dict(meta["gmres"])
+        cfgd = dict(meta[solver])
         cfgd["tolerance"] = tol
-        x, (r0, r1), rep = dist_gmres_pmg_solve(
-            z["L1_row_ptr"], z["L1_col"], z["L1_val"], z["L1_rhs"], SolverConfig(**cfgd),
-            dim=meta["dim"])
+        if solver == "gmres":
+            x, (r0, r1), rep = dist_gmres_pmg_solve(
+                z["L1_row_ptr"], z["L1_col"], z["L1_val"], z["L1_rhs"],
+                SolverConfig(**cfgd), dim=meta["dim"])
+        else:
+            hier = load_hierarchy(z)
+            x, (r0, r1), rep = dist_ortho_mg_solve(hier, np.asarray(z["L1_rhs"]),
+                                                   SolverConfig(**cfgd))
         q.put((rank, r0, r1, x, rep.iterations, rep.converged, rep.final_residual))
     finally:
         dist.destroy_process_group()
 
 
-def run_world(world, case, tol):
+def run_world(world, case, tol, solver="gmres"):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, case, tol, q))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, tol, q, solver))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -83,3 +90,41 @@ def test_distributed_gmres_cfg1(world):
 def test_distributed_gmres_bench4_matches_single_gpu_count():
     res = run_world(2, "bench4", 1e-10)
     assert {r[4] for r in res} <= {708, 709, 710}   # reference: 709 in every run
+
+
+def _assemble(z, res):
+    N = int(z["L1_N"])
+    x = np.zeros(len(z["L1_rhs"]))
+    for _, r0, r1, xl, *_ in res:
+        x[r0 * N: r1 * N] = xl
+    return x
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_distributed_omg_bench4(world):
+    """bench4 OMG is stable under 1-ulp perturbations in the reference (211
+    in every run at 1e-10): the distributed solver must match it +-1."""
+    z = np.load(golden_path("bench4"))
+    res = run_world(world, "bench4", 1e-10, "omg")
+    its = {r[4] for r in res}
+    assert len(its) == 1
+    assert 210 <= its.pop() <= 212
+    xd = z["L1_direct_rhs"]
+    assert np.linalg.norm(_assemble(z, res) - xd) <= 1e-8 * np.linalg.norm(xd)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_distributed_omg_cfg1(world):
+    """cfg1 OMG is chaotic in the reference (358-503 at 1e-8, K=40): check
+    the solution and the count against the chaotic-regime bar."""
+    z = np.load(golden_path("cfg1"))
+    env = np.load(os.path.join(os.path.dirname(golden_path("cfg1")), "cfg1_env.npz"))[
+        "omg_tol1e-08"]
+    res = run_world(world, "cfg1", 1e-8, "omg")
+    its = {r[4] for r in res}
+    assert len(its) == 1
+    it = its.pop()
+    slack = int(round(0.10 * np.median(env)))
+    assert env.min() - slack <= it <= env.max() + slack, (it, env.min(), env.max())
+    xd = z["L1_direct_rhs"]
+    assert np.linalg.norm(_assemble(z, res) - xd) <= 1e-6 * np.linalg.norm(xd)
