@@ -450,6 +450,8 @@ class _DistRm:
     def init(self, x, r):
         self.x0.copy_(x)
         self.r0.copy_(r)
+        self.x.copy_(x)      # current point / true residual (RmState.current())
+        self.r.copy_(r)
         self.y.zero_()
         self.My.zero_()
         self.ctx.dot(self.r0, self.r0, self.sc[7:8])
