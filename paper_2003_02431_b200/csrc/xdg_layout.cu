@@ -106,8 +106,8 @@ extern "C" int xdg_blocks_transpose(int64_t nnzb, int N, const double* in,
                                     double* out, xdg_stream_t stream) {
   using namespace xdg;
   XDG_REQUIRE(N >= 1 && nnzb >= 0, XDG_ERR_ARG, "bad block shape");
-  XDG_REQUIRE(in != out, XDG_ERR_ARG, "in-place transpose not supported");
   if (nnzb == 0) return XDG_OK;
+  XDG_REQUIRE(in != out, XDG_ERR_ARG, "in-place transpose not supported");
   const int nn = N * N;
   const int per_tile = (4096 / nn) > 0 ? (4096 / nn) : 1;
   const size_t smem = sizeof(double) * (size_t)per_tile * nn;

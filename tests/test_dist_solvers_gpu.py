@@ -63,7 +63,18 @@ def run_world(world, case, tol, solver="gmres"):
              for r in range(world)]
     for p in procs:
         p.start()
-    res = sorted([q.get(timeout=600) for _ in range(world)], key=lambda t: t[0])
+    import queue as _q
+    import time as _t
+
+    res, deadline = [], _t.time() + 900
+    while len(res) < world:
+        try:
+            res.append(q.get(timeout=5))
+        except _q.Empty:
+            dead = [p.exitcode for p in procs if p.exitcode not in (None, 0)]
+            assert not dead, f"a rank failed (exit codes {dead})"
+            assert _t.time() < deadline, "distributed solve timed out"
+    res.sort(key=lambda t: t[0])
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
