@@ -268,6 +268,30 @@ def time_solves(torch, budget_s: float):
     return out
 
 
+def time_dist_solve(torch, dist):
+    """Distributed OMG (z-ordered row partition per level, NCCL) on the
+    serialized full-size BASELINE config-2 hierarchy, if present."""
+    from paper_2003_02431_b200.dist_solvers import dist_ortho_mg_solve
+    from paper_2003_02431_b200.hierarchy import load_hierarchy
+    from paper_2003_02431_b200.solvers import SolverConfig
+
+    path = os.path.join(ROOT, "tests", "golden", "large", "cfg2.npz")
+    if not os.path.exists(path):
+        return {"skipped": "tests/golden/large/cfg2.npz absent"}
+    z = np.load(path)
+    meta = json.loads(bytes(z["meta"]).decode())
+    hier = load_hierarchy(z)
+    dist.barrier()
+    x, (r0, r1), rep = dist_ortho_mg_solve(hier, np.asarray(hier.level(1).rhs),
+                                           SolverConfig(**meta["omg"]))
+    t = torch.tensor([rep.time_iterations], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return {"case": "large/cfg2", "solver": "omg (distributed)", "n_gpus": dist.get_world_size(),
+            "dofs_raw": meta["dofs_raw"], "iterations": rep.iterations,
+            "converged": rep.converged, "solve_s": float(t.item()),
+            "dof_per_s": meta["dofs_raw"] / float(t.item())}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -410,6 +434,14 @@ def run_ours(args):
             line["solve"] = time_solves(torch, args.solve_budget)
         except Exception as exc:  # noqa: BLE001
             line["solve_error"] = repr(exc)
+    if world > 1 and not args.no_solve:
+        # DOF/s of the full-size cfg2 OMG solve over all ranks (dist_solvers)
+        try:
+            solve = time_dist_solve(torch, dist)
+        except Exception as exc:  # noqa: BLE001
+            solve = {"error": repr(exc)}
+        if rank == 0:
+            line["solve"] = [solve]
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
             from oracle import spmv as ospmv
