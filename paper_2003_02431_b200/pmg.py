@@ -117,43 +117,27 @@ class PmgPlan:
             self.lu_off.data_ptr(), self.dims.data_ptr(), D.val_t.data_ptr(),
             A.data_ptr(), ctx.stream), "pmg_build_low")
         piv = torch.zeros(int(vec_off[-1]), dtype=I32, device=dev)
-        # factor systems of equal size as one batch; the size groups run
-        # concurrently on a pool of streams (each group is small), and the
-        # singularity check is one deferred flag read for all groups
-        main = torch.cuda.current_stream(dev)
-        ready = torch.cuda.Event()
-        ready.record(main)
-        pool = [torch.cuda.Stream(dev) for _ in range(min(8, max(1, len(np.unique(dims)))))]
+        # factor systems of equal size as one batch; the singularity check is
+        # one deferred flag read for all groups (no per-group host sync)
         bad_flags = torch.zeros(self.nsys, dtype=torch.bool, device=dev)
-        keep = []
-        for gi, n in enumerate(np.unique(dims)):
+        for n in np.unique(dims):
             idx = np.flatnonzero(dims == n)
             n = int(n)
             if n == 0:
                 continue
-            st = pool[gi % len(pool)]
-            st.wait_event(ready)
-            with torch.cuda.stream(st):
-                if len(idx) == 1:
-                    views = A[lu_off[idx[0]]:lu_off[idx[0]] + n * n].view(1, n, n)
-                else:
-                    views = torch.stack([A[lu_off[s]:lu_off[s] + n * n] for s in idx]
-                                        ).view(len(idx), n, n)
-                LU, pv, info = torch.linalg.lu_factor_ex(views)
-                dg = torch.diagonal(LU, dim1=-2, dim2=-1)
-                bad = (info != 0) | ~torch.isfinite(LU).flatten(1).all(1) | (dg == 0).any(1)
-                idx_t = torch.from_numpy(idx).to(dev)
-                bad_flags.index_copy_(0, idx_t, bad)
-                INV = triangular_inverses(LU)
-                for q, s_ in enumerate(idx):
-                    A[lu_off[s_]:lu_off[s_] + n * n] = INV[q].reshape(-1)
-                    piv[vec_off[s_]:vec_off[s_] + n] = pv[q].to(I32)
-                keep.append((views, LU, pv, INV, idx_t))  # alive until joined
-        for st in pool:
-            done = torch.cuda.Event()
-            done.record(st)
-            main.wait_event(done)
-        del keep
+            if len(idx) == 1:
+                views = A[lu_off[idx[0]]:lu_off[idx[0]] + n * n].view(1, n, n)
+            else:
+                views = torch.stack([A[lu_off[s]:lu_off[s] + n * n] for s in idx]
+                                    ).view(len(idx), n, n)
+            LU, pv, info = torch.linalg.lu_factor_ex(views)
+            dg = torch.diagonal(LU, dim1=-2, dim2=-1)
+            bad = (info != 0) | ~torch.isfinite(LU).flatten(1).all(1) | (dg == 0).any(1)
+            bad_flags.index_copy_(0, torch.from_numpy(idx).to(dev), bad)
+            INV = triangular_inverses(LU)
+            for q, s_ in enumerate(idx):
+                A[lu_off[s_]:lu_off[s_] + n * n] = INV[q].reshape(-1)
+                piv[vec_off[s_]:vec_off[s_] + n] = pv[q].to(I32)
         if bool(bad_flags.any()):
             s_bad = int(torch.nonzero(bad_flags)[0])
             cells = tuple(int(c) for c in sets[s_bad][:8])
