@@ -20,6 +20,7 @@ through the per-cell restatement.
 """
 from __future__ import annotations
 
+import os
 from functools import lru_cache
 
 import numpy as np
@@ -42,23 +43,32 @@ _EXTRA = {  # asymmetric interior probes of the linearity test (quadrature.py:33
 # ---------------------------------------------------------------------------
 # level sets (levelset.py:63-126) -- identical arithmetic
 
-def level_set(name: str, params: dict | None = None):
-    p = dict(params or {})
-    if name == "sphere":
-        c = np.asarray(p.get("center", (0.0, 0.0, 0.0)), dtype=float)
-        r2 = float(p.get("radius", 0.7)) ** 2
+class LevelSet:
+    """Picklable level-set function (worker processes evaluate it too)."""
 
-        def phi(x):
-            d = x - c
-            return np.einsum("ij,ij->i", d, d) - r2
-        return phi
-    if name == "plane":
-        n = np.asarray(p.get("normal", (1.0, 0.0, 0.0)), dtype=float)
-        off = p.get("offset", 0.0)
-        return lambda x: x @ n - off
-    if name in ("paper-benchmark", "benchmark"):
-        return lambda x: x[:, 0] ** 2 + x[:, 1] ** 2 + x[:, 2] ** 3 - 0.49
-    raise ValueError(f"unknown level set name: {name!r}")
+    def __init__(self, name: str, params: dict | None = None):
+        self.name = name
+        p = dict(params or {})
+        if name == "sphere":
+            self.c = np.asarray(p.get("center", (0.0, 0.0, 0.0)), dtype=float)
+            self.r2 = float(p.get("radius", 0.7)) ** 2
+        elif name == "plane":
+            self.n = np.asarray(p.get("normal", (1.0, 0.0, 0.0)), dtype=float)
+            self.off = p.get("offset", 0.0)
+        elif name not in ("paper-benchmark", "benchmark"):
+            raise ValueError(f"unknown level set name: {name!r}")
+
+    def __call__(self, x):
+        if self.name == "sphere":
+            d = x - self.c
+            return np.einsum("ij,ij->i", d, d) - self.r2
+        if self.name == "plane":
+            return x @ self.n - self.off
+        return x[:, 0] ** 2 + x[:, 1] ** 2 + x[:, 2] ** 3 - 0.49
+
+
+def level_set(name: str, params: dict | None = None) -> LevelSet:
+    return LevelSet(name, params)
 
 
 # ---------------------------------------------------------------------------
@@ -344,8 +354,22 @@ class CartesianMesh:
         return [sorted(x) for x in nbrs]
 
 
-def species_volumes(mesh: CartesianMesh, phi, quad_depth: int, gauss_order: int):
-    """species_volume (num_cells, 2) of classify_and_build (cutcells.py:105-127)."""
+def _cells_job(args):
+    phi, los, his, depth, order, cells = args
+    vols = np.zeros((len(cells), 2))
+    for i, j in enumerate(cells):
+        try:
+            vols[i] = cell_species_volumes(phi, los[i], his[i], depth, order)
+        except DegenerateLevelSetError as exc:
+            raise DegenerateLevelSetError(f"cell {j}: {exc}") from exc
+    return cells, vols
+
+
+def species_volumes(mesh: CartesianMesh, phi, quad_depth: int, gauss_order: int,
+                    workers: int | None = None):
+    """species_volume (num_cells, 2) of classify_and_build (cutcells.py:105-127).
+    Cut cells are spread over `workers` processes (default: all cores when
+    there are >= 64 of them); the result does not depend on the split."""
     J, dim = mesh.num_cells, mesh.dim
     lo, hi = mesh.bounds(np.arange(J))
     ref, _ = _tensor_ref(dim, gauss_order + 2)
@@ -370,11 +394,20 @@ def species_volumes(mesh: CartesianMesh, phi, quad_depth: int, gauss_order: int)
             m = float((rw * p).sum())
             cache[p] = m
         out[j, NEG if neg[j] else POS] = m
-    for j in np.flatnonzero(exact):
-        try:
-            out[j] = cell_species_volumes(phi, lo[j], hi[j], quad_depth, gauss_order)
-        except DegenerateLevelSetError as exc:
-            raise DegenerateLevelSetError(f"cell {j}: {exc}") from exc
+    todo = np.flatnonzero(exact)
+    if workers is None:
+        workers = min(os.cpu_count() or 1, 16) if len(todo) >= 64 else 1
+    if workers > 1 and len(todo) > 1:
+        from concurrent.futures import ProcessPoolExecutor
+
+        chunks = np.array_split(todo, workers * 4)
+        jobs = [(phi, lo[c], hi[c], quad_depth, gauss_order, c) for c in chunks if len(c)]
+        with ProcessPoolExecutor(max_workers=workers) as pool:
+            for cells, vols in pool.map(_cells_job, jobs):
+                out[cells] = vols
+    else:
+        _, vols = _cells_job((phi, lo[todo], hi[todo], quad_depth, gauss_order, todo))
+        out[todo] = vols
     return out
 
 
@@ -429,3 +462,44 @@ def aggregates(species_volume, edges):
     for p, i in index.items():
         groups.setdefault(root(i), []).append(p)
     return [sorted(groups[r]) for r in sorted(groups)]
+
+
+def axis_block_edges(mesh: CartesianMesh, level: int):
+    """Mesh-graph edges (a < b) inside the same axis-aligned index block of
+    width 2^(level-1), the last block per axis absorbing the remainder
+    (build_multigrid_aggregation_sequence, mesh.py:254-287)."""
+    width = 2 ** (level - 1)
+    J = mesh.num_cells
+    m = mesh.multi(np.arange(J))
+    nblocks = np.maximum(np.array(mesh.n) // width, 1)
+    blk = np.minimum(m // width, nblocks - 1)
+    strides = np.cumprod((1,) + mesh.n[:-1])
+    out = []
+    for a in range(mesh.dim):
+        src = np.flatnonzero(m[:, a] + 1 < mesh.n[a])
+        dst = src + strides[a]
+        same = np.all(blk[src] == blk[dst], axis=1)
+        out += list(zip(src[same].tolist(), dst[same].tolist()))
+    return out
+
+
+def lift_edges(bg_edges, species_volume):
+    """Background edges duplicated per species present on both cells
+    (lift_aggregation_to_cutcells, agglomeration.py:79-93)."""
+    edges = set()
+    for a, b in bg_edges:
+        for s in (NEG, POS):
+            if species_volume[a, s] > 0 and species_volume[b, s] > 0:
+                edges.add(tuple(sorted(((a, s), (b, s)))))
+    return edges
+
+
+def level_aggregates(mesh: CartesianMesh, species_volume, small_edges, num_levels: int):
+    """Aggregates of hierarchy levels 1..num_levels (build_hierarchy,
+    transfer.py:480-500): level 1 = small-cell map; level l = lifted axis
+    blocks of width 2^(l-1) united with the small-cell map."""
+    out = [aggregates(species_volume, small_edges)]
+    for lam in range(2, num_levels + 1):
+        eff = lift_edges(axis_block_edges(mesh, lam), species_volume) | set(small_edges)
+        out.append(aggregates(species_volume, eff))
+    return out

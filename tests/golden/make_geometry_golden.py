@@ -14,10 +14,15 @@ import numpy as np
 
 sys.dont_write_bytecode = True
 sys.path.insert(0, "/root/reference/pkg/src")
-from cutdg.agglomeration import cut_aggregates, small_cell_agglomeration_map  # noqa: E402
+from cutdg.agglomeration import (  # noqa: E402
+    cut_aggregates,
+    lift_aggregation_to_cutcells,
+    small_cell_agglomeration_map,
+    union_maps,
+)
 from cutdg.cutcells import classify_and_build  # noqa: E402
 from cutdg.levelset import make_level_set  # noqa: E402
-from cutdg.mesh import build_cartesian  # noqa: E402
+from cutdg.mesh import build_cartesian, build_multigrid_aggregation_sequence  # noqa: E402
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 
@@ -58,7 +63,20 @@ def run(name):
     for i, g in enumerate(aggs):
         ptr[i + 1] = ptr[i] + len(g)
         flat += [j * 2 + s for j, s in g]
-    np.savez_compressed(os.path.join(HERE, f"{name}.npz"),
+    # aggregates of hierarchy levels 2..4 (transfer.py:496-500: lifted
+    # background axis blocks of width 2^(l-1) united with the small-cell map)
+    levels = {}
+    for lam, bg in enumerate(build_multigrid_aggregation_sequence(mesh, 4)[1:], start=2):
+        eff = union_maps(lift_aggregation_to_cutcells(bg, cm), small)
+        g = cut_aggregates(eff)
+        lp = np.zeros(len(g) + 1, np.int64)
+        lf = []
+        for i, grp in enumerate(g):
+            lp[i + 1] = lp[i] + len(grp)
+            lf += [j * 2 + s for j, s in grp]
+        levels[f"L{lam}_agg_ptr"] = lp
+        levels[f"L{lam}_agg_pieces"] = np.array(lf, np.int64)
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **levels,
                         species_volume=cm.species_volume, small_edges=edges,
                         agg_ptr=ptr, agg_pieces=np.array(flat, np.int64),
                         dim=c["dim"], cells=c["cells"], degree=c["degree"],

@@ -36,11 +36,16 @@ def test_classification_and_aggregates_match_reference(case):
     edges = G.small_cell_pairs(vol, mesh.cell_volume, mesh.adjacency(), float(z["alpha"]))
     got = np.array(sorted((a[0], a[1], b[0], b[1]) for a, b in edges), np.int64).reshape(-1, 4)
     assert np.array_equal(got, z["small_edges"])
+    def unpack(ptr, flat):
+        return [[(int(p) // 2, int(p) % 2) for p in flat[ptr[i]:ptr[i + 1]]]
+                for i in range(len(ptr) - 1)]
+
     aggs = G.aggregates(vol, edges)
-    ptr, flat = z["agg_ptr"], z["agg_pieces"]
-    want = [[(int(p) // 2, int(p) % 2) for p in flat[ptr[i]:ptr[i + 1]]]
-            for i in range(len(ptr) - 1)]
-    assert aggs == want
+    assert aggs == unpack(z["agg_ptr"], z["agg_pieces"])
+    if "L2_agg_ptr" in z.files:       # multigrid levels 2..4
+        levels = G.level_aggregates(mesh, vol, edges, 4)
+        for lam in (2, 3, 4):
+            assert levels[lam - 1] == unpack(z[f"L{lam}_agg_ptr"], z[f"L{lam}_agg_pieces"]), lam
 
 
 def test_degenerate_level_set_raises():
