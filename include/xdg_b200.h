@@ -188,6 +188,15 @@ int xdg_pmg_combine(int nbr, int N, const int* cptr, const int64_t* cpos,
                     const double* out, const double* damping, double* z,
                     xdg_stream_t stream);
 
+/* ---- Galerkin coarse operator (transfer.py:344-351) -------------------- */
+/* Mc = R^T M R where R has one block per fine row.  Output block o of Mc
+ * accumulates, in order, the terms t in [tptr[o], tptr[o+1]):
+ *   R[t_ri[t]]^T  M[t_e[t]]  R[t_rk[t]]   (all blocks column-major, N <= 64).
+ * One CTA per output block; deterministic. */
+int xdg_galerkin(int nout, int N, const int* tptr, const int* t_e,
+                 const int* t_ri, const int* t_rk, const double* Mv,
+                 const double* Rv, double* Cv, xdg_stream_t stream);
+
 /* ======================================================================
  * Native solver driver (the reference's control loops, solvers.py:559-846,
  * run in C++ over device data: one host sync per rm_step / GMRES inner
