@@ -268,6 +268,62 @@ def time_solves(torch, budget_s: float):
     return out
 
 
+def time_matops(torch):
+    """The paper's Table-2 instance (6^3 cells, k=5, benchmark surface): SpMV
+    and the Galerkin product R0^T M R0 (micro_bench_matops, bench.py:326-352),
+    next to the published BoSSS numbers and the
+    reference timings recorded when the fixture was generated."""
+    from paper_2003_02431_b200.blockmatrix import BlockSparseMatrix, uniform_layout
+    from paper_2003_02431_b200.hierarchy import fixture_array
+    from paper_2003_02431_b200.transfer import galerkin_device, galerkin_restrict
+
+    path = os.path.join(ROOT, "tests", "golden", "large", "matops_6_k5.npz")
+    if not os.path.exists(path):
+        return {"skipped": "tests/golden/large/matops_6_k5.npz absent"}
+    z = np.load(path)
+
+    def mat(prefix):
+        rp = z[prefix + "_row_ptr"]
+        val = fixture_array(z, prefix + "_val")
+        N = val.shape[1]
+        return BlockSparseMatrix.from_bsr(rp, z[prefix + "_col"], val,
+                                          uniform_layout(len(rp) - 1, N),
+                                          uniform_layout(int(z[prefix + "_ncols"]), N))
+
+    M, R0 = mat("M"), mat("R0")
+    D = M.device()
+    v = torch.ones(D.nbc * D.N, dtype=torch.float64, device="cuda")
+    y = D.spmv(v)
+
+    def events(fn, reps):
+        ts = []
+        for _ in range(reps):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            fn()
+            e.record()
+            e.synchronize()
+            ts.append(s.elapsed_time(e))
+        return statistics.median(ts)
+
+    events(lambda: D.spmv(v, y), 3)
+    spmv_ms = events(lambda: D.spmv(v, y), 20)
+    galerkin_device(M, R0)
+    gal_dev_ms = events(lambda: galerkin_device(M, R0), 5)
+    t0 = time.perf_counter()
+    galerkin_restrict(M, None, R0)
+    gal_api_ms = 1e3 * (time.perf_counter() - t0)
+    return {"instance": "6^3 cells, k=5 (N=56), paper benchmark surface",
+            "nonzero_rows": int(z["nonzero_rows"]),
+            "matvec_ms": spmv_ms, "matvec_GBs": D.algorithmic_bytes() / spmv_ms / 1e6,
+            "matmat_device_ms": gal_dev_ms, "matmat_api_ms": gal_api_ms,
+            "reference_cpu_build_container_ms": {"matvec": float(z["matvec_ms"]),
+                                                 "matmat": float(z["matmat_ms"])},
+            "published_bosss_ms": {"matvec_1core_i7": 14.6, "matvec_4core_i7": 8.99,
+                                   "matmat_1core_i7": 3880.0, "matmat_4core_i7": 1293.0,
+                                   "source": "PAPER.md:1328-1338 (24,192 rows)"}}
+
+
 def time_dist_solve(torch, dist):
     """Distributed OMG (z-ordered row partition per level, NCCL) on the
     serialized full-size BASELINE config-2 hierarchy, if present."""
@@ -434,6 +490,10 @@ def run_ours(args):
             line["solve"] = time_solves(torch, args.solve_budget)
         except Exception as exc:  # noqa: BLE001
             line["solve_error"] = repr(exc)
+        try:
+            line["matops"] = time_matops(torch)
+        except Exception as exc:  # noqa: BLE001
+            line["matops"] = {"error": repr(exc)}
     if world > 1 and not args.no_solve:
         # DOF/s of the full-size cfg2 OMG solve over all ranks (dist_solvers)
         try:
