@@ -201,9 +201,17 @@ cudaError_t dispatch_n(int rb, int re, int N, const int* rp, const int* col,
 #define XDG_F(NN) \
   case NN:        \
     return launch_flat<NN, MODE, NORM>(rb, re, N, rp, col, val, x, y, a, bt, b, nrm, ws, s);
+#ifndef XDG_SPMV_FLAT20
+#define XDG_SPMV_FLAT20 0
+#endif
   switch (N) {
     XDG_W(1) XDG_W(2) XDG_W(3) XDG_W(4) XDG_W(6) XDG_W(10) XDG_W(15)
-    XDG_W(20) XDG_W(21) XDG_W(28)
+#if XDG_SPMV_FLAT20
+    XDG_F(20)
+#else
+    XDG_W(20)
+#endif
+    XDG_W(21) XDG_W(28)
     XDG_F(35) XDG_F(56)
     default:
       if (N <= 32) break;

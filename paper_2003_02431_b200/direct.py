@@ -38,6 +38,51 @@ def lu_factor_dense(A: torch.Tensor, what: str = "matrix"):
     return LU, piv
 
 
+class _quiet_stdout:
+    """Silence C-level stdout (MAGMA prints an advisory banner for batched
+    getrf); flushes libc's buffer before restoring so nothing leaks into the
+    one-line JSON contract of bench.py."""
+
+    def __enter__(self):
+        import ctypes
+        import os
+        import sys
+
+        sys.stdout.flush()
+        self._libc = ctypes.CDLL(None)
+        self._libc.fflush(None)
+        self._saved = os.dup(1)
+        self._null = os.open(os.devnull, os.O_WRONLY)
+        os.dup2(self._null, 1)
+        return self
+
+    def __exit__(self, *exc):
+        import os
+
+        self._libc.fflush(None)
+        os.dup2(self._saved, 1)
+        os.close(self._saved)
+        os.close(self._null)
+
+
+def lu_factor_batched(A: torch.Tensor):
+    """Partial-pivoting LU of a batch (b, n, n): MAGMA's batched getrf when
+    the batch is large enough to pay off (5-17x faster per matrix than
+    looping cuSOLVER at n = 512..1300, measured by tools/bench_setup_lu.py),
+    cuSOLVER otherwise.  Returns (LU, pivots, info)."""
+    if A.dim() == 3 and A.shape[0] >= 4:
+        prev = torch.backends.cuda.preferred_linalg_library()
+        torch.backends.cuda.preferred_linalg_library("magma")
+        try:
+            with _quiet_stdout():
+                out = torch.linalg.lu_factor_ex(A)
+                torch.cuda.synchronize(A.device)
+        finally:
+            torch.backends.cuda.preferred_linalg_library(prev)
+        return out
+    return torch.linalg.lu_factor_ex(A)
+
+
 def ipiv_to_perm(ctx, piv: torch.Tensor, dims: torch.Tensor,
                  vec_off: torch.Tensor) -> torch.Tensor:
     perm = torch.empty(piv.numel(), dtype=I32, device=ctx.device)

@@ -117,27 +117,35 @@ class PmgPlan:
             self.lu_off.data_ptr(), self.dims.data_ptr(), D.val_t.data_ptr(),
             A.data_ptr(), ctx.stream), "pmg_build_low")
         piv = torch.zeros(int(vec_off[-1]), dtype=I32, device=dev)
-        # factor systems of equal size as one batch; the singularity check is
-        # one deferred flag read for all groups (no per-group host sync)
+        # factor the systems in size buckets: each bucket is padded with
+        # identity to a common size P (the LU / triangular inverses of
+        # diag(A, I) are diag(LU_A, I) -- padding rows hold zeros in A's
+        # columns so partial pivoting never selects them), batched (MAGMA
+        # for batches >= 4), and the top-left n x n blocks copied back.  One
+        # deferred singularity check for all systems.
         bad_flags = torch.zeros(self.nsys, dtype=torch.bool, device=dev)
-        for n in np.unique(dims):
-            idx = np.flatnonzero(dims == n)
-            n = int(n)
-            if n == 0:
+        pad_to = np.where(dims <= 64, dims, ((dims + 127) // 128) * 128)
+        for P in np.unique(pad_to):
+            idx = np.flatnonzero(pad_to == P)
+            P = int(P)
+            if P == 0:
                 continue
-            if len(idx) == 1:
-                views = A[lu_off[idx[0]]:lu_off[idx[0]] + n * n].view(1, n, n)
-            else:
-                views = torch.stack([A[lu_off[s]:lu_off[s] + n * n] for s in idx]
-                                    ).view(len(idx), n, n)
-            LU, pv, info = torch.linalg.lu_factor_ex(views)
-            dg = torch.diagonal(LU, dim1=-2, dim2=-1)
-            bad = (info != 0) | ~torch.isfinite(LU).flatten(1).all(1) | (dg == 0).any(1)
-            bad_flags.index_copy_(0, torch.from_numpy(idx).to(dev), bad)
-            INV = triangular_inverses(LU)
-            for q, s_ in enumerate(idx):
-                A[lu_off[s_]:lu_off[s_] + n * n] = INV[q].reshape(-1)
-                piv[vec_off[s_]:vec_off[s_] + n] = pv[q].to(I32)
+            for c0 in range(0, len(idx), max(1, (1 << 31) // (8 * P * P))):
+                chunk = idx[c0:c0 + max(1, (1 << 31) // (8 * P * P))]
+                batch = torch.eye(P, dtype=F64, device=dev).repeat(len(chunk), 1, 1)
+                for q, s_ in enumerate(chunk):
+                    n = int(dims[s_])
+                    batch[q, :n, :n] = A[lu_off[s_]:lu_off[s_] + n * n].view(n, n)
+                LU, pv, info = lu_factor_batched(batch)
+                dg = torch.diagonal(LU, dim1=-2, dim2=-1)
+                bad = (info != 0) | ~torch.isfinite(LU).flatten(1).all(1) | (dg == 0).any(1)
+                bad_flags.index_copy_(0, torch.from_numpy(chunk).to(dev), bad)
+                INV = triangular_inverses(LU)
+                for q, s_ in enumerate(chunk):
+                    n = int(dims[s_])
+                    A[lu_off[s_]:lu_off[s_] + n * n] = INV[q, :n, :n].reshape(-1)
+                    piv[vec_off[s_]:vec_off[s_] + n] = pv[q, :n].to(I32)
+                del batch, LU, INV
         if bool(bad_flags.any()):
             s_bad = int(torch.nonzero(bad_flags)[0])
             cells = tuple(int(c) for c in sets[s_bad][:8])

@@ -9,11 +9,11 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-VARIANTS = [(1, 1), (2, 2), (3, 3), (4, 4), (2, 1), (4, 2)]
+VARIANTS = [(3, 3, 0), (3, 3, 1), (3, 2, 1), (3, 4, 1)]
 
 
-def build(small, large):
-    out = f"/tmp/xdg_tune_{small}_{large}"
+def build(small, large, flat20=0):
+    out = f"/tmp/xdg_tune_{small}_{large}_{flat20}"
     os.makedirs(out, exist_ok=True)
     lib = os.path.join(out, "libxdg_b200.so")
     srcs = [os.path.join(ROOT, "paper_2003_02431_b200", "csrc", f) for f in
@@ -22,6 +22,7 @@ def build(small, large):
     subprocess.run(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a",
                     "-O3", "-std=c++17", "--shared", "-Xcompiler", "-fPIC", "--threads", "0",
                     f"-DXDG_SPMV_MINB_SMALL={small}", f"-DXDG_SPMV_MINB_LARGE={large}",
+                    f"-DXDG_SPMV_FLAT20={flat20}",
                     "-I", os.path.join(ROOT, "include"), "-o", lib, *srcs], check=True)
     return lib
 
@@ -62,9 +63,9 @@ if __name__ == "__main__":
     if "--measure" in sys.argv:
         measure()
     else:
-        for sm, lg in VARIANTS:
-            lib = build(sm, lg)
+        for sm, lg, f20 in VARIANTS:
+            lib = build(sm, lg, f20)
             out = subprocess.run([sys.executable, __file__, "--measure"], capture_output=True,
                                  text=True, env=dict(os.environ, XDG_LIB=lib))
-            print(f"MINB small={sm} large={lg}:", out.stdout.strip().splitlines()[-1]
+            print(f"MINB small={sm} large={lg} flat20={f20}:", out.stdout.strip().splitlines()[-1]
                   if out.stdout.strip() else out.stderr[-500:], flush=True)
