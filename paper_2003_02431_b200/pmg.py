@@ -21,7 +21,7 @@ import numpy as np
 import torch
 
 from . import _native as nat
-from .direct import ipiv_to_perm, lu_factor_dense, triangular_inverses
+from .direct import ipiv_to_perm, lu_factor_batched, triangular_inverses
 from .errors import SingularSystemError
 
 F64 = torch.float64
