@@ -15,11 +15,7 @@ from typing import Optional
 
 import numpy as np
 
-from .errors import (
-    DimensionMismatchError,
-    LayoutMismatchError,
-    SingularSystemError,
-)
+from .errors import DimensionMismatchError, LayoutMismatchError
 
 
 @dataclass(frozen=True)
@@ -95,10 +91,6 @@ class BlockSparseMatrix:
             self._blocks = d
             self._bsr = None
         return self._blocks
-
-    def _invalidate(self):
-        self._dev = None
-        self._bsr_sorted = None
 
     @property
     def shape(self) -> tuple:

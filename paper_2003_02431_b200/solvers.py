@@ -2,18 +2,23 @@
 running on the B200.
 
 Same public names, signatures, defaults, error classes and report
-semantics as the reference; host Python keeps the control flow (restarts,
-accept/reject, Givens rotations -- scalar work) while every vector-sized
-operation runs in libxdg_b200.so on device-resident data:
+semantics as the reference.  Python builds the device plans (setup, counted
+inside `time_iterations` like the reference's lazy factorisations); the
+iteration loops run in the native C++ driver of libxdg_b200.so, which makes
+the reference's scalar decisions (dependent candidate, accept/reject,
+Givens, convergence) on the host and launches every vector operation as a
+kernel:
 
-  pmg_apply / schwarz_apply   -> pmg.PmgPlan (batched LU solves + fused
-                                 high-order residual/solve + ordered combine)
-  rm_step / RmState           -> SpMV with fused norm, W^T w / W c kernels,
-                                 fused exact-image update
-  ortho_mg_solve              -> recursion over device level mirrors;
-                                 R, R^T products are BSR SpMVs
-  gmres_pmg_solve             -> MGS with device scalars, one host sync per
-                                 inner iteration (the Hessenberg column)
+  pmg_apply / schwarz_apply   -> pmg.PmgPlan -> xdg_pmg_apply_op (triangular-
+                                 inverse LU applies + fused high-order
+                                 residual/solve + ordered combine)
+  rm_step / RmState           -> xdg_rm_step (SpMV with fused norm, W^T w /
+                                 W c kernels, fused exact-image update; one
+                                 host sync per step)
+  ortho_mg_solve              -> xdg_omg_solve (recursion over the level
+                                 structs; R, R^T products are BSR SpMVs)
+  gmres_pmg_solve             -> xdg_gmres_solve (cooperative fused MGS, one
+                                 host sync per inner iteration)
 
 Public functions accept numpy arrays (returning numpy, like the reference)
 or CUDA tensors (returning CUDA tensors, zero-copy for device callers).
@@ -35,11 +40,11 @@ from .blockmatrix import as_block_sparse
 from .device import Context, DeviceBSR
 from .direct import DirectFactorization, direct_factor
 from .driver import RmBuffers, XdgOmgLevel, bsr_struct, direct_struct, pmg_struct
+from ._native import check as nat_check
 from .errors import (
     DimensionMismatchError,
     InvalidConfigError,
     LayoutMismatchError,
-    SingularSystemError,
 )
 from .pmg import PmgPlan
 from .schwarz import SchwarzPartition, schwarz_partition
@@ -190,10 +195,6 @@ def _device_operator(M, ctx: Context) -> DeviceBSR:
     n = A.shape[0]
     return DeviceBSR.from_arrays(np.array([0, 1]), np.array([0]),
                                  A.reshape(1, n, n), n, 1, ctx)
-
-
-def _sync_read(t: torch.Tensor) -> np.ndarray:
-    return t.cpu().numpy()
 
 
 # ---------------------------------------------------------------------------
@@ -360,12 +361,6 @@ class RmState:
         """Collapse the space onto the current point (solvers.py:548-556)."""
         nat_check(self._ctx.lib.xdg_rm_restart(C.byref(self._buf.s), self._ctx.stream),
                   "rm_restart")
-
-
-def nat_check(status, what):
-    from . import _native as nat
-
-    nat.check(status, what)
 
 
 def rm_step(state: RmState, z_candidate, M) -> tuple:
