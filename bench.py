@@ -36,6 +36,28 @@ METRIC = "XDG multigrid-GMRES DOF/s per solve; block-SpMV GB/s vs HBM peak"
 NOMINAL_HBM_GBS = 8000.0
 
 
+def ncu_traffic(kernel_substr: str = "spmv_warp_rows<10"):
+    """dram read+write bytes per launch of the dominant kernel from the
+    committed `ncu --set full` capture (profiles/), or None."""
+    import csv
+
+    path = os.path.join(ROOT, "profiles", "r1_spmv_ncu_raw_v2.csv")
+    try:
+        rows = list(csv.reader(open(path)))
+        h, units = rows[0], rows[1]
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        for r in rows[2:]:
+            if kernel_substr in r[h.index("Kernel Name")]:
+                tot = 0.0
+                for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                    i = h.index(m)
+                    tot += float(r[i]) * scale[units[i]]
+                return tot
+    except Exception:  # noqa: BLE001
+        return None
+    return None
+
+
 def measured_peak():
     for p in (os.path.join(ROOT, "MEASURED_PEAKS.json"),):
         try:
@@ -477,7 +499,9 @@ def run_ours(args):
                          "frac_of_nominal_8TBs": achieved / NOMINAL_HBM_GBS,
                          "kernel": "xdg spmv_warp_rows<10>",
                          "kernel_ms": kern_ms, "bytes_per_launch": B_local,
-                         "traffic": None},
+                         "traffic": ncu_traffic() if args.n == 128 and world == 1 else None,
+                         "traffic_source": "profiles/r1_spmv_ncu_raw_v2.csv (ncu --set full, "
+                                           "same command, dram__bytes_read+write per launch)"},
             "e2e": {"value": e2e_val, "unit": "GB/s",
                     "h2d_bytes_per_step": 8 * nloc * N, "d2h_bytes_per_step": 8 * nloc * N,
                     "path": "pinned host x -> H2D -> xdg_bsr_spmv (C-ABI) -> D2H y"},
