@@ -197,6 +197,17 @@ int xdg_galerkin(int nout, int N, const int* tptr, const int* t_e,
                  const int* t_ri, const int* t_rk, const double* Mv,
                  const double* Rv, double* Cv, xdg_stream_t stream);
 
+/* ---- SIP-DG raw operator formation (assembly.py:255-367) -------------- */
+/* out[o] = sum_{t in [tptr[o],tptr[o+1])} coef[t] * tables[tid[t]]
+ *        + sum_{d in [dptr[o],dptr[o+1])} dense[didx[d]]
+ * All blocks N x N column-major; one warp per output block; deterministic.
+ * Replaces the per-block add_block accumulation of assemble_sip
+ * (assembly.py:271-367, blockmatrix.py:65-76). */
+int xdg_assemble_blocks(int nout, int N, const int* tptr, const int* tid,
+                        const double* coef, const double* tables, const int* dptr,
+                        const int* didx, const double* dense, double* out,
+                        xdg_stream_t stream);
+
 /* ======================================================================
  * Native solver driver (the reference's control loops, solvers.py:559-846,
  * run in C++ over device data: one host sync per rm_step / GMRES inner

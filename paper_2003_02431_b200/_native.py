@@ -54,6 +54,7 @@ SIGNATURES = {
     "xdg_pmg_high": (_i32, [_i32, _i32, _i32] + [_vp] * 15),
     "xdg_pmg_combine": (_i32, [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp]),
     "xdg_galerkin": (_i32, [_i32, _i32] + [_vp] * 8),
+    "xdg_assemble_blocks": (_i32, [_i32, _i32] + [_vp] * 9),
     "xdg_rm_step": (_i32, [_vp, _vp, _vp, _vp]),
     "xdg_rm_normalize": (_i32, [_i64, _vp, _vp, _vp, _vp]),
     "xdg_rm_commit": (_i32, [_i64] + [_vp] * 9),

@@ -67,8 +67,19 @@ class BlockSparseMatrix:
         self.row_layout = row_layout
         self.col_layout = col_layout
         self._blocks: Optional[dict] = {}
+        self._host_fn = None
         self._bsr = None  # (row_ptr, col, val) host arrays, sorted
         self._dev = None
+
+    @property
+    def _bsr(self):
+        if self._bsr_data is None and self._host_fn is not None:
+            self._bsr_data, self._host_fn = self._host_fn(), None
+        return self._bsr_data
+
+    @_bsr.setter
+    def _bsr(self, value):
+        self._bsr_data = value
 
     # ---- construction ----------------------------------------------------
     @classmethod
@@ -78,6 +89,17 @@ class BlockSparseMatrix:
         M._blocks = None
         M._bsr = (np.asarray(row_ptr, np.int64), np.asarray(col, np.int64),
                   np.asarray(val, np.float64))
+        return M
+
+    @classmethod
+    def from_device(cls, dev, row_layout: BlockLayout,
+                    col_layout: BlockLayout) -> "BlockSparseMatrix":
+        """Wrap a DeviceBSR built in HBM (assembly, Galerkin products); the
+        host arrays are copied back only if something asks for them."""
+        M = cls(row_layout, col_layout)
+        M._blocks = None
+        M._host_fn = dev.to_host_rowmajor
+        M._dev, M._dev_pad = dev, None
         return M
 
     @property

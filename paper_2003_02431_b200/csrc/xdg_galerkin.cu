@@ -7,9 +7,12 @@
 // R_i^T M_ik R_k to the coarse block (parent(i), parent(k)).  The host builds
 // the output pattern and, per output block, its term list sorted by (i, k);
 // this kernel runs one CTA per output block and accumulates the terms in that
-// order (deterministic, no atomics).  Per term: stage M_ik, R_k and R_i^T in
-// shared memory, P = M_ik R_k, acc += R_i^T P.  Compute: 4 N^3 flops per
-// term; bytes: 3 N^2 doubles read per term + N^2 written per output block.
+// order (deterministic, no atomics).  Same association as the reference's
+// bs_matmat(R^T, bs_matmat(M, R)): per fine row i the products M_ik R_k are
+// summed first (P_i), then acc += R_i^T P_i -- with the large carrier
+// coefficients of small cut pieces, forming R_i^T M_ik R_k term by term
+// cancels far worse.  Compute <= 4 N^3 flops per term; bytes: 2 N^2 doubles
+// read per term + N^2 per fine row + N^2 written per output block.
 // All blocks column-major (BSR-T).
 #include "xdg_common.cuh"
 
@@ -31,17 +34,44 @@ galerkin_kernel(int nout, int N, const int* __restrict__ tptr,
   double* Ct = sm + 2 * NN;  // R_i^T     Ct[c*N + a] = R_i(c, a)
   double* P = sm + 3 * NN;   // M_ik R_k  column-major
   const int o = blockIdx.x;
-  double acc[kGMaxOwn];
+  double acc[kGMaxOwn], pac[kGMaxOwn];
 #pragma unroll
-  for (int q = 0; q < kGMaxOwn; ++q) acc[q] = 0.0;
-  for (int t = tptr[o]; t < tptr[o + 1]; ++t) {
+  for (int q = 0; q < kGMaxOwn; ++q) acc[q] = pac[q] = 0.0;
+  const int tb = tptr[o], te = tptr[o + 1];
+  for (int t = tb; t < te; ++t) {
     const double* Me = Mv + (int64_t)t_e[t] * NN;
     const double* Rk = Rv + (int64_t)t_rk[t] * NN;
-    const double* Ri = Rv + (int64_t)t_ri[t] * NN;
     __syncthreads();
     for (int x = threadIdx.x; x < NN; x += kGT) {
       A[x] = Me[x];
       B[x] = Rk[x];
+    }
+    __syncthreads();
+    // P_i += M_ik R_k   (reference order: (M R) first, blockmatrix.py:132-150)
+#pragma unroll
+    for (int q = 0; q < kGMaxOwn; ++q) {
+      const int x = threadIdx.x + q * kGT;
+      if (x < NN) {
+        const int b = x / N, a = x - b * N;
+        double s = 0.0;
+        for (int c = 0; c < N; ++c) s = fma(A[c * N + a], B[b * N + c], s);
+        pac[q] += s;
+      }
+    }
+    const int ri = t_ri[t];
+    if (t + 1 < te && t_ri[t + 1] == ri) continue;
+    // last term of fine row i: acc += R_i^T P_i
+    const double* Ri = Rv + (int64_t)ri * NN;
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < kGMaxOwn; ++q) {
+      const int x = threadIdx.x + q * kGT;
+      if (x < NN) {
+        P[x] = pac[q];
+        pac[q] = 0.0;
+      }
+    }
+    for (int x = threadIdx.x; x < NN; x += kGT) {
       const int a = x / N, c = x - a * N;  // Ri column-major: x = a*N + c
       Ct[c * N + a] = Ri[x];
     }
@@ -52,19 +82,8 @@ galerkin_kernel(int nout, int N, const int* __restrict__ tptr,
       if (x < NN) {
         const int b = x / N, a = x - b * N;
         double s = 0.0;
-        for (int c = 0; c < N; ++c) s = fma(A[c * N + a], B[b * N + c], s);
-        P[x] = s;
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < kGMaxOwn; ++q) {
-      const int x = threadIdx.x + q * kGT;
-      if (x < NN) {
-        const int b = x / N, a = x - b * N;
-        double s = acc[q];
         for (int c = 0; c < N; ++c) s = fma(Ct[c * N + a], P[b * N + c], s);
-        acc[q] = s;
+        acc[q] += s;
       }
     }
   }

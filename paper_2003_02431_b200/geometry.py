@@ -12,7 +12,10 @@ clipping, section polygons, fan triangulation into Duffy triangles /
 tetrahedra with the sliver filter -- and forms each rule's weight arrays with
 the same floating-point operations, so `species_volume` is the reference's
 to the last bit (tests/test_geometry.py pins it against rules the reference
-built).  Node coordinates, normals and face rules are not formed.
+built).  The recursion takes an accumulator: `_Measure` keeps weights only;
+cutcells._Rules also forms node coordinates and interface rules (same
+operations as the reference's map_triangle / map_tet / tensor_rule), which
+the SIP assembly consumes.
 
 Pure cells are classified for the whole mesh at once (vectorised probes);
 cells whose probe values come within 1e-9 of zero, and all cut cells, go
@@ -65,6 +68,48 @@ class LevelSet:
         if self.name == "plane":
             return x @ self.n - self.off
         return x[:, 0] ** 2 + x[:, 1] ** 2 + x[:, 2] ** 3 - 0.49
+
+    def gradient(self, x):
+        """Analytic gradients (levelset.py:75-108)."""
+        if self.name == "sphere":
+            return 2.0 * (x - self.c)
+        if self.name == "plane":
+            return np.broadcast_to(self.n, x.shape).copy()
+        g = np.empty_like(x)
+        g[:, 0] = 2 * x[:, 0]
+        g[:, 1] = 2 * x[:, 1]
+        g[:, 2] = 3 * x[:, 2] ** 2
+        return g
+
+    def unit_normal(self, x):
+        """grad(phi)/|grad(phi)|, NEG -> POS (levelset.py:52-57)."""
+        g = self.gradient(x)
+        norms = np.linalg.norm(g, axis=1, keepdims=True)
+        norms[norms == 0] = 1.0
+        return g / norms
+
+
+class UnionLevelSet:
+    """min of several level sets: NEG inside any of them (e.g. the two
+    spheres of BASELINE config 4).  The reference expresses such a field as a
+    user LevelSet(phi, grad) (levelset.py:19-35); this is that field."""
+
+    def __init__(self, parts):
+        self.parts = list(parts)
+        self.name = "union"
+
+    def _vals(self, x):
+        return np.stack([p(x) for p in self.parts])
+
+    def __call__(self, x):
+        return self._vals(x).min(axis=0)
+
+    def gradient(self, x):
+        k = self._vals(x).argmin(axis=0)
+        g = np.stack([p.gradient(x) for p in self.parts])
+        return g[k, np.arange(len(x))]
+
+    unit_normal = LevelSet.unit_normal
 
 
 def level_set(name: str, params: dict | None = None) -> LevelSet:
@@ -218,14 +263,21 @@ def _section(lo, hi, c0, c):
 
 
 class _Measure:
-    """Weight arrays per species in the reference's accumulation order."""
+    """Weight arrays per species in the reference's accumulation order.  The
+    `nodes` callables are only invoked by accumulators that keep nodes
+    (cutcells._Rules); measures never build coordinates."""
+
+    want_interface = False
 
     def __init__(self):
         self.w = {NEG: [], POS: []}
 
-    def add(self, s, weights):
+    def add(self, s, weights, nodes=None):
         if len(weights):
             self.w[s].append(weights)
+
+    def add_interface(self, weights, nodes):
+        pass
 
     def measure(self, s) -> float:
         if not self.w[s]:
@@ -233,10 +285,50 @@ class _Measure:
         return float(np.concatenate(self.w[s]).sum())
 
 
-def _clip_leaf(lo, hi, c0, c, order, acc: _Measure):
+@lru_cache(maxsize=None)
+def _tri_nodes(order: int) -> np.ndarray:
+    """Duffy nodes of the unit triangle (quadrature.py:93-103)."""
+    x, _ = np.polynomial.legendre.leggauss(order)
+    u = 0.5 * (x + 1)
+    U, V = np.meshgrid(u, u, indexing="ij")
+    return np.stack([U.ravel(), (V * (1 - U)).ravel()], axis=1)
+
+
+@lru_cache(maxsize=None)
+def _tet_nodes(order: int) -> np.ndarray:
+    """Duffy nodes of the unit tetrahedron (quadrature.py:106-121)."""
+    x, _ = np.polynomial.legendre.leggauss(order)
+    u = 0.5 * (x + 1)
+    U, V, W = np.meshgrid(u, u, u, indexing="ij")
+    return np.stack([U.ravel(), (V * (1 - U)).ravel(), (W * (1 - U) * (1 - V)).ravel()], axis=1)
+
+
+def _box_nodes(lo, hi, order):
+    ref, _ = _tensor_ref(len(lo), order)
+    return 0.5 * (hi + lo) + ref * (0.5 * (hi - lo))
+
+
+def _tri_map(p0, e1, e2, order):
+    r = _tri_nodes(order)
+    return p0 + np.outer(r[:, 0], e1) + np.outer(r[:, 1], e2)
+
+
+def _clip_leaf(lo, hi, c0, c, order, acc):
+    """Exact rules of a box cut by the plane c0 + c.x = 0
+    (_clip_box_rules, quadrature.py:366-437)."""
     dim = len(lo)
     if float(np.linalg.norm(c)) < 1e-300:
-        acc.add(NEG if c0 < 0 else POS, _box_weights(lo, hi, order))
+        acc.add(NEG if c0 < 0 else POS, _box_weights(lo, hi, order),
+                lambda: _box_nodes(lo, hi, order))
+        return
+    if dim == 1:
+        root = min(max(-c0 / c[0], lo[0]), hi[0])
+        lo_s = NEG if c[0] > 0 else POS
+        for s, (a, b) in ((lo_s, (lo[0], root)), (1 - lo_s, (root, hi[0]))):
+            if b - a > SLIVER_REL_TOL * (hi[0] - lo[0]):
+                al, bl = np.array([a]), np.array([b])
+                acc.add(s, _box_weights(al, bl, order),
+                        lambda al=al, bl=bl: _box_nodes(al, bl, order))
         return
     if dim == 2:
         ring = np.array([[lo[0], lo[1]], [hi[0], lo[1]], [hi[0], hi[1]], [lo[0], hi[1]]])
@@ -249,7 +341,25 @@ def _clip_leaf(lo, hi, c0, c, order, acc: _Measure):
                 e1, e2 = poly[i] - poly[0], poly[i + 1] - poly[0]
                 wts = tw * abs(e1[0] * e2[1] - e1[1] * e2[0])
                 if wts.sum() > SLIVER_REL_TOL * area:
-                    acc.add(s, wts)
+                    acc.add(s, wts, lambda p0=poly[0], e1=e1, e2=e2: _tri_map(p0, e1, e2, order))
+        if acc.want_interface:
+            vals = c0 + ring @ c
+            pts = []
+            for i in range(4):
+                va, vb = vals[i], vals[(i + 1) % 4]
+                a, b = ring[i], ring[(i + 1) % 4]
+                if (va < 0 < vb) or (vb < 0 < va):
+                    t = va / (va - vb)
+                    pts.append(a + t * (b - a))
+            if len(pts) >= 2:
+                pts = np.array(pts)
+                proj = pts @ np.array([-c[1], c[0]])
+                p0, p1 = pts[np.argmin(proj)], pts[np.argmax(proj)]
+                length = float(np.linalg.norm(p1 - p0))
+                if length > SLIVER_REL_TOL * float(np.linalg.norm(hi - lo)):
+                    x1, w1 = np.polynomial.legendre.leggauss(order)
+                    acc.add_interface(0.5 * w1 * length,
+                                      lambda: p0 + np.outer(0.5 * (x1 + 1), p1 - p0))
         return
     vol = float(np.prod(hi - lo))
     diam = float(np.linalg.norm(hi - lo))
@@ -270,15 +380,23 @@ def _clip_leaf(lo, hi, c0, c, order, acc: _Measure):
                 B = np.stack([poly[0] - apex, poly[i] - apex, poly[i + 1] - apex], axis=1)
                 wts = tw * abs(np.linalg.det(B))
                 if wts.sum() > SLIVER_REL_TOL * vol:
-                    acc.add(s, wts)
+                    acc.add(s, wts, lambda B=B, apex=apex: apex + _tet_nodes(order) @ B.T)
+    if acc.want_interface and len(sec) >= 3:
+        tw2 = _tri_weights(order)
+        for i in range(1, len(sec) - 1):
+            e1, e2 = sec[i] - sec[0], sec[i + 1] - sec[0]
+            wts = tw2 * float(np.linalg.norm(np.cross(e1, e2)))
+            if wts.sum() > SLIVER_REL_TOL * diam ** 2:
+                acc.add_interface(wts, lambda p0=sec[0], e1=e1, e2=e2: _tri_map(p0, e1, e2, order))
 
 
-def _recurse(phi, lo, hi, depth, order, leaf_order, acc: _Measure):
+def _recurse(phi, lo, hi, depth, order, leaf_order, acc):
     cls = _probe_class(phi(_probes(lo, hi, order)))
     if cls == "zero":
         return
     if cls in ("neg", "pos"):
-        acc.add(NEG if cls == "neg" else POS, _box_weights(lo, hi, order))
+        acc.add(NEG if cls == "neg" else POS, _box_weights(lo, hi, order),
+                lambda: _box_nodes(lo, hi, order))
         return
     corners = _corners(lo, hi)
     cvals = phi(corners)
