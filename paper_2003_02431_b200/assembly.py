@@ -230,6 +230,14 @@ def penalty_inv_h(cm: CutCellMesh, pidx: PieceIndex, groups) -> np.ndarray:
     return inv
 
 
+def _stiffness(weights, G):
+    """sum_p w_p G_p G_p^T (the einsum "p,pid,pld->il" of assembly.py:275)
+    as one GEMM over the (point, axis) pairs."""
+    P, N, D = G.shape
+    Gt = G.transpose(1, 0, 2).reshape(N, P * D)
+    return (Gt * np.repeat(weights, D)[None, :]) @ Gt.T
+
+
 def _pair_terms(weights, eta, mu_pen, sides):
     """assembly.py:236-252."""
     n = len(sides)
@@ -241,6 +249,58 @@ def _pair_terms(weights, eta, mu_pen, sides):
             out[(a, b)] = (-mean * sa * Wa.T @ Gnb - mean * sb * (Gna * weights[:, None]).T @ Vb
                            + eta * mu_pen * sa * sb * Wa.T @ Vb)
     return out
+
+
+# ---------------------------------------------------------------------------
+# cut items: per-item dense blocks with the reference's operations
+
+def _eval_item(item):
+    from ._pool import STATE
+
+    cm, basis, problem = STATE["cm"], STATE["basis"], STATE["problem"]
+    mesh = cm.mesh
+    kind = item[0]
+    if kind == "vol":
+        _, b, j, s = item
+        rule = quad_volume(cm, j, s)
+        V, G = basis.eval_with_grad(*mesh.bounds(j), rule.nodes)
+        return ([(b, b, problem.mu(s) * _stiffness(rule.weights, G))],
+                [(b, V.T @ (rule.weights * problem.source(rule.nodes)))])
+    if kind == "face":
+        _, fid, s, a, jm, jp, bm, bp, eta, mu = item
+        rule = quad_cut_face(cm, fid, s)
+        Vm, Gm = basis.eval_with_grad(*mesh.bounds(jm), rule.nodes)
+        Vp, Gp = basis.eval_with_grad(*mesh.bounds(jp), rule.nodes)
+        blocks = _pair_terms(rule.weights, eta, mu,
+                             [(Vm, mu * Gm[:, :, a], 1.0), (Vp, mu * Gp[:, :, a], -1.0)])
+        idb = (bm, bp)
+        return [(idb[x], idb[y], blk) for (x, y), blk in blocks.items()], []
+    if kind == "bface":
+        _, fid, s, a, side, j, b, eta, mu = item
+        bkind, g = problem.condition(a, side)
+        sign = -1.0 if side == 0 else 1.0
+        rule = quad_cut_face(cm, fid, s)
+        V, G = basis.eval_with_grad(*mesh.bounds(j), rule.nodes)
+        gv = _bvals(g, rule.nodes, s)
+        if bkind == NEUMANN:
+            return [], [(b, V.T @ (rule.weights * mu * gv))]
+        blk = _pair_terms(rule.weights, eta, mu, [(V, mu * sign * G[:, :, a], 1.0)])
+        Gn = sign * G[:, :, a]
+        return [(b, b, blk[(0, 0)])], [(b, (eta * V - Gn).T @ (rule.weights * mu * gv))]
+    _, j, bn, bp, eta = item
+    rule = cm.interface_rules[j]
+    Vn, Gn_ = basis.eval_with_grad(*mesh.bounds(j), rule.nodes)
+    gn = (Gn_ * rule.normals[:, None, :]).sum(axis=2)
+    sides = [(Vn, problem.mu(NEG) * gn, 1.0), (Vn, problem.mu(POS) * gn, -1.0)]
+    blocks = _pair_terms(rule.weights, eta, problem.mu_max, sides)
+    idb = (bn, bp)
+    return [(idb[x], idb[y], blk) for (x, y), blk in blocks.items()], []
+
+
+def _eval_items(cm, basis, problem, items, workers=None):
+    from ._pool import fork_map
+
+    return fork_map(_eval_item, items, dict(cm=cm, basis=basis, problem=problem), workers)
 
 
 # ---------------------------------------------------------------------------
@@ -331,7 +391,7 @@ def _ref_cell(cm):
 
 
 def sip_terms(cm: CutCellMesh, basis: PlainBasis, problem: PoissonProblem,
-              groups, c_eta: float = 4.0) -> SipTerms:
+              groups, c_eta: float = 4.0, workers: int | None = None) -> SipTerms:
     """Term lists of assemble_sip + assemble_rhs (assembly.py:255-422) with
     the penalty of the small-cell aggregates `groups` (the reference's
     agg_map argument)."""
@@ -351,7 +411,7 @@ def sip_terms(cm: CutCellMesh, basis: PlainBasis, problem: PoissonProblem,
     # ---- volume terms ----------------------------------------------------
     rule0 = tensor_rule(rlo, rhi, order)
     V0, G0 = basis.eval_with_grad(rlo, rhi, rule0.nodes)
-    tid_K = tb.table(np.einsum("p,pid,pld->il", rule0.weights, G0, G0))
+    tid_K = tb.table(_stiffness(rule0.weights, G0))
     pj, ps = pidx.pieces[:, 0], pidx.pieces[:, 1]
     cut_piece = np.array([(int(a), int(b)) in cm.cut_volume_rules for a, b in pidx.pieces],
                          dtype=bool) if B else np.zeros(0, bool)
@@ -368,13 +428,9 @@ def sip_terms(cm: CutCellMesh, basis: PlainBasis, problem: PoissonProblem,
             fv = np.asarray(problem.source(nodes.reshape(-1, D)), float).reshape(len(nodes), -1)
             vec = (fv * rule0.weights[None]) @ V0
             rhs.reshape(B, N)[reg[sl]] += vec
+    items = []   # cut items, evaluated in parallel below (reference order kept)
     for b in np.flatnonzero(cut_piece):
-        j, s = int(pj[b]), int(ps[b])
-        rule = quad_volume(cm, j, s)
-        lo, hi = mesh.bounds(j)
-        V, G = basis.eval_with_grad(lo, hi, rule.nodes)
-        tb.add_dense(b, b, problem.mu(s) * np.einsum("p,pid,pld->il", rule.weights, G, G))
-        rhs[b * N:(b + 1) * N] += V.T @ (rule.weights * problem.source(rule.nodes))
+        items.append(("vol", int(b), int(pj[b]), int(ps[b])))
 
     # ---- face tables -------------------------------------------------------
     # reference face of cell 0 along each axis: its hi face (cell 0 = minus
@@ -426,20 +482,12 @@ def sip_terms(cm: CutCellMesh, basis: PlainBasis, problem: PoissonProblem,
                 tb.add_table(rows, cols, tc, mu)
                 tb.add_table(rows, cols, tp, eta * mu)
         for fid in np.flatnonzero(ok & stored[:, s]):
-            a = int(f.axis[fid])
-            rule = quad_cut_face(cm, fid, s)
-            if len(rule.weights) == 0:
+            if len(cm.cut_face_rules[(int(fid), s)].weights) == 0:
                 continue
             jm_, jp_ = int(jm[fid]), int(jp[fid])
-            bm, bp = pidx.block[jm_, s], pidx.block[jp_, s]
+            bm, bp = int(pidx.block[jm_, s]), int(pidx.block[jp_, s])
             eta = ck2 * max(inv_h[bm], inv_h[bp])
-            Vm, Gm = basis.eval_with_grad(*mesh.bounds(jm_), rule.nodes)
-            Vp, Gp = basis.eval_with_grad(*mesh.bounds(jp_), rule.nodes)
-            blocks = _pair_terms(rule.weights, eta, mu,
-                                 [(Vm, mu * Gm[:, :, a], 1.0), (Vp, mu * Gp[:, :, a], -1.0)])
-            idb = (bm, bp)
-            for (x, y), blk in blocks.items():
-                tb.add_dense(idb[x], idb[y], blk)
+            items.append(("face", int(fid), s, int(f.axis[fid]), jm_, jp_, bm, bp, eta, mu))
         # boundary faces
         for a in range(D):
             for side in (0, 1):
@@ -472,39 +520,24 @@ def sip_terms(cm: CutCellMesh, basis: PlainBasis, problem: PoissonProblem,
                                         eta[:, None, None] * Vt[None] - Gnt[None])
                     np.add.at(rhs.reshape(B, N), bb, vec)
                 for fid in np.flatnonzero(on & stored[:, s]):
-                    rule = quad_cut_face(cm, fid, s)
-                    if len(rule.weights) == 0:
+                    if len(cm.cut_face_rules[(int(fid), s)].weights) == 0:
                         continue
                     j = int(cell[fid])
-                    b = pidx.block[j, s]
-                    V, G = basis.eval_with_grad(*mesh.bounds(j), rule.nodes)
-                    gv = _bvals(g, rule.nodes, s)
-                    if kind == NEUMANN:
-                        rhs[b * N:(b + 1) * N] += V.T @ (rule.weights * mu * gv)
-                        continue
-                    eta_b = ck2 * inv_h[b]
-                    blk = _pair_terms(rule.weights, eta_b, mu, [(V, mu * sign * G[:, :, a], 1.0)])
-                    tb.add_dense(b, b, blk[(0, 0)])
-                    Gn = sign * G[:, :, a]
-                    rhs[b * N:(b + 1) * N] += (eta_b * V - Gn).T @ (rule.weights * mu * gv)
+                    b = int(pidx.block[j, s])
+                    items.append(("bface", int(fid), s, a, side, j, b, ck2 * inv_h[b], mu))
 
     # ---- interface -------------------------------------------------------------
     for j in sorted(cm.interface_rules):
-        rule = cm.interface_rules[j]
-        if len(rule.weights) == 0:
+        if len(cm.interface_rules[j].weights) == 0:
             continue
-        bn, bp = pidx.block[j, NEG], pidx.block[j, POS]
+        bn, bp = int(pidx.block[j, NEG]), int(pidx.block[j, POS])
         if bn < 0 or bp < 0:
             raise MissingSpeciesError(f"cell {j}: interface without both species")
-        eta = ck2 * max(inv_h[bn], inv_h[bp])
-        lo, hi = mesh.bounds(j)
-        Vn, Gn_ = basis.eval_with_grad(lo, hi, rule.nodes)
-        Vp, Gp_ = Vn, Gn_  # plain basis: both species share the cell's basis
-        nrm = rule.normals
-        sides = [(Vn, problem.mu(NEG) * np.einsum("pid,pd->pi", Gn_, nrm), 1.0),
-                 (Vp, problem.mu(POS) * np.einsum("pid,pd->pi", Gp_, nrm), -1.0)]
-        blocks = _pair_terms(rule.weights, eta, problem.mu_max, sides)
-        idb = (bn, bp)
-        for (x, y), blk in blocks.items():
-            tb.add_dense(idb[x], idb[y], blk)
+        items.append(("iface", int(j), bn, bp, ck2 * max(inv_h[bn], inv_h[bp])))
+
+    for dense, vecs in _eval_items(cm, basis, problem, items, workers):
+        for r, c, blk in dense:
+            tb.add_dense(r, c, blk)
+        for b, vec in vecs:
+            rhs[b * N:(b + 1) * N] += vec
     return tb.finish(B, rhs)

@@ -212,7 +212,19 @@ def build_hierarchy(cm, basis, pidx, raw_dev, rhs, level_groups, phase_times=Non
 
 
 def assemble_case(case: BenchCase, keep_terms: bool = False) -> Assembled:
-    """bench.py:165-206 on the B200 pipeline (see module docstring)."""
+    """bench.py:165-206 on the B200 pipeline (see module docstring).  Host
+    BLAS runs single-threaded: the host work is many tiny dense products
+    (multi-threaded BLAS costs ~100x on 20x20 solves); worker processes
+    provide the parallelism."""
+    try:
+        from threadpoolctl import threadpool_limits
+    except ImportError:  # pragma: no cover
+        return _assemble_case(case, keep_terms)
+    with threadpool_limits(1):
+        return _assemble_case(case, keep_terms)
+
+
+def _assemble_case(case: BenchCase, keep_terms: bool) -> Assembled:
     from .device import Context
 
     times: dict = {}

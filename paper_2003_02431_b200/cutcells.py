@@ -289,7 +289,9 @@ def _run(fn, jobs, workers):
     if workers > 1 and len(jobs) > 1:
         from concurrent.futures import ProcessPoolExecutor
 
-        with ProcessPoolExecutor(max_workers=workers) as pool:
+        from ._pool import _init_worker
+
+        with ProcessPoolExecutor(max_workers=workers, initializer=_init_worker) as pool:
             for res in pool.map(fn, jobs):
                 yield from res
     else:

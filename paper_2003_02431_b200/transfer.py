@@ -11,6 +11,7 @@ of the solvers (solvers.py:730,734) are device BSR SpMVs.
 from __future__ import annotations
 
 import numpy as np
+import scipy.linalg  # noqa: F401  (imported before worker processes fork)
 import torch
 
 from . import _native as nat
@@ -114,12 +115,13 @@ def _monomial_values(points, lo, hi, dim, degree):
     halfwidth = 0.5 * (hi - lo)
     t = (points - center) / halfwidth
     exps = multi_indices(degree, dim)
+    pw = [[None] + [t[:, d] ** e for e in range(1, degree + 1)] for d in range(dim)]
     out = np.empty((len(points), len(exps)))
     for m, a in enumerate(exps):
         col = np.ones(len(points))
         for d, e in enumerate(a):
             if e:
-                col *= t[:, d] ** e
+                col *= pw[d][e]
         out[:, m] = col
     return out
 
@@ -143,14 +145,18 @@ def _chol_or_degenerate(G, context):
 
 
 class LevelBuilder:
-    """Carriers and transfer blocks of one cut-cell mesh (transfer.py:152-341)."""
+    """Carriers and transfer blocks of one cut-cell mesh (transfer.py:152-341).
+    Per-aggregate work runs in forked worker processes (_pool.fork_map); the
+    mass matrices of cut pieces are computed once and shared by all levels."""
 
-    def __init__(self, cm, basis):
+    def __init__(self, cm, basis, workers=None):
         self.cm, self.basis = cm, basis
         self.mesh = cm.mesh
         self.N = basis.size
+        self.workers = workers
         self._carrier_cache: dict = {}
         self._block_cache: dict = {}
+        self.mass: dict = {}
         self.cache_hits = 0
 
     def uncut(self, p) -> bool:
@@ -197,26 +203,64 @@ class LevelBuilder:
             out[i * n:(i + 1) * n] = self._cell_monomial_coefficients(j, lo, hi) @ T
         return out
 
-    def carrier(self, pieces):
-        if all(self.uncut(p) for p in pieces):
-            key = self._shape_key(pieces)
-            c = self._carrier_cache.get(key)
-            if c is None:
-                c = self._carrier_cache[key] = self._carrier_exact(pieces)
-            else:
-                self.cache_hits += 1
-            return c
-        return self._carrier_exact(pieces)
-
-    def piece_mass(self, p):
-        """_piece_plain_mass (transfer.py:267-278); None = identity."""
-        if self.uncut(p):
-            return None
+    def _mass_exact(self, p):
+        """_piece_plain_mass (transfer.py:267-278) of a cut piece."""
         j, s = p
         rule = self.cm.cut_volume_rules[(j, s)]
         lo, hi = self.mesh.bounds(j)
         vals = self.basis.eval(lo, hi, rule.nodes)
         return vals.T @ (vals * rule.weights[:, None])
+
+    def piece_mass(self, p):
+        """None = identity (uncut piece)."""
+        if self.uncut(p):
+            return None
+        m = self.mass.get(p)
+        if m is None:
+            m = self.mass[p] = self._mass_exact(p)
+        return m
+
+    def precompute_masses(self):
+        from ._pool import fork_map
+
+        todo = sorted(k for k in self.cm.cut_volume_rules if k not in self.mass)
+        for p, m in zip(todo, fork_map(_mass_job, todo, {"lb": self}, self.workers)):
+            self.mass[p] = m
+
+
+def _mass_job(p):
+    from ._pool import STATE
+
+    return STATE["lb"]._mass_exact(p)
+
+
+def _carrier_job(pieces):
+    from ._pool import STATE
+
+    return STATE["lb"]._carrier_exact(pieces)
+
+
+def _restriction_job(job):
+    """Carrier of one coarse aggregate and its blocks against every fine
+    member (transfer.py:318-334)."""
+    from ._pool import STATE
+
+    lb, fine = STATE["lb"], STATE["fine"]
+    pieces, members = job
+    n = lb.N
+    carrier = lb._carrier_exact(pieces)
+    pos = {p: i for i, p in enumerate(pieces)}
+    blocks = []
+    for g in members:
+        block = np.zeros((n, n))
+        fc = fine.carriers[g]
+        for i, p in enumerate(fine.aggregates[g]):
+            left = _rows(fc, i, n)
+            right = carrier[pos[p] * n:(pos[p] + 1) * n]
+            mass = lb.piece_mass(p)
+            block += left.T @ right if mass is None else left.T @ mass @ right
+        blocks.append(block)
+    return carrier, blocks
 
 
 class LevelData:
@@ -234,15 +278,36 @@ class LevelData:
 
 def aggregation_level_data(lb: LevelBuilder, groups) -> LevelData:
     """transfer.py:208-236: uncut singletons keep the background basis."""
-    aggs, carriers = [], []
+    from ._pool import fork_map
+
+    aggs, carriers, todo, where = [], [], [], {}
     for g in groups:
         pieces = tuple((int(j), int(s)) for j, s in sorted(g))
         aggs.append(pieces)
         if len(pieces) == 1 and lb.uncut(pieces[0]):
             carriers.append(None)
+            continue
+        key = lb._shape_key(pieces) if all(lb.uncut(p) for p in pieces) else None
+        if key is not None and (key in lb._carrier_cache or key in where):
+            lb.cache_hits += 1
+            carriers.append(("key", key))
+            continue
+        if key is not None:
+            where[key] = len(todo)
+        carriers.append(("job", len(todo)))
+        todo.append(pieces)
+    res = fork_map(_carrier_job, todo, {"lb": lb}, lb.workers)
+    for key, i in where.items():
+        lb._carrier_cache[key] = res[i]
+    out = []
+    for c in carriers:
+        if c is None:
+            out.append(None)
+        elif c[0] == "job":
+            out.append(res[c[1]])
         else:
-            carriers.append(lb.carrier(pieces))
-    return LevelData(aggs, carriers)
+            out.append(lb._carrier_cache[c[1]])
+    return LevelData(aggs, out)
 
 
 def _rows(carrier, i, n):
@@ -266,7 +331,10 @@ def initial_restriction(level: LevelData, block_of, n):
 
 def build_restriction(lb: LevelBuilder, fine: LevelData, coarse_groups):
     """transfer.py:281-341: returns ((row_ptr, col, val) over fine
-    aggregates, coarse LevelData)."""
+    aggregates, coarse LevelData).  Coarse aggregates made of uncut pieces
+    are computed once per (shape, member partition) class."""
+    from ._pool import fork_map
+
     from .errors import InvalidMapError
 
     n = lb.N
@@ -275,48 +343,48 @@ def build_restriction(lb: LevelBuilder, fine: LevelData, coarse_groups):
         for p in pieces:
             p2f[p] = g
     nf = fine.num_blocks
-    col = np.empty(nf, np.int64)
-    val = np.empty((nf, n, n))
-    aggs, carriers = [], []
+    plan, todo, pending = [], [], {}
+    lb.precompute_masses()
     for G, group in enumerate(coarse_groups):
         pieces = tuple((int(j), int(s)) for j, s in sorted(group))
         members = sorted({p2f[p] for p in pieces})
         if sum(len(fine.aggregates[g]) for g in members) != len(pieces):
             raise InvalidMapError(
                 f"coarse aggregation map splits a fine aggregate (coarse group {pieces})")
-        aggs.append(pieces)
         if len(members) == 1:
+            plan.append((pieces, members, "inherit", None))
+            continue
+        key = None
+        if all(lb.uncut(p) for p in pieces):
+            pos = {p: i for i, p in enumerate(pieces)}
+            key = (lb._shape_key(pieces),
+                   tuple(tuple(pos[p] for p in fine.aggregates[g]) for g in members))
+            if key in lb._block_cache or key in pending:
+                lb.cache_hits += 1
+                plan.append((pieces, members, "cache", key))
+                continue
+            pending[key] = len(todo)
+        plan.append((pieces, members, "job", len(todo)))
+        todo.append((pieces, members))
+    res = fork_map(_restriction_job, todo, {"lb": lb, "fine": fine}, lb.workers)
+    for key, i in pending.items():
+        lb._block_cache[key] = res[i]
+        lb._carrier_cache.setdefault(key[0], res[i][0])
+    col = np.empty(nf, np.int64)
+    val = np.empty((nf, n, n))
+    aggs, carriers = [], []
+    for G, (pieces, members, how, ref) in enumerate(plan):
+        aggs.append(pieces)
+        if how == "inherit":
             carriers.append(fine.carriers[members[0]])
             col[members[0]] = G
             val[members[0]] = np.eye(n)
             continue
-        carrier = lb.carrier(pieces)
+        carrier, blocks = res[ref] if how == "job" else lb._block_cache[ref]
         carriers.append(carrier)
-        pos = {p: i for i, p in enumerate(pieces)}
-        key = None
-        if all(lb.uncut(p) for p in pieces):
-            key = (lb._shape_key(pieces),
-                   tuple(tuple(pos[p] for p in fine.aggregates[g]) for g in members))
-            hit = lb._block_cache.get(key)
-            if hit is not None:
-                for g, blk in zip(members, hit):
-                    col[g] = G
-                    val[g] = blk
-                continue
-        blocks = []
-        for g in members:
-            block = np.zeros((n, n))
-            fc = fine.carriers[g]
-            for i, p in enumerate(fine.aggregates[g]):
-                left = _rows(fc, i, n)
-                right = carrier[pos[p] * n:(pos[p] + 1) * n]
-                mass = lb.piece_mass(p)
-                block += left.T @ right if mass is None else left.T @ mass @ right
+        for g, blk in zip(members, blocks):
             col[g] = G
-            val[g] = block
-            blocks.append(block)
-        if key is not None:
-            lb._block_cache[key] = blocks
+            val[g] = blk
     return (np.arange(nf + 1, dtype=np.int64), col, val), LevelData(aggs, carriers)
 
 
