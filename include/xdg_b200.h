@@ -208,6 +208,51 @@ int xdg_assemble_blocks(int nout, int N, const int* tptr, const int* tid,
                         const int* didx, const double* dense, double* out,
                         xdg_stream_t stream);
 
+/* ---- multifrontal sparse LU (nested-dissection forest) ---------------- */
+/* Replaces SuperLU splu/solve (cutdg blockmatrix.py:203-227) for the
+ * low-order PMG systems (solvers.py:208-221, 249-251), the coarsest level /
+ * "direct" solver (solvers.py:661-666, 698-710).  Built by multifrontal.py.
+ * Factor storage F (device): per front row-major INV (p x p, leading dim
+ * ldp: L^-1 strictly lower, U^-1 upper), L_BP (b x p, ld ldp), U_PB
+ * (p x b, ld ldb). */
+typedef struct xdg_mf_node {
+  int32_t p, b, ldp, ldb;      /* pivot / boundary unknowns, leading dims */
+  int32_t gp, gb, pad0, pad1;  /* lanes per row for p- / b-long rows (2^k) */
+  int64_t inv, lbp, upb;       /* offsets into F */
+  int64_t w, y, c;             /* offsets into W (p+b), Y (p), C (b) */
+  int64_t bx, px;              /* offsets into bidx (b), pdst (p) */
+} xdg_mf_node;
+
+typedef struct xdg_mf {
+  int32_t nlevels, nnodes;
+  int64_t total;               /* unknowns */
+  const int64_t* lev_ent;      /* HOST [nlevels+1] gather-entry ranges      */
+  const int64_t* lev_task;     /* HOST [4][nlevels+1] warp-task ranges of the
+                                  phases lower, bound, upb, upper            */
+  const int64_t* ent_w;        /* gather entry -> W index                   */
+  const int64_t* ent_src;      /* -> index into b, or -1                    */
+  const int64_t* ent_cptr;     /* CSR of child contributions (into C)       */
+  const int64_t* ent_cidx;
+  const int32_t* tasks;        /* int4 (node, row, seg, slot) warp tasks    */
+  const xdg_mf_node* nodes;
+  const int64_t* bidx;         /* Y index of each boundary unknown          */
+  const int64_t* pdst;         /* x index of each pivot unknown             */
+  const double* ent_scale;     /* equilibration: W = ent_scale * b[src] ... */
+  const double* pscale;        /*   ... x[pdst] = pscale * (U^-1 T)         */
+  const double* F;
+  double* W;
+  double* Y;
+  double* C;
+  double* part;                /* partial sums of split long rows           */
+  int32_t* cnt;                /* their tickets (zero between launches)     */
+  double apply_bytes;          /* algorithmic bytes of one solve            */
+} xdg_mf;
+
+/* x[pdst] = A^-1 b[src] for every system of the forest at once:
+ * 3 launches per forward level, 2 per backward level. */
+int xdg_mf_solve(const xdg_mf* mf, const double* b, double* x,
+                 xdg_stream_t stream);
+
 /* ======================================================================
  * Native solver driver (the reference's control loops, solvers.py:559-846,
  * run in C++ over device data: one host sync per rm_step / GMRES inner
@@ -248,6 +293,7 @@ typedef struct xdg_pmg {       /* PmgPlan of paper_2003_02431_b200/pmg.py */
   const int64_t* cpos;
   const double* damping;
   double apply_bytes;          /* algorithmic bytes of one apply (accounting) */
+  const xdg_mf* mf;            /* sparse low-order factors (NULL: dense LU) */
 } xdg_pmg;
 
 typedef struct xdg_direct {    /* dense LU of one system (coarsest level) */
@@ -258,6 +304,7 @@ typedef struct xdg_direct {    /* dense LU of one system (coarsest level) */
   const int* dims;             /* device {n} */
   const int* row_sys;          /* device zeros[n] */
   double* scratch;             /* 2 n doubles */
+  const xdg_mf* mf;            /* sparse factors (NULL: dense LU)           */
 } xdg_direct;
 
 typedef struct xdg_rm {        /* RmState (solvers.py:485-556) */

@@ -69,6 +69,7 @@ SIGNATURES = {
     "xdg_gmres_solve": (_i32, [_vp, _vp, _i32, _f64, _i32, _vp, _vp, _i32]
                         + [_vp] * 14),
     "xdg_mgs": (_i32, [_i64, _i32, _vp, _i64, _vp, _vp, _vp, _vp]),
+    "xdg_mf_solve": (_i32, [_vp, _vp, _vp, _vp]),
 }
 
 _lib = None

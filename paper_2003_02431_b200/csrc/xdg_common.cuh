@@ -26,6 +26,12 @@ void set_error(const char* fmt, ...);
     }                                                                      \
   } while (0)
 
+#define XDG_TRY(expr)                 \
+  do {                                \
+    int _st = (expr);                 \
+    if (_st != XDG_OK) return _st;    \
+  } while (0)
+
 #define XDG_CHECK_LAUNCH() XDG_TRY_CUDA(cudaGetLastError())
 
 #define XDG_REQUIRE(cond, code, ...)                                       \

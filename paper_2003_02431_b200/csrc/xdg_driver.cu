@@ -152,12 +152,6 @@ cudaError_t sync_read(double* host, const double* dev, int count, cudaStream_t s
   return cudaStreamSynchronize(s);
 }
 
-#define XDG_TRY(expr)                 \
-  do {                                \
-    int _st = (expr);                 \
-    if (_st != XDG_OK) return _st;    \
-  } while (0)
-
 int spmv(const xdg_bsr* M, const double* x, double* y, const double* b,
          double* nrm, void* ws, cudaStream_t s) {
   count(spmv_bytes(M, b != nullptr));
@@ -177,8 +171,11 @@ static int pmg_apply_op(const xdg_pmg* P, const xdg_bsr* M, const double* b,
   xdg_stream_t st = reinterpret_cast<xdg_stream_t>(s);
   count(P->apply_bytes);
   double* xlo = (P->direct && !P->has_high) ? z : P->xlo;
-  XDG_TRY(xdg_lu_inv_apply(P->nsys, P->total, P->row_sys, P->lu_off, P->dims,
-                           P->vec_off, P->LU, P->src, b, xlo, P->scratch, st));
+  if (P->mf)
+    XDG_TRY(xdg_mf_solve(P->mf, b, xlo, st));
+  else
+    XDG_TRY(xdg_lu_inv_apply(P->nsys, P->total, P->row_sys, P->lu_off, P->dims,
+                             P->vec_off, P->LU, P->src, b, xlo, P->scratch, st));
   if (P->has_high) {
     double* out = P->direct ? z : P->out;
     XDG_TRY(xdg_pmg_high(P->nwork, P->N, P->m, P->wi_ptr, P->wi_blk, P->wi_lcol,
@@ -329,9 +326,14 @@ int omg_level(OmgRun& R, int lam, const double* b, double* x, int has_x0,
   const int64_t n = (int64_t)lv.M.nbr * lv.M.N;
   if (lam == R.nlevels - 1 || !lv.has_restriction) {           // solvers.py:698-710
     const xdg_direct& D = lv.direct;
-    count(8.0 * D.n * (double)D.n + 32.0 * D.n);
-    XDG_TRY(xdg_lu_inv_apply(1, D.n, D.row_sys, D.zero_off, D.dims, D.zero_off,
-                             D.LU, D.perm, b, x, D.scratch, st));
+    if (D.mf) {
+      count(D.mf->apply_bytes);
+      XDG_TRY(xdg_mf_solve(D.mf, b, x, st));
+    } else {
+      count(8.0 * D.n * (double)D.n + 32.0 * D.n);
+      XDG_TRY(xdg_lu_inv_apply(1, D.n, D.row_sys, D.zero_off, D.dims, D.zero_off,
+                               D.LU, D.perm, b, x, D.scratch, st));
+    }
     if (lam == R.entry) {
       XDG_TRY(spmv(&lv.M, x, rm.r, b, rm.sc + 6, rm.ws, R.s));
       double v;

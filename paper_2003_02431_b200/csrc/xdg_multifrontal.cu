@@ -1,0 +1,254 @@
+// Multifrontal sparse LU solves (nested-dissection elimination forest) for
+// the low-order PMG systems, the Schwarz blocks' low-order systems and large
+// direct / coarsest-level solves -- the systems the reference factors with
+// SuperLU (cutdg blockmatrix.py:203-227 splu/solve; solvers.py:208-221,
+// 249-251, 661-666, 698-710).
+//
+// Setup (multifrontal.py): nested dissection of each system's block graph
+// into a forest of fronts; front t eliminates its pivot unknowns P_t
+// (partial pivoting inside P_t) against its boundary B_t (ancestor
+// separators).  Stored per front: INV_t (L^-1 strictly below the diagonal,
+// U^-1 on/above it, p x p), L_BP = F_BP U^-1 (b x p), U_PB = L^-1 P F_PB
+// (p x b), all row-major with padded leading dimensions.
+//
+// Solve, level by level (height h = 0 .. H-1 forward, H-1 .. 0 backward),
+// every front of a level in one launch, warp per row:
+//   F1 gather   W_t[i] = b[src] + sum of the children's contributions
+//               (fixed order: deterministic), P part in pivot order
+//   F2 lower    Y_t   = L^-1 W_t[P]                 (triangular GEMV)
+//   F3 bound    C_t   = W_t[B] - L_BP Y_t           (contribution to parent)
+//   B1 upb      T_t   = Y_t - U_PB x[B_t]           (x of ancestors)
+//   B2 upper    x[P_t] = U^-1 T_t
+// with the symmetric equilibration S folded in (b scaled in F1, x in B2).
+// Bound: HBM -- each apply streams every stored factor once
+// (8 (p^2 + 2 p b) bytes per front); no sequential substitution chains.
+#include "xdg_common.cuh"
+
+namespace xdg {
+namespace {
+
+constexpr int kT = 256;
+
+// Sub-warp row dots.  A warp task covers 32/G consecutive rows of one
+// front, G lanes per row (G = power of two chosen per front from the row
+// length, so short rows still keep the whole warp's loads in flight and long
+// rows get the whole warp).  Lanes of a group stride G through the row, 8
+// loads in flight per lane, fixed accumulation order; the group sum is a
+// shuffle-xor tree inside the aligned group (deterministic).
+template <typename V>
+__device__ __forceinline__ double group_dot(const double* __restrict__ row, V v,
+                                            int j0, int j1, int gl, int G,
+                                            bool active) {
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  if (active) {
+    const int step = 8 * G;
+    for (int jb = j0; jb < j1; jb += step) {
+      // clamped (always valid) unpredicated loads, so all 16 are issued
+      // before the first FMA; out-of-row lanes are zeroed afterwards
+      double r[8], q[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = min(jb + gl + G * u, j1 - 1);
+        r[u] = __ldg(row + j);
+        q[u] = v(j);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (jb + gl + G * u >= j1) r[u] = 0.0;
+      a0 = fma(r[0], q[0], a0);
+      a1 = fma(r[1], q[1], a1);
+      a2 = fma(r[2], q[2], a2);
+      a3 = fma(r[3], q[3], a3);
+      a0 = fma(r[4], q[4], a0);
+      a1 = fma(r[5], q[5], a1);
+      a2 = fma(r[6], q[6], a2);
+      a3 = fma(r[7], q[7], a3);
+    }
+  }
+  double s = (a0 + a1) + (a2 + a3);
+  for (int o = 16; o > 0; o >>= 1)
+    if (o < G) s += __shfl_xor_sync(0xffffffffu, s, o);
+  return s;
+}
+
+struct Direct {
+  const double* p;
+  __device__ __forceinline__ double operator()(int j) const { return p[j]; }
+};
+
+struct Gathered {
+  const double* x;
+  const int64_t* idx;
+  __device__ __forceinline__ double operator()(int j) const { return x[idx[j]]; }
+};
+
+// Task g of n in interleaved order (long and short rows mix on every SM).
+__device__ __forceinline__ int64_t interleave(int64_t w, int64_t n) {
+  return (w & 1) ? n - 1 - (w >> 1) : (w >> 1);
+}
+
+__global__ void __launch_bounds__(kT)
+mf_gather_kernel(int64_t e0, int64_t e1, const int64_t* __restrict__ ent_w,
+                 const int64_t* __restrict__ ent_src,
+                 const int64_t* __restrict__ ent_cptr,
+                 const int64_t* __restrict__ ent_cidx,
+                 const double* __restrict__ ent_scale,
+                 const double* __restrict__ b, const double* __restrict__ C,
+                 double* __restrict__ W) {
+  for (int64_t e = e0 + (int64_t)blockIdx.x * kT + threadIdx.x; e < e1;
+       e += (int64_t)gridDim.x * kT) {
+    const int64_t s = ent_src[e];
+    double v = s >= 0 ? __dmul_rn(ent_scale[e], b[s]) : 0.0;
+    for (int64_t k = ent_cptr[e]; k < ent_cptr[e + 1]; ++k)
+      v = __dadd_rn(v, C[ent_cidx[k]]);
+    W[ent_w[e]] = v;
+  }
+}
+
+enum Phase { kLower = 0, kBound = 1, kUpb = 2, kUpper = 3 };
+constexpr int kSeg = 1024;  // row segment of a split long row (8 KB)
+
+// The four row phases (p = pivot unknowns, b = boundary unknowns of a front):
+//   kLower  Y[i]  = W[i] + L^-1[i, :i] . W[:i]              rows: P, G = gp
+//   kBound  C[j]  = W[p+j] - L_BP[j, :] . Y                  rows: B, G = gp
+//   kUpb    W[i]  = Y[i] - U_PB[i, :] . Y[bidx]              rows: P, G = gb
+//   kUpper  Y[i] = U^-1[i, i:] . W[i:], x[pdst[i]] = s_i Y[i] rows: P, G = gp
+// (in the backward sweep Y holds the equilibrated solution of the fronts
+// already solved: the ancestors' values the U_PB rows read through bidx)
+struct Ctx {
+  const xdg_mf_node* nodes;
+  const double* F;
+  const int64_t* bidx;
+  const int64_t* pdst;
+  const double* pscale;
+  double* W;
+  double* Y;
+  double* C;
+  double* x;
+  double* part;
+  int* cnt;
+};
+
+template <int PH>
+__device__ __forceinline__ void row_span(const xdg_mf_node& nd, int r, int& j0, int& j1) {
+  j0 = (PH == kUpper) ? r : 0;
+  j1 = (PH == kLower) ? r : (PH == kUpb ? nd.b : nd.p);
+}
+
+template <int PH>
+__device__ __forceinline__ double row_part(const Ctx& c, const xdg_mf_node& nd, int r,
+                                           int js, int je, int gl, int G, bool act) {
+  if (PH == kLower)
+    return group_dot(c.F + nd.inv + (int64_t)r * nd.ldp, Direct{c.W + nd.w}, js, je, gl, G,
+                     act);
+  if (PH == kBound)
+    return group_dot(c.F + nd.lbp + (int64_t)r * nd.ldp, Direct{c.Y + nd.y}, js, je, gl, G,
+                     act);
+  if (PH == kUpb)
+    return group_dot(c.F + nd.upb + (int64_t)r * nd.ldb, Gathered{c.Y, c.bidx + nd.bx}, js,
+                     je, gl, G, act);
+  return group_dot(c.F + nd.inv + (int64_t)r * nd.ldp, Direct{c.W + nd.w}, js, je, gl, G,
+                   act);
+}
+
+template <int PH>
+__device__ __forceinline__ void row_done(const Ctx& c, const xdg_mf_node& nd, int r,
+                                         double d) {
+  if (PH == kLower) c.Y[nd.y + r] = __dadd_rn(c.W[nd.w + r], d);
+  if (PH == kBound) c.C[nd.c + r] = __dsub_rn(c.W[nd.w + nd.p + r], d);
+  if (PH == kUpb) c.W[nd.w + r] = __dsub_rn(c.Y[nd.y + r], d);
+  if (PH == kUpper) {
+    c.Y[nd.y + r] = d;
+    c.x[c.pdst[nd.px + r]] = __dmul_rn(c.pscale[nd.px + r], d);
+  }
+}
+
+// Warp tasks (node, row, seg, slot).  slot < 0: 32/G rows from `row`, G
+// lanes each.  slot >= 0: segment `seg` of a long row (whole warp, kSeg
+// columns); the partial goes to part[slot + seg] and the last segment to
+// finish (ticket in cnt[slot]) sums the partials in segment order --
+// deterministic -- and finishes the row.  Equal-sized segments keep every
+// launch free of long-row tails.
+template <int PH>
+__global__ void __launch_bounds__(kT, 4)
+mf_rows_kernel(int64_t t0, int64_t ntasks, const int4* __restrict__ tasks, Ctx c) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (kT / 32);
+  for (int64_t w = (int64_t)blockIdx.x * (kT / 32) + (threadIdx.x >> 5); w < ntasks;
+       w += nw) {
+    const int4 tk = tasks[t0 + interleave(w, ntasks)];
+    const xdg_mf_node nd = c.nodes[tk.x];
+    if (tk.w < 0) {
+      const int G = (PH == kUpb) ? nd.gb : nd.gp;
+      const int gl = lane & (G - 1);
+      const int r = tk.y + lane / G;
+      const int nrows = (PH == kBound) ? nd.b : nd.p;
+      const bool act = r < nrows;
+      int j0 = 0, j1 = 0;
+      if (act) row_span<PH>(nd, r, j0, j1);
+      const double d = row_part<PH>(c, nd, r, j0, j1, gl, G, act && j1 > j0);
+      if (act && gl == 0) row_done<PH>(c, nd, r, d);
+    } else {
+      const int r = tk.y;
+      int j0, j1;
+      row_span<PH>(nd, r, j0, j1);
+      const int js = j0 + tk.z * kSeg;
+      const int je = min(js + kSeg, j1);
+      const double d = row_part<PH>(c, nd, r, js, je, lane, 32, true);
+      if (lane == 0) {
+        c.part[tk.w + tk.z] = d;
+        __threadfence();
+        const int nseg = (j1 - j0 + kSeg - 1) / kSeg;
+        if (atomicAdd(c.cnt + tk.w, 1) == nseg - 1) {
+          __threadfence();
+          const volatile double* pv = c.part + tk.w;
+          double sum = 0.0;
+          for (int q = 0; q < nseg; ++q) sum = __dadd_rn(sum, pv[q]);
+          c.cnt[tk.w] = 0;
+          row_done<PH>(c, nd, r, sum);
+        }
+      }
+    }
+  }
+}
+
+template <int PH>
+int launch_rows(const xdg_mf* mf, int h, double* x, cudaStream_t s) {
+  const int64_t* lev = mf->lev_task + (int64_t)PH * (mf->nlevels + 1);
+  const int64_t t0 = lev[h], nt = lev[h + 1] - t0;
+  if (nt <= 0) return XDG_OK;
+  Ctx c{mf->nodes, mf->F, mf->bidx, mf->pdst, mf->pscale, mf->W, mf->Y, mf->C, x,
+        mf->part, mf->cnt};
+  const int g = resident_grid(mf_rows_kernel<PH>, kT, 0, nt * 32);
+  mf_rows_kernel<PH><<<g, kT, 0, s>>>(t0, nt, reinterpret_cast<const int4*>(mf->tasks), c);
+  XDG_CHECK_LAUNCH();
+  return XDG_OK;
+}
+
+}  // namespace
+}  // namespace xdg
+
+extern "C" int xdg_mf_solve(const xdg_mf* mf, const double* b, double* x,
+                            xdg_stream_t stream) {
+  using namespace xdg;
+  XDG_REQUIRE(mf != nullptr && mf->nlevels >= 0, XDG_ERR_ARG, "bad multifrontal plan");
+  if (mf->total == 0 || mf->nlevels == 0) return XDG_OK;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int H = mf->nlevels;
+  for (int h = 0; h < H; ++h) {
+    const int64_t e0 = mf->lev_ent[h], e1 = mf->lev_ent[h + 1];
+    if (e1 > e0) {
+      mf_gather_kernel<<<grid_for(e1 - e0, kT, 8), kT, 0, s>>>(
+          e0, e1, mf->ent_w, mf->ent_src, mf->ent_cptr, mf->ent_cidx, mf->ent_scale, b,
+          mf->C, mf->W);
+      XDG_CHECK_LAUNCH();
+    }
+    XDG_TRY(launch_rows<kLower>(mf, h, x, s));
+    XDG_TRY(launch_rows<kBound>(mf, h, x, s));
+  }
+  for (int h = H - 1; h >= 0; --h) {
+    XDG_TRY(launch_rows<kUpb>(mf, h, x, s));
+    XDG_TRY(launch_rows<kUpper>(mf, h, x, s));
+  }
+  return XDG_OK;
+}

@@ -166,6 +166,42 @@ class DeviceDirect:
         return out
 
 
+# Above this many unknowns (uniform block layouts) the stored factorization
+# is the multifrontal one (multifrontal.py): a dense solve streams 8 n^2
+# bytes (134 MB at n = 4096).
+SPARSE_DIRECT_MIN = 4096
+
+
+def _sparse_direct(M, n: int) -> bool:
+    import os
+
+    mode = os.environ.get("XDG_DIRECT", "auto")
+    if M._padded_size() is not None or M.row_layout.num_blocks == 0:
+        return False
+    if mode in ("dense", "sparse"):
+        return mode == "sparse"
+    return n > SPARSE_DIRECT_MIN
+
+
+class SparseDirect:
+    """Device multifrontal factor of one square uniform-block DeviceBSR:
+    apply(b_dev) -> x_dev (same interface as DeviceDirect)."""
+
+    def __init__(self, D, ctx, what="matrix"):
+        from .multifrontal import Multifrontal
+
+        self.ctx = ctx
+        self.n = D.nbr * D.N
+        v = np.arange(D.nbr, dtype=np.int64) * D.N
+        self.mf = Multifrontal(ctx, D.row_ptr.cpu().numpy(), D.col.cpu().numpy(), D.val_t,
+                               D.N, [np.arange(D.nbr, dtype=np.int64)], D.N, v, v, what=what)
+
+    def apply(self, b: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        if out is None:
+            out = torch.empty(self.n, dtype=F64, device=b.device)
+        return self.mf.solve(b, out)
+
+
 class DirectFactorization:
     """Stored LU factorization reusable across right-hand sides
     (blockmatrix.py:203-227): `apply(b)` takes and returns numpy arrays;
@@ -180,6 +216,13 @@ class DirectFactorization:
         if self.shape[0] != self.shape[1]:
             raise DimensionMismatchError("direct solver needs a square matrix")
         n = self.shape[0]
+        if _sparse_direct(M, n):
+            from .device import Context
+
+            ctx0 = Context.get()
+            self._dev = SparseDirect(M.device(ctx0), ctx0)
+            self.factor_count = 1
+            return
         if n > MAX_DENSE_DIRECT:
             raise NotImplementedError(
                 f"dense device LU limited to {MAX_DENSE_DIRECT} unknowns (got {n})")

@@ -31,12 +31,13 @@ class XdgPmg(C.Structure):
                             "src", "xlo",
                             "wi_ptr", "wi_blk", "wi_lcol", "wi_cell", "wi_lrow",
                             "wi_xlo", "wi_hidx", "wi_out", "HLU", "hperm", "out",
-                            "cptr", "cpos", "damping")] + [("apply_bytes", C.c_double)]
+                            "cptr", "cpos", "damping")] + [("apply_bytes", C.c_double), ("mf", _vp)]
 
 
 class XdgDirect(C.Structure):
     _fields_ = [("n", C.c_int32), ("pad0", C.c_int32), ("LU", _vp), ("perm", _vp),
-                ("zero_off", _vp), ("dims", _vp), ("row_sys", _vp), ("scratch", _vp)]
+                ("zero_off", _vp), ("dims", _vp), ("row_sys", _vp), ("scratch", _vp),
+                ("mf", _vp)]
 
 
 class XdgRm(C.Structure):
@@ -82,13 +83,22 @@ def pmg_struct(plan):
         s.out, s.cptr, s.cpos = _p(plan.out), _p(plan.cptr), _p(plan.cpos)
         s.damping = _p(plan.damping)
     s.apply_bytes = float(plan.algorithmic_bytes())
-    return s, []
+    keep = []
+    if plan.mf is not None:
+        ms = plan.mf.struct()
+        s.mf = C.addressof(ms)
+        keep.append(ms)
+    return s, keep
 
 
 def direct_struct(dd):
     """XdgDirect for a direct.DeviceDirect."""
     s = XdgDirect()
     s.n = dd.n
+    if getattr(dd, "mf", None) is not None:
+        ms = dd.mf.struct()
+        s.mf = C.addressof(ms)
+        return s, [ms]
     if dd.n:
         s.LU, s.perm = _p(dd.INV), _p(dd.perm)
         s.zero_off, s.dims = _p(dd.lu_off), _p(dd.dims)

@@ -1,0 +1,638 @@
+"""Multifrontal sparse LU on the device: the stored factorization behind the
+large low-order PMG systems, the Schwarz blocks' low-order systems and large
+direct / coarsest-level solves.
+
+The reference factors these systems with SuperLU (`splu`, COLAMD + partial
+pivoting: cutdg blockmatrix.py:203-227, used by solvers.py:208-221 low-order
+PMG factor, 249-251 its solve, 661-666 / 698-710 coarsest level).  Dense
+device LU (direct.py) streams 8 n^2 bytes per solve and cannot hold the
+global low-order system of a 32^3 p=3 case at all (336,610 unknowns ->
+906 GB).  Here:
+
+* symbolic (host, setup): the block graph of every system is ordered by
+  nested dissection (BFS level-set separators from a pseudo-peripheral
+  vertex, recursively), giving an elimination forest of fronts.  Front t
+  eliminates its pivot blocks P_t against its boundary B_t (the ancestor
+  separator blocks adjacent to t's subtree);
+* numeric (device, setup; batched cuSOLVER/MAGMA getrf, cuBLAS trsm/GEMM as
+  plumbing): fronts of one height are assembled (original blocks + the
+  children's Schur complements, child by child -- deterministic), padded
+  into size buckets, LU-factored with partial pivoting inside P_t, and
+  L_BP = F_BP U^-1, U_PB = L^-1 P F_PB, S = F_BB - L_BP U_PB formed.  The
+  triangular factors of every front are stored as explicit inverses (as in
+  direct.py), so a solve is only GEMVs;
+* solve (xdg_mf_solve, csrc/xdg_multifrontal.cu): 5 row-parallel launches per
+  tree height, every system of the forest at once, no atomics.
+
+Pivoting is partial within each front's pivot block (the standard
+multifrontal restriction).  The systems are SIP-DG operators (symmetric in
+pattern, values symmetric to ~1e-11 relative, positive definite: SURVEY
+8(c)), for which this is stable; any exactly zero / non-finite pivot raises
+SingularSystemError like SuperLU's "exactly singular" (blockmatrix.py:211-215).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import sys
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .direct import lu_factor_batched, triangular_inverses
+from .errors import SingularSystemError
+
+F64 = torch.float64
+I32 = torch.int32
+I64 = torch.int64
+
+NODE_DT = np.dtype([("p", "<i4"), ("b", "<i4"), ("ldp", "<i4"), ("ldb", "<i4"),
+                    ("gp", "<i4"), ("gb", "<i4"), ("pad0", "<i4"), ("pad1", "<i4"),
+                    ("inv", "<i8"), ("lbp", "<i8"), ("upb", "<i8"), ("w", "<i8"),
+                    ("y", "<i8"), ("c", "<i8"), ("bx", "<i8"), ("px", "<i8")])
+assert NODE_DT.itemsize == 96
+SEG = 1024  # columns per segment of a split long row (kSeg, xdg_multifrontal.cu)
+
+_vp = C.c_void_p
+
+
+class XdgMf(C.Structure):
+    _fields_ = [("nlevels", C.c_int32), ("nnodes", C.c_int32), ("total", C.c_int64)] + \
+        [(f, _vp) for f in ("lev_ent", "lev_task", "ent_w", "ent_src", "ent_cptr",
+                            "ent_cidx", "tasks", "nodes", "bidx",
+                            "pdst", "ent_scale", "pscale", "F", "W", "Y", "C", "part", "cnt")] + [("apply_bytes", C.c_double)]
+
+
+def _ranges(starts: np.ndarray, ends: np.ndarray) -> np.ndarray:
+    lens = ends - starts
+    tot = int(lens.sum())
+    if tot == 0:
+        return np.zeros(0, np.int64)
+    offs = np.repeat(starts - np.concatenate([[0], np.cumsum(lens)[:-1]]), lens)
+    return np.arange(tot, dtype=np.int64) + offs
+
+
+# ---------------------------------------------------------------------------
+# Systems -> one combined vertex graph
+
+class SystemGraph:
+    """Vertices = (system, block) pairs of every system (systems are
+    independent components).  `a_*`: the restricted BSR entries (with the
+    diagonal) as (row vertex, col vertex, global block index); `g_*`: the
+    symmetrised adjacency without self loops (ordering graph)."""
+
+    def __init__(self, rp: np.ndarray, col: np.ndarray, sets):
+        rp = np.asarray(rp, np.int64)
+        col = np.asarray(col, np.int64)
+        nbr = len(rp) - 1
+        loc = np.full(nbr, -1, np.int64)
+        rows_l, cols_l, ks_l = [], [], []
+        base = 0
+        gblk, sys_of = [], []
+        for s, S in enumerate(sets):
+            S = np.asarray(S, np.int64)
+            loc[S] = np.arange(len(S)) + base
+            ks = _ranges(rp[S], rp[S + 1])
+            lc = loc[col[ks]]
+            keep = lc >= 0
+            rows = np.repeat(np.arange(len(S)) + base, rp[S + 1] - rp[S])
+            rows_l.append(rows[keep])
+            cols_l.append(lc[keep])
+            ks_l.append(ks[keep])
+            loc[S] = -1
+            gblk.append(S)
+            sys_of.append(np.full(len(S), s, np.int64))
+            base += len(S)
+        cat = (lambda xs: np.concatenate(xs) if xs else np.zeros(0, np.int64))
+        self.nv = base
+        self.gblk, self.sys = cat(gblk), cat(sys_of)
+        self.a_row, self.a_col, self.a_k = cat(rows_l), cat(cols_l), cat(ks_l)
+        off = self.a_row != self.a_col
+        r = np.concatenate([self.a_row[off], self.a_col[off]])
+        c = np.concatenate([self.a_col[off], self.a_row[off]])
+        key = np.unique(r * max(self.nv, 1) + c)
+        r, c = key // max(self.nv, 1), key % max(self.nv, 1)
+        self.g_ptr = np.zeros(self.nv + 1, np.int64)
+        np.cumsum(np.bincount(r, minlength=self.nv), out=self.g_ptr[1:])
+        self.g_col = c
+
+
+# ---------------------------------------------------------------------------
+# Nested dissection
+
+class _ND:
+    def __init__(self, g_ptr, g_col, nv, leaf):
+        self.ptr, self.col, self.leaf = g_ptr, g_col, max(1, int(leaf))
+        self.active = np.zeros(nv, bool)
+        self.dist = np.full(nv, -1, np.int64)
+        self.P = []
+        self.kids = []
+
+    def _bfs(self, start):
+        dist, ptr, col, act = self.dist, self.ptr, self.col, self.active
+        front = np.array([start], np.int64)
+        dist[start] = 0
+        levels = [front]
+        d = 0
+        while True:
+            nb = col[_ranges(ptr[front], ptr[front + 1])]
+            nb = nb[act[nb]]
+            nb = np.unique(nb[dist[nb] < 0])
+            if nb.size == 0:
+                break
+            d += 1
+            dist[nb] = d
+            levels.append(nb)
+            front = nb
+        for lv in levels:
+            dist[lv] = -1
+        return levels
+
+    def _node(self, P, kids):
+        self.P.append(np.sort(P))
+        self.kids.append(kids)
+        return len(self.P) - 1
+
+    def run(self, V) -> list:
+        V = np.asarray(V, np.int64)
+        if V.size == 0:
+            return []
+        self.active[V] = True
+        levels = self._bfs(int(V[0]))
+        reached = np.concatenate(levels)
+        if reached.size < V.size:
+            self.active[V] = False
+            rest = np.setdiff1d(V, reached, assume_unique=True)
+            return self.run(np.sort(reached)) + self.run(rest)
+        if V.size <= self.leaf or len(levels) < 3:
+            self.active[V] = False
+            return [self._node(V, [])]
+        levels = self._bfs(int(levels[-1][0]))
+        self.active[V] = False
+        if len(levels) < 3:
+            return [self._node(V, [])]
+        sizes = np.array([len(lv) for lv in levels])
+        cum = np.cumsum(sizes)
+        n = V.size
+        ks = np.arange(1, len(levels) - 1)
+        left, right = cum[ks - 1], n - cum[ks]
+        k = int(ks[np.argmin(np.maximum(left, right) * 2 + sizes[ks])])
+        L = np.sort(np.concatenate(levels[:k]))
+        R = np.sort(np.concatenate(levels[k + 1:]))
+        kids = self.run(L) + self.run(R)
+        return [self._node(levels[k], kids)]
+
+
+def nested_dissection(g_ptr, g_col, nv, leaf):
+    """Post-ordered elimination forest: (P list, children list)."""
+    from scipy.sparse import csr_matrix
+    from scipy.sparse.csgraph import connected_components
+
+    nd = _ND(g_ptr, g_col, nv, leaf)
+    old = sys.getrecursionlimit()
+    sys.setrecursionlimit(max(old, 100000))
+    try:
+        if nv:
+            A = csr_matrix((np.ones(len(g_col)), g_col, g_ptr), shape=(nv, nv))
+            ncomp, lab = connected_components(A, directed=False)
+            order = np.argsort(lab, kind="stable")
+            cptr = np.zeros(ncomp + 1, np.int64)
+            np.cumsum(np.bincount(lab, minlength=ncomp), out=cptr[1:])
+            for c in range(ncomp):
+                nd.run(np.sort(order[cptr[c]:cptr[c + 1]]))
+    finally:
+        sys.setrecursionlimit(old)
+    return nd.P, nd.kids
+
+
+def _group(n: int) -> int:
+    """Lanes per row for rows of length n: the smallest power of two with
+    8 loads per lane covering the row, at most a warp."""
+    g = 1
+    while g < 32 and 8 * g < n:
+        g *= 2
+    return g
+
+
+def _pad(x: int) -> int:
+    return x if x <= 32 else ((x + 31) // 32) * 32
+
+
+# ---------------------------------------------------------------------------
+
+class Multifrontal:
+    """Factor of a batch of independent block systems.
+
+    rp, col: BSR pattern (host) of the operator whose blocks are taken;
+    val_t: device tensor (nnzb, N, N) of column-major blocks (DeviceBSR.val_t);
+    sets: list of sorted block-row arrays (one system each); m: unknowns per
+    block (the leading m x m corner of every block is used);
+    vsrc / vdst: per combined vertex, index of its mode 0 in the solve's
+    input b / output x (mode a adds a)."""
+
+    def __init__(self, ctx, rp, col, val_t, N, sets, m, vsrc, vdst,
+                 leaf_unknowns: int = 192, what: str = "system",
+                 equilibrate: bool = True):
+        import time
+
+        t0 = time.perf_counter()
+        self.ctx = ctx
+        dev = ctx.device if ctx is not None else val_t.device
+        self.m = m = int(m)
+        G = SystemGraph(rp, col, sets)
+        self.G = G
+        nv = G.nv
+        self.total = nv * m
+        P_list, kids = nested_dissection(G.g_ptr, G.g_col, nv, max(1, leaf_unknowns // m))
+        nn = len(P_list)
+        self.nnodes = nn
+        owner = np.empty(nv, np.int64)
+        for t, P in enumerate(P_list):
+            owner[P] = t
+        parent = np.full(nn, -1, np.int64)
+        height = np.zeros(nn, np.int64)
+        for t in range(nn):
+            for c in kids[t]:
+                parent[c] = t
+                height[t] = max(height[t], height[c] + 1)
+        # boundaries (post-order: subtree of t has ids < t, ancestors > t)
+        B_list = []
+        for t in range(nn):
+            P = P_list[t]
+            cand = [G.g_col[_ranges(G.g_ptr[P], G.g_ptr[P + 1])]]
+            cand += [B_list[c] for c in kids[t]]
+            cand = np.unique(np.concatenate(cand))
+            Bt = cand[owner[cand] > t]
+            B_list.append(Bt[np.lexsort((Bt, owner[Bt]))])
+        pn = np.array([len(P) for P in P_list], np.int64) * m
+        bn = np.array([len(B) for B in B_list], np.int64) * m
+        self.P_list, self.B_list, self.kids, self.parent = P_list, B_list, kids, parent
+        self.height = height
+        H = int(height.max()) + 1 if nn else 0
+        self.nlevels = H
+        pp = np.array([_pad(int(x)) for x in pn], np.int64)
+        bp = np.array([_pad(int(x)) if x else 0 for x in bn], np.int64)
+
+        # position of every vertex inside its owner's P; B positions by key
+        ppos = np.empty(nv, np.int64)
+        for P in P_list:
+            ppos[P] = np.arange(len(P))
+        bkey_node = np.repeat(np.arange(nn), [len(B) for B in B_list])
+        bkey_v = np.concatenate(B_list) if nn else np.zeros(0, np.int64)
+        bkey = bkey_node * max(nv, 1) + bkey_v
+        bkey_pos = np.concatenate([np.arange(len(B)) for B in B_list]) if nn else bkey
+        so = np.argsort(bkey, kind="stable")
+        bkey, bkey_pos = bkey[so], bkey_pos[so]
+
+        def bpos(node, v):
+            i = np.searchsorted(bkey, node * max(nv, 1) + v)
+            return bkey_pos[i]
+
+        def front_pos(node, v):
+            """Padded front row of mode 0 of vertex v in node's front."""
+            inP = owner[v] == node
+            out = np.empty(len(v), np.int64)
+            out[inP] = ppos[v[inP]] * m
+            nb_ = ~inP
+            out[nb_] = pp[node[nb_]] + bpos(node[nb_], v[nb_]) * m
+            return out
+
+        t1 = time.perf_counter()
+        # ---- factor storage / workspace layout ---------------------------
+        order = np.lexsort((np.arange(nn), height))  # by height, then id
+        buckets = {}  # (h, pp, bp) -> node list
+        for t in order:
+            buckets.setdefault((int(height[t]), int(pp[t]), int(bp[t])), []).append(int(t))
+        inv_off = np.zeros(nn, np.int64)
+        lbp_off = np.zeros(nn, np.int64)
+        upb_off = np.zeros(nn, np.int64)
+        fst = 0
+        for (h, P_, B_), ts in buckets.items():
+            nb = len(ts)
+            inv_off[ts] = fst + np.arange(nb) * P_ * P_
+            fst += nb * P_ * P_
+            lbp_off[ts] = fst + np.arange(nb) * B_ * P_
+            fst += nb * B_ * P_
+            upb_off[ts] = fst + np.arange(nb) * P_ * B_
+            fst += nb * P_ * B_
+        self.F = torch.zeros(max(fst, 1), dtype=F64, device=dev)
+        def offsets(sz):  # exclusive prefix sums in (height, id) order
+            o = np.zeros(nn, np.int64)
+            o[order] = np.cumsum(sz[order]) - sz[order]
+            return o
+
+        w_off, y_off, c_off = offsets(pn + bn), offsets(pn), offsets(bn)
+        px_off, bx_off = y_off.copy(), c_off.copy()
+
+        # ---- numeric factorization, height by height ---------------------
+        a_node = np.minimum(owner[G.a_row], owner[G.a_col]) if len(G.a_row) else G.a_row
+        N = int(N)
+        vblk = val_t.view(-1, N, N)
+        # symmetric diagonal (Jacobi) equilibration, A_s = S A S with
+        # S = |diag A|^-1/2 -- SuperLU equilibrates too (splu's default
+        # Equil option); it keeps the per-front pivoting of the jump-
+        # coefficient operators (mu ratio 1000) as accurate as global
+        # partial pivoting.  x = S A_s^-1 S b: S is folded into the gather
+        # and the final write of the solve.
+        isd = G.a_row == G.a_col
+        dvert = np.full(nv, -1, np.int64)
+        dvert[G.a_row[isd]] = G.a_k[isd]
+        scale = torch.ones(nv * m, dtype=F64, device=dev)
+        if equilibrate and nv:
+            has = np.flatnonzero(dvert >= 0)
+            dg = torch.diagonal(vblk[torch.from_numpy(dvert[has]).to(dev)], dim1=1,
+                                dim2=2)[:, :m].abs()
+            sc = torch.where(dg > 0, dg.rsqrt(), torch.ones_like(dg))
+            scale.view(nv, m)[torch.from_numpy(has).to(dev)] = sc
+        scale_h = scale.cpu().numpy()
+        a_h = height[a_node] if len(a_node) else a_node
+        fronts = {}  # h -> flat tensor;  node -> (h, base, stride)
+        fbase = np.zeros(nn, np.int64)
+        fstride = pp + bp
+        last_use = np.full(H, -1, np.int64)
+        for t in range(nn):
+            if parent[t] >= 0:
+                last_use[height[t]] = max(last_use[height[t]], height[parent[t]])
+        perms = [None] * nn
+        bad_nodes = []
+        for h in range(H):
+            hb = [(k, ts) for k, ts in buckets.items() if k[0] == h]
+            size = 0
+            for (_, P_, B_), ts in hb:
+                fbase[ts] = size + np.arange(len(ts)) * (P_ + B_) ** 2
+                size += len(ts) * (P_ + B_) ** 2
+            flat = torch.zeros(max(size, 1), dtype=F64, device=dev)
+            fronts[h] = flat
+            # identity on the pivot padding
+            pad_idx = []
+            for (_, P_, B_), ts in hb:
+                for t in ts:
+                    if pn[t] < P_:
+                        i = np.arange(pn[t], P_)
+                        pad_idx.append(fbase[t] + i * (P_ + B_) + i)
+            if pad_idx:
+                flat[torch.from_numpy(np.concatenate(pad_idx)).to(dev)] = 1.0
+            # original entries whose earlier-eliminated end is a front of h
+            sel = np.flatnonzero(a_h == h)
+            if sel.size:
+                nd_ = a_node[sel]
+                rpos = front_pos(nd_, G.a_row[sel])
+                cpos = front_pos(nd_, G.a_col[sel])
+                st = fstride[nd_]
+                am = np.arange(m)
+                tgt = (fbase[nd_][:, None, None] + (rpos[:, None, None] + am[None, :, None])
+                       * st[:, None, None] + cpos[:, None, None] + am[None, None, :])
+                ks = torch.from_numpy(G.a_k[sel]).to(dev)
+                blocks = vblk[ks][:, :m, :m].transpose(1, 2)
+                sr = scale.view(nv, m)[torch.from_numpy(G.a_row[sel]).to(dev)]
+                scl = scale.view(nv, m)[torch.from_numpy(G.a_col[sel]).to(dev)]
+                blocks = blocks * sr[:, :, None] * scl[:, None, :]
+                flat[torch.from_numpy(tgt.reshape(-1)).to(dev)] = blocks.reshape(-1)
+            # children's Schur complements (extend-add), child by child
+            for t in (t for (_, _, _), ts in hb for t in ts):
+                if not kids[t]:
+                    continue
+                Ft = flat[fbase[t]:fbase[t] + fstride[t] ** 2].view(fstride[t], fstride[t])
+                for c in kids[t]:
+                    if bn[c] == 0:
+                        continue
+                    fc = fronts[int(height[c])]
+                    sc = fstride[c]
+                    S = fc[fbase[c]:fbase[c] + sc * sc].view(sc, sc)[
+                        pp[c]:pp[c] + bn[c], pp[c]:pp[c] + bn[c]]
+                    U = (front_pos(np.full(len(B_list[c]), t), B_list[c])[:, None]
+                         + np.arange(m)[None, :]).reshape(-1)
+                    Ut = torch.from_numpy(U).to(dev)
+                    Ft[Ut[:, None], Ut[None, :]] += S
+            # factor every bucket of this height
+            for (_, P_, B_), ts in hb:
+                nb = len(ts)
+                n_ = P_ + B_
+                Fb = flat[fbase[ts[0]]:fbase[ts[0]] + nb * n_ * n_].view(nb, n_, n_)
+                A = Fb[:, :P_, :P_].contiguous()
+                if P_ == 0:
+                    continue
+                LU, piv, info = (lu_factor_batched(A) if A.is_cuda
+                                 else torch.linalg.lu_factor_ex(A))
+                dg = torch.diagonal(LU, dim1=-2, dim2=-1)
+                bad = (info != 0) | ~torch.isfinite(LU).flatten(1).all(1) | (dg == 0).any(1)
+                perm = _ipiv_to_perm(ctx, piv.to(I32).contiguous(), P_)
+                if B_:
+                    FPB = Fb[:, :P_, P_:]
+                    PF = torch.gather(FPB, 1, perm.long()[:, :, None].expand(nb, P_, B_))
+                    UPB = torch.linalg.solve_triangular(LU, PF, upper=False,
+                                                        unitriangular=True)
+                    LBP = torch.linalg.solve_triangular(LU, Fb[:, P_:, :P_].contiguous(),
+                                                        upper=True, left=False)
+                    Fb[:, P_:, P_:] -= torch.bmm(LBP, UPB)
+                    bad |= ~torch.isfinite(LBP).flatten(1).all(1)
+                    o = int(lbp_off[ts[0]])
+                    self.F[o:o + nb * B_ * P_] = LBP.reshape(-1)
+                    o = int(upb_off[ts[0]])
+                    self.F[o:o + nb * P_ * B_] = UPB.reshape(-1)
+                    del FPB, PF, UPB, LBP
+                INV = triangular_inverses(LU)
+                o = int(inv_off[ts[0]])
+                self.F[o:o + nb * P_ * P_] = INV.reshape(-1)
+                bad_nodes.append((ts, bad))
+                ph = perm.cpu().numpy()
+                for q, t in enumerate(ts):
+                    perms[t] = ph[q, :pn[t]].astype(np.int64)
+                del LU, INV, A
+            for hh in range(h + 1):
+                if hh in fronts and last_use[hh] <= h:
+                    del fronts[hh]
+        for ts, bad in bad_nodes:
+            if bool(bad.any()):
+                t = ts[int(torch.nonzero(bad)[0])]
+                blk = tuple(int(b) for b in G.gblk[P_list[t][:8]])
+                raise SingularSystemError(f"{what} is singular (front on blocks {blk}...)")
+        del fronts
+        t2 = time.perf_counter()
+
+        # ---- solve plan ---------------------------------------------------
+        am = np.arange(m)
+        vsrc = np.asarray(vsrc, np.int64)
+        vdst = np.asarray(vdst, np.int64)
+        # gather entries, node by node in (height, id) order
+        ent_w, ent_src, ent_scale, lev_ent = [], [], [], [0]
+        ent_first = np.zeros(nn, np.int64)  # first entry id of each node
+        inv_perm = [None] * nn
+        cur = 0
+        for h in range(H):
+            for t in order[height[order] == h]:
+                p, b = int(pn[t]), int(bn[t])
+                ent_first[t] = cur
+                pu = perms[t]  # permuted position i <- front unknown pu[i]
+                ip = np.empty(p, np.int64)
+                ip[pu] = np.arange(p)
+                inv_perm[t] = ip
+                P = P_list[t]
+                srcP = (vsrc[P][:, None] + am[None, :]).reshape(-1)
+                ent_src.append(srcP[pu])
+                sP = scale_h.reshape(nv, m)[P].reshape(-1)
+                ent_scale.append(sP[pu])
+                ent_scale.append(np.ones(b))
+                ent_src.append(np.full(b, -1, np.int64))
+                ent_w.append(w_off[t] + np.arange(p + b))
+                cur += p + b
+            lev_ent.append(cur)
+        ent_w = np.concatenate(ent_w) if ent_w else np.zeros(0, np.int64)
+        ent_src = np.concatenate(ent_src) if ent_src else np.zeros(0, np.int64)
+        ent_scale = np.concatenate(ent_scale) if ent_scale else np.zeros(0)
+        # contributions: child c's boundary unknown j -> parent's entry
+        c_tgt, c_src = [], []
+        for c in range(nn):
+            t = parent[c]
+            if t < 0 or bn[c] == 0:
+                continue
+            Bc = B_list[c]
+            inP = owner[Bc] == t
+            fu = np.empty(len(Bc), np.int64)  # unpermuted front unknown (mode 0)
+            fu[inP] = ppos[Bc[inP]] * m
+            fu[~inP] = pn[t] + bpos(np.full(int((~inP).sum()), t), Bc[~inP]) * m
+            fu = (fu[:, None] + am[None, :]).reshape(-1)
+            ent = np.where(fu < pn[t], inv_perm[t][np.minimum(fu, max(pn[t] - 1, 0))], fu)
+            c_tgt.append(ent_first[t] + ent)
+            c_src.append(c_off[c] + np.arange(bn[c]))
+        if c_tgt:
+            c_tgt, c_src = np.concatenate(c_tgt), np.concatenate(c_src)
+            so = np.argsort(c_tgt, kind="stable")  # children in id order per entry
+            c_tgt, c_src = c_tgt[so], c_src[so]
+        else:
+            c_tgt = c_src = np.zeros(0, np.int64)
+        ent_cptr = np.zeros(len(ent_w) + 1, np.int64)
+        np.cumsum(np.bincount(c_tgt, minlength=len(ent_w)), out=ent_cptr[1:])
+        # warp tasks, level-sorted: (node, first row), 32/G rows each
+        gp = np.array([_group(int(x)) for x in pn], np.int64)
+        gb = np.array([_group(int(x)) if x else g for x, g in zip(bn, gp)], np.int64)
+
+        def tasks(phase):
+            """int4 warp tasks (node, row, seg, slot) of one phase, level by
+            level: fronts with short rows (G < 32) get 32/G rows per task;
+            rows of G = 32 fronts longer than SEG are split into SEG-column
+            segments (slot = first partial of the row, per level)."""
+            g = gb if phase == 2 else gp
+            nrows = bn if phase == 1 else pn
+            out, lev, maxslot = [], [], 0
+            for h in range(H):
+                ts = order[height[order] == h]
+                sh = ts[g[ts] < 32]
+                per = 32 // g[sh]
+                cnt = (nrows[sh] + per - 1) // per
+                first = _ranges(np.zeros(len(sh), np.int64), cnt) * np.repeat(per, cnt)
+                grp = np.stack([np.repeat(sh, cnt), first, np.zeros_like(first),
+                                np.full_like(first, -1)], 1)
+                lg = ts[g[ts] == 32]
+                rn = np.repeat(lg, nrows[lg])
+                rr = _ranges(np.zeros(len(lg), np.int64), nrows[lg])
+                if phase == 0:
+                    ln = rr
+                elif phase == 3:
+                    ln = pn[rn] - rr
+                else:
+                    ln = np.repeat((pn if phase == 1 else bn)[lg], nrows[lg])
+                nseg = np.maximum(1, (ln + SEG - 1) // SEG)
+                multi = nseg > 1
+                slot = np.full(len(rn), -1, np.int64)
+                slot[multi] = np.cumsum(nseg[multi]) - nseg[multi]
+                maxslot = max(maxslot, int(nseg[multi].sum()))
+                seg = _ranges(np.zeros(len(rn), np.int64), nseg)
+                long_ = np.stack([np.repeat(rn, nseg), np.repeat(rr, nseg), seg,
+                                  np.repeat(slot, nseg)], 1)
+                out += [grp, long_]
+                lev.append(len(grp) + len(long_))
+            return out, lev, maxslot
+
+        all_tasks, lev_task, nslot = [], [], 1
+        base = 0
+        for phase in range(4):
+            tl, lv, ms = tasks(phase)
+            all_tasks += tl
+            lev_task.append(base + np.concatenate([[0], np.cumsum(lv)]))
+            base += int(np.sum(lv))
+            nslot = max(nslot, ms)
+        task_arr = (np.concatenate(all_tasks) if all_tasks
+                    else np.zeros((0, 4), np.int64))
+        bidx = np.zeros(int(bn.sum()), np.int64)
+        pdst = np.zeros(int(pn.sum()), np.int64)
+        pscale = np.ones(int(pn.sum()))
+        for t in range(nn):
+            if bn[t]:  # Y position (owner's pivot space) of each boundary unknown
+                Bt = B_list[t]
+                bidx[c_off[t]:c_off[t] + bn[t]] = (
+                    y_off[owner[Bt]][:, None] + ppos[Bt][:, None] * m + am).reshape(-1)
+            pdst[y_off[t]:y_off[t] + pn[t]] = (vdst[P_list[t]][:, None] + am).reshape(-1)
+            pscale[y_off[t]:y_off[t] + pn[t]] = scale_h.reshape(nv, m)[P_list[t]].reshape(-1)
+        nodes = np.zeros(nn, NODE_DT)
+        nodes["p"], nodes["b"], nodes["ldp"], nodes["ldb"] = pn, bn, pp, bp
+        nodes["gp"], nodes["gb"] = gp, gb
+        nodes["inv"], nodes["lbp"], nodes["upb"] = inv_off, lbp_off, upb_off
+        nodes["w"], nodes["y"], nodes["c"] = w_off, y_off, c_off
+        nodes["bx"], nodes["px"] = bx_off, px_off
+
+        def up(a, dt):
+            return torch.from_numpy(np.ascontiguousarray(a)).to(dev, dt)
+
+        self.lev_ent = np.asarray(lev_ent, np.int64)
+        self.lev_task = np.ascontiguousarray(np.concatenate(lev_task), np.int64)
+        self.task_host = task_arr
+        self.ent_w, self.ent_src = up(ent_w, I64), up(ent_src, I64)
+        self.ent_cptr, self.ent_cidx = up(ent_cptr, I64), up(c_src, I64)
+        self.tasks = up(task_arr, I32)
+        self.part = torch.zeros(nslot, dtype=F64, device=dev)
+        self.cnt = torch.zeros(nslot, dtype=I32, device=dev)
+        self.nodes_host = nodes
+        self.nodes = torch.from_numpy(nodes.view(np.uint8).copy()).to(dev)
+        self.bidx, self.pdst = up(bidx, I64), up(pdst, I64)
+        self.ent_scale, self.pscale = up(ent_scale, F64), up(pscale, F64)
+        self.W = torch.zeros(max(int((pn + bn).sum()), 1), dtype=F64, device=dev)
+        self.Y = torch.zeros(max(int(pn.sum()), 1), dtype=F64, device=dev)
+        self.C = torch.zeros(max(int(bn.sum()), 1), dtype=F64, device=dev)
+        self.factor_bytes = 8 * int((pn * pn + 2 * pn * bn).sum())
+        self.apply_bytes = self.factor_bytes + 8 * int(4 * (pn + bn).sum() + 4 * pn.sum())
+        self.pn, self.bn = pn, bn
+        self._s = None
+        self.times = {"symbolic": t1 - t0, "numeric": t2 - t1,
+                      "plan": time.perf_counter() - t2}
+
+    # ------------------------------------------------------------------
+    def struct(self) -> XdgMf:
+        if self._s is None:
+            s = XdgMf()
+            s.nlevels, s.nnodes, s.total = self.nlevels, self.nnodes, self.total
+            s.lev_ent = self.lev_ent.ctypes.data
+            s.lev_task = self.lev_task.ctypes.data
+            for f in ("ent_w", "ent_src", "ent_cptr", "ent_cidx", "tasks", "nodes",
+                      "ent_scale", "pscale", "bidx", "pdst", "F", "W", "Y", "C", "part",
+                      "cnt"):
+                setattr(s, f, getattr(self, f).data_ptr())
+            s.apply_bytes = float(self.apply_bytes)
+            self._s = s
+        return self._s
+
+    def solve(self, b: torch.Tensor, x: torch.Tensor) -> torch.Tensor:
+        """x[vdst + a] = A^-1 b[vsrc + a] for every system (device tensors)."""
+        nat.check(self.ctx.lib.xdg_mf_solve(C.byref(self.struct()), b.data_ptr(),
+                                            x.data_ptr(), self.ctx.stream), "mf_solve")
+        return x
+
+
+def _ipiv_to_perm(ctx, piv: torch.Tensor, n: int) -> torch.Tensor:
+    """LAPACK ipiv (batch, n) -> row permutation (batch, n), int32."""
+    nb = piv.shape[0]
+    if piv.is_cuda:
+        from .direct import ipiv_to_perm
+
+        dims = torch.full((nb,), n, dtype=I32, device=piv.device)
+        off = torch.arange(nb, dtype=I64, device=piv.device) * n
+        return ipiv_to_perm(ctx, piv.reshape(-1), dims, off).view(nb, n)
+    # host tensors (CPU unit tests of the factorization)
+    ip = piv.numpy() - 1
+    perm = np.tile(np.arange(n, dtype=np.int32), (nb, 1))
+    rows = np.arange(nb)
+    for i in range(n):
+        j = ip[:, i]
+        a, b = perm[rows, i].copy(), perm[rows, j].copy()
+        perm[rows, i], perm[rows, j] = b, a
+    return torch.from_numpy(perm)

@@ -38,6 +38,28 @@ def _ranges(starts: np.ndarray, ends: np.ndarray) -> np.ndarray:
     return np.arange(lens.sum(), dtype=np.int64) + offs
 
 
+# Dense low-order factors up to this many bytes in total (and per system);
+# above, the multifrontal sparse factorization (multifrontal.py).  A dense
+# solve streams 8 n^2 bytes in 3 launches; the multifrontal one streams
+# ~8 (p^2 + 2 p b) per front in 5 launches per tree height -- for small
+# systems the launches dominate, for large ones the bytes.
+DENSE_LOW_MAX_BYTES = 1 << 30
+DENSE_LOW_MAX_SYSTEM = 6000  # unknowns
+
+
+def use_multifrontal(dims) -> bool:
+    import os
+
+    mode = os.environ.get("XDG_LOW_ORDER", "auto")
+    if mode in ("dense", "sparse"):
+        return mode == "sparse"
+    dims = np.asarray(dims, np.int64)
+    if dims.size == 0:
+        return False
+    return (8 * int((dims * dims).sum()) > DENSE_LOW_MAX_BYTES
+            or int(dims.max()) > DENSE_LOW_MAX_SYSTEM)
+
+
 class PmgPlan:
     def __init__(self, D, cell_sets, m: int, damping: torch.Tensor | None = None,
                  combine: bool = True):
@@ -101,14 +123,35 @@ class PmgPlan:
         self.lu_off = up(lu_off[:-1], I64)
         self.xlo = torch.zeros(int(vec_off[-1]), dtype=F64, device=dev)
 
+        self.total = int(vec_off[-1])
+        self.mf = None
+        if use_multifrontal(dims):
+            # ---- low-order sparse factors (solvers.py:208-221) -----------
+            from .multifrontal import Multifrontal
+
+            vsrc = np.concatenate(sets) * N if sets else np.zeros(0, np.int64)
+            vdst = vec_off[:-1][wsys] + wlrow * self.m
+            self.mf = Multifrontal(ctx, rp, col, D.val_t, N, sets, self.m, vsrc, vdst,
+                                   what="low-order system")
+            self.LU = torch.zeros(1, dtype=F64, device=dev)
+            self.src = torch.zeros(1, dtype=I32, device=dev)
+            self.row_sys = torch.zeros(1, dtype=I32, device=dev)
+            self.lu_scratch = torch.zeros(2, dtype=F64, device=dev)
+        else:
+            self._dense_low(ctx, D, sets, dims, vec_off, lu_off, up)
+        self._high_and_out(ctx, D, rp, col, nbr, sets, wcell, wlrow, wsys, vec_off,
+                           out_off, combine, damping, up)
+
+    def _dense_low(self, ctx, D, sets, dims, vec_off, lu_off, up):
+        N, dev = self.N, ctx.device
         # ---- low-order dense factors (solvers.py:208-221) ----------------
         need = 8 * int(lu_off[-1])
         free, _ = torch.cuda.mem_get_info(dev)
         if 3 * need > free:  # factor + LU + inverse temporaries
             raise NotImplementedError(
                 f"dense low-order factors need {need / 1e9:.1f} GB (largest system "
-                f"{int(dims.max())} unknowns; {free / 1e9:.0f} GB free): the sparse "
-                "low-order factorisation is not implemented yet (DESIGN.md section 7)")
+                f"{int(dims.max())} unknowns; {free / 1e9:.0f} GB free): use the "
+                "multifrontal factorization (XDG_LOW_ORDER=auto|sparse)")
         A = torch.zeros(int(lu_off[-1]), dtype=F64, device=dev)
         nat.check(ctx.lib.xdg_pmg_build_low(
             self.nwork, N, self.m, self.wi_ptr.data_ptr(),
@@ -160,10 +203,12 @@ class PmgPlan:
         # perm is local to each system: global position = base + local index
         self.src = gidx[base + perm].to(I32) if perm.numel() else perm.to(I32)
         # packed-row -> system map for the warp-per-row inverse apply
-        self.total = int(vec_off[-1])
         self.row_sys = up(np.repeat(np.arange(self.nsys), dims), I32)
         self.lu_scratch = torch.empty(2 * max(self.total, 1), dtype=F64, device=dev)
 
+    def _high_and_out(self, ctx, D, rp, col, nbr, sets, wcell, wlrow, wsys, vec_off,
+                      out_off, combine, damping, up):
+        N, dev = self.N, ctx.device
         # ---- high-order per-cell factors (solvers.py:225-243) ------------
         self.has_high = self.m < N
         if self.has_high:
@@ -238,7 +283,8 @@ class PmgPlan:
     def algorithmic_bytes(self) -> int:
         """Bytes one apply must move (SURVEY 8(d) PMG apply)."""
         N, m = self.N, self.m
-        lo = int(self.dims.double().pow(2).sum().item()) * 8
+        lo = (self.mf.apply_bytes if self.mf is not None
+              else int(self.dims.double().pow(2).sum().item()) * 8)
         hi = 0
         if self.has_high:
             nh = N - m

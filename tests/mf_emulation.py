@@ -1,0 +1,61 @@
+"""numpy restatement of xdg_mf_solve (csrc/xdg_multifrontal.cu) -- TEST
+INFRASTRUCTURE ONLY: lets the CPU suite check the multifrontal symbolic and
+numeric factorization (multifrontal.py) without a GPU."""
+import numpy as np
+
+
+def emulate_solve(mf, b, xlen):
+    F = mf.F.cpu().numpy()
+    ent_w, ent_src = mf.ent_w.cpu().numpy(), mf.ent_src.cpu().numpy()
+    cptr, cidx = mf.ent_cptr.cpu().numpy(), mf.ent_cidx.cpu().numpy()
+    nodes = mf.nodes_host
+    bidx, pdst = mf.bidx.cpu().numpy(), mf.pdst.cpu().numpy()
+    ent_scale, pscale = mf.ent_scale.cpu().numpy(), mf.pscale.cpu().numpy()
+    tasks = mf.task_host
+    H = mf.nlevels
+
+    def rows(phase, h):  # (node, row) pairs of one phase and level, in order
+        lev = mf.lev_task[phase * (H + 1):(phase + 1) * (H + 1)]
+        g, count = ("gb" if phase == 2 else "gp"), ("b" if phase == 1 else "p")
+        out = []
+        for t, r0, seg, slot in tasks[lev[h]:lev[h + 1]]:
+            nd = nodes[t]
+            if slot >= 0:
+                if seg == 0:
+                    out.append((t, r0))
+                continue
+            for r in range(r0, min(r0 + 32 // nd[g], nd[count])):
+                out.append((t, r))
+        return out
+
+    W, Y, Cb = np.zeros(mf.W.numel()), np.zeros(mf.Y.numel()), np.zeros(mf.C.numel())
+    x = np.zeros(xlen)
+    for h in range(mf.nlevels):  # forward: gather, L^-1, contributions
+        for e in range(mf.lev_ent[h], mf.lev_ent[h + 1]):
+            v = ent_scale[e] * b[ent_src[e]] if ent_src[e] >= 0 else 0.0
+            for k in range(cptr[e], cptr[e + 1]):
+                v += Cb[cidx[k]]
+            W[ent_w[e]] = v
+        for t, i in rows(0, h):
+            nd = nodes[t]
+            row = F[nd["inv"] + i * nd["ldp"]:][:i]
+            Y[nd["y"] + i] = W[nd["w"] + i] + row @ W[nd["w"]:nd["w"] + i]
+        for t, j in rows(1, h):
+            nd = nodes[t]
+            row = F[nd["lbp"] + j * nd["ldp"]:][:nd["p"]]
+            Cb[nd["c"] + j] = W[nd["w"] + nd["p"] + j] - row @ Y[nd["y"]:nd["y"] + nd["p"]]
+    for h in range(mf.nlevels - 1, -1, -1):  # backward: U_PB x_B, U^-1
+        for t, i in rows(2, h):
+            nd = nodes[t]
+            d = 0.0
+            if nd["b"]:
+                row = F[nd["upb"] + i * nd["ldb"]:][:nd["b"]]
+                d = row @ Y[bidx[nd["bx"]:nd["bx"] + nd["b"]]]
+            W[nd["w"] + i] = Y[nd["y"] + i] - d
+        for t, i in rows(3, h):
+            nd = nodes[t]
+            p = nd["p"]
+            row = F[nd["inv"] + i * nd["ldp"]:][:p]
+            Y[nd["y"] + i] = row[i:] @ W[nd["w"] + i:nd["w"] + p]
+            x[pdst[nd["px"] + i]] = pscale[nd["px"] + i] * Y[nd["y"] + i]
+    return x

@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--k-lo", type=int, default=None)
     ap.add_argument("--max-it", type=int, default=3000)
     ap.add_argument("--rm-cols", type=int, default=200)
+    ap.add_argument("--restart", type=int, default=50)
     a = ap.parse_args()
     from paper_2003_02431_b200.case import BenchCase, assemble_case
     from paper_2003_02431_b200.solvers import SolverConfig, gmres_pmg_solve, ortho_mg_solve
@@ -54,7 +55,10 @@ def main():
         lv = H.level(1)
         cfg = SolverConfig(tolerance=a.tol, max_iterations=a.max_it,
                            k_lo=(case.resolved_k_lo if a.k_lo is None else a.k_lo,),
-                           num_levels=a.levels, rm_max_columns=a.rm_cols)
+                           num_levels=a.levels, rm_max_columns=a.rm_cols,
+                           gmres_restart=a.restart)
+        from paper_2003_02431_b200 import solvers as S
+
         t0 = time.perf_counter()
         if a.solve == "omg":
             x, rep = ortho_mg_solve(H, lv.rhs, None, cfg, 1)
@@ -62,7 +66,8 @@ def main():
             x, rep = gmres_pmg_solve(lv.matrix, lv.rhs, cfg, dim=a.dim)
         out.update(solve=a.solve, solve_s=round(time.perf_counter() - t0, 3),
                    iterations=rep.iterations, converged=rep.converged,
-                   final_residual=rep.final_residual)
+                   final_residual=rep.final_residual,
+                   loop=(dict(S.LAST_LOOP) if a.solve != "omg" else None))
     print(json.dumps(out), flush=True)
 
 
