@@ -209,8 +209,44 @@ def run_reference(args):
 
 # ---------------------------------------------------------------------------
 
+CFG2_META = {  # BASELINE config 2: 32^3, p=3, sphere r=0.6, mu 1/1000
+    "name": "cfg2", "dim": 3, "cells": 32, "degree": 3, "num_levels": 3,
+    "omg": {"tolerance": 1e-10, "max_iterations": 2000, "k_lo": 2, "rm_max_columns": 800,
+            "num_levels": 3},
+    "gmres": {"tolerance": 1e-10, "max_iterations": 10000, "k_lo": 2, "gmres_restart": 50}}
+
+
+def native_cfg2(world: int = 1):
+    """BASELINE config 2 built by this package's own setup pipeline
+    (case.assemble_case: geometry, agglomeration, SIP assembly, hierarchy);
+    returns (hierarchy, meta, setup row)."""
+    from paper_2003_02431_b200.case import BenchCase, assemble_case
+
+    c = np.random.default_rng(0).uniform(-0.1, 0.1, 3)
+    case = BenchCase(dim=3, cells=32, degree=3, levelset="sphere",
+                     levelset_params={"center": tuple(c), "radius": 0.6}, mu_a=1.0,
+                     mu_b=1000.0, alpha=0.1, num_levels=3,
+                     workers=max(1, (os.cpu_count() or 1) // world))
+    t0 = time.perf_counter()
+    asm = assemble_case(case)
+    setup = time.perf_counter() - t0
+    meta = dict(CFG2_META, dofs_raw=int(len(asm.rhs)))
+    row = {"case": "cfg2", "what": "native setup (mesh, cut cells, agglomeration, SIP "
+                                   "assembly, 3-level hierarchy)",
+           "setup_s": setup, "phases": {k: round(v, 3) for k, v in asm.phase_times.items()},
+           "dofs_raw": meta["dofs_raw"], "level_blocks": [
+               asm.hierarchy.level(lam).data.num_blocks
+               for lam in range(1, asm.hierarchy.num_levels + 1)],
+           "reference_setup_s_build_container": 847.8,
+           "reference_setup_source": "tests/golden/make_large.py cfg2 (cutdg assemble_case, "
+                                     "1 host thread)"}
+    return asm.hierarchy, meta, row
+
+
 def time_solves(torch, budget_s: float):
-    """XDG solves on the serialized reference hierarchies: DOF/s per solve."""
+    """XDG solves: DOF/s per solve on the reference's serialized hierarchies
+    (cfg1, 8^3 p=3 sphere, and the full-size cfg2 when its fixture is
+    present) or on the natively built cfg2 hierarchy otherwise."""
     from paper_2003_02431_b200 import solvers as S
     from paper_2003_02431_b200.hierarchy import load_hierarchy
     from paper_2003_02431_b200.solvers import SolverConfig, gmres_pmg_solve, ortho_mg_solve
@@ -225,15 +261,28 @@ def time_solves(torch, budget_s: float):
     torch.linalg.solve_triangular(eye, eye, upper=True)
     torch.cuda.synchronize()
 
+    def cases():
+        for case in ("cfg1", "sphere8p3", "large/s16p3"):
+            path = os.path.join(ROOT, "tests", "golden", f"{case}.npz")
+            if os.path.exists(path):
+                z = np.load(path)
+                yield case, z, json.loads(bytes(z["meta"]).decode()), load_hierarchy(z), None
+        path = os.path.join(ROOT, "tests", "golden", "large", "cfg2.npz")
+        if os.path.exists(path) and not os.environ.get("XDG_BENCH_NATIVE_CFG2"):
+            z = np.load(path)
+            meta = json.loads(bytes(z["meta"]).decode())
+            meta["gmres"] = dict(meta["gmres"], max_iterations=CFG2_META["gmres"][
+                "max_iterations"])
+            yield "large/cfg2", z, meta, load_hierarchy(z), None
+        else:
+            hier, meta, row = native_cfg2()
+            yield "cfg2 (native setup)", {}, meta, hier, row
+
     out = []
     t_start = time.perf_counter()
-    for case in ("cfg1", "sphere8p3", "large/s16p3", "large/cfg2"):
-        path = os.path.join(ROOT, "tests", "golden", f"{case}.npz")
-        if not os.path.exists(path):
-            continue
-        z = np.load(path)
-        meta = json.loads(bytes(z["meta"]).decode())
-        hier = load_hierarchy(z)
+    for case, z, meta, hier, setup_row in cases():
+        if setup_row is not None:
+            out.append(setup_row)
         lv = hier.level(1)
         for solver in ("gmres", "omg"):
             if time.perf_counter() - t_start > budget_s:
@@ -269,7 +318,9 @@ def time_solves(torch, budget_s: float):
                 "ref_iterations_envelope": ([int(z[f"{solver}_envelope"].min()),
                                              int(z[f"{solver}_envelope"].max())]
                                             if f"{solver}_envelope" in z else None),
-                "converged": rep.converged, "solve_s": rep.time_iterations,
+                "converged": rep.converged, "final_residual": rep.final_residual,
+                "relative_residual": rep.final_residual / float(np.linalg.norm(lv.rhs)),
+                "solve_s": rep.time_iterations,
                 "dof_per_s": meta["dofs_raw"] / rep.time_iterations,
                 "ms_per_iteration": 1e3 * rep.time_iterations / max(rep.iterations, 1),
                 "setup_s": loop["setup_seconds"], "loop_s": loop["seconds"],
@@ -353,11 +404,12 @@ def time_dist_solve(torch, dist):
     from paper_2003_02431_b200.solvers import SolverConfig
 
     path = os.path.join(ROOT, "tests", "golden", "large", "cfg2.npz")
-    if not os.path.exists(path):
-        return {"skipped": "tests/golden/large/cfg2.npz absent"}
-    z = np.load(path)
-    meta = json.loads(bytes(z["meta"]).decode())
-    hier = load_hierarchy(z)
+    if os.path.exists(path):
+        z = np.load(path)
+        meta = json.loads(bytes(z["meta"]).decode())
+        hier = load_hierarchy(z)
+    else:  # every rank builds the hierarchy with its share of the host cores
+        hier, meta, _ = native_cfg2(dist.get_world_size())
     dist.barrier()
     x, (r0, r1), rep = dist_ortho_mg_solve(hier, np.asarray(hier.level(1).rhs),
                                            SolverConfig(**meta["omg"]))
@@ -551,7 +603,7 @@ def main():
     ap.add_argument("--n", type=int, default=128)
     ap.add_argument("--ref-sample", type=int, default=48)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
-    ap.add_argument("--solve-budget", type=float, default=120.0)
+    ap.add_argument("--solve-budget", type=float, default=240.0)
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

@@ -35,37 +35,38 @@ constexpr int kT = 256;
 // rows get the whole warp).  Lanes of a group stride G through the row, 8
 // loads in flight per lane, fixed accumulation order; the group sum is a
 // shuffle-xor tree inside the aligned group (deterministic).
+#ifndef MF_U
+#define MF_U 8  // loads in flight per lane per chunk
+#endif
+#ifndef MF_MINB
+#define MF_MINB 3  // resident CTAs per SM the row kernels are compiled for
+#endif
+
 template <typename V>
 __device__ __forceinline__ double group_dot(const double* __restrict__ row, V v,
                                             int j0, int j1, int gl, int G,
                                             bool active) {
-  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  double a[4] = {0.0, 0.0, 0.0, 0.0};
   if (active) {
-    const int step = 8 * G;
+    const int step = MF_U * G;
     for (int jb = j0; jb < j1; jb += step) {
-      // clamped (always valid) unpredicated loads, so all 16 are issued
-      // before the first FMA; out-of-row lanes are zeroed afterwards
-      double r[8], q[8];
+      // clamped (always valid) unpredicated loads, so all of them are
+      // issued before the first FMA; out-of-row lanes are zeroed afterwards
+      double r[MF_U], q[MF_U];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < MF_U; ++u) {
         const int j = min(jb + gl + G * u, j1 - 1);
         r[u] = __ldg(row + j);
         q[u] = v(j);
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
+      for (int u = 0; u < MF_U; ++u)
         if (jb + gl + G * u >= j1) r[u] = 0.0;
-      a0 = fma(r[0], q[0], a0);
-      a1 = fma(r[1], q[1], a1);
-      a2 = fma(r[2], q[2], a2);
-      a3 = fma(r[3], q[3], a3);
-      a0 = fma(r[4], q[4], a0);
-      a1 = fma(r[5], q[5], a1);
-      a2 = fma(r[6], q[6], a2);
-      a3 = fma(r[7], q[7], a3);
+#pragma unroll
+      for (int u = 0; u < MF_U; ++u) a[u & 3] = fma(r[u], q[u], a[u & 3]);
     }
   }
-  double s = (a0 + a1) + (a2 + a3);
+  double s = (a[0] + a[1]) + (a[2] + a[3]);
   for (int o = 16; o > 0; o >>= 1)
     if (o < G) s += __shfl_xor_sync(0xffffffffu, s, o);
   return s;
@@ -106,7 +107,10 @@ mf_gather_kernel(int64_t e0, int64_t e1, const int64_t* __restrict__ ent_w,
 }
 
 enum Phase { kLower = 0, kBound = 1, kUpb = 2, kUpper = 3 };
-constexpr int kSeg = 1024;  // row segment of a split long row (8 KB)
+#ifndef MF_SEG
+#define MF_SEG 4096
+#endif
+constexpr int kSeg = MF_SEG;  // row segment of a split long row (32 KB)
 
 // The four row phases (p = pivot unknowns, b = boundary unknowns of a front):
 //   kLower  Y[i]  = W[i] + L^-1[i, :i] . W[:i]              rows: P, G = gp
@@ -170,7 +174,7 @@ __device__ __forceinline__ void row_done(const Ctx& c, const xdg_mf_node& nd, in
 // deterministic -- and finishes the row.  Equal-sized segments keep every
 // launch free of long-row tails.
 template <int PH>
-__global__ void __launch_bounds__(kT, 4)
+__global__ void __launch_bounds__(kT, MF_MINB)
 mf_rows_kernel(int64_t t0, int64_t ntasks, const int4* __restrict__ tasks, Ctx c) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = (int64_t)gridDim.x * (kT / 32);

@@ -167,9 +167,11 @@ class DeviceDirect:
 
 
 # Above this many unknowns (uniform block layouts) the stored factorization
-# is the multifrontal one (multifrontal.py): a dense solve streams 8 n^2
-# bytes (134 MB at n = 4096).
-SPARSE_DIRECT_MIN = 4096
+# is the multifrontal one (multifrontal.py).  A dense solve streams 8 n^2
+# bytes in 3 launches, the multifrontal one far fewer bytes in ~5 launches
+# per tree height: at n = 10,480 (cfg2 coarsest level) dense takes ~0.15 ms
+# and multifrontal 0.25 ms (launch-bound), so dense stays up to here.
+SPARSE_DIRECT_MIN = 16000
 
 
 def _sparse_direct(M, n: int) -> bool:

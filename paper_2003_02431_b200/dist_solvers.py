@@ -32,7 +32,13 @@ import torch.distributed as dist
 
 from . import _native as nat
 from .device import Context, DeviceBSR
-from .direct import DeviceDirect, dense_from_device_bsr, ipiv_to_perm
+from .direct import (
+    SPARSE_DIRECT_MIN,
+    DeviceDirect,
+    SparseDirect,
+    dense_from_device_bsr,
+    ipiv_to_perm,
+)
 from .distributed import DistributedSpMV, HaloPlan
 from .errors import SingularSystemError
 from .solvers import SolverConfig, SolverReport, space_dimension
@@ -121,12 +127,16 @@ class DistPmg:
         # replicated low-order factor from the global blocks' (:m, :m) parts
         lo_val = np.ascontiguousarray(np.asarray(val)[:, :m, :m])
         Dlo = DeviceBSR.from_arrays(rp, col, lo_val, m, nbr, ctx)
-        A = dense_from_device_bsr(Dlo)
         try:
-            self.low = DeviceDirect(A, ctx, "low-order system")
+            if nbr * m > SPARSE_DIRECT_MIN:  # multifrontal (cfg2: 336,610 unknowns)
+                self.low = SparseDirect(Dlo, ctx, "low-order system")
+            else:
+                A = dense_from_device_bsr(Dlo)
+                self.low = DeviceDirect(A, ctx, "low-order system")
+                del A
         except SingularSystemError as exc:
             raise SingularSystemError("low-order system is singular") from exc
-        del A, Dlo
+        del Dlo
         self.blo_own = torch.empty(nloc * m, dtype=F64, device=dev)
         self.xlo = torch.empty(nbr * m, dtype=F64, device=dev)
         self.rows_global = torch.arange(op.r0, op.r1, dtype=I32, device=dev)
@@ -546,8 +556,9 @@ def dist_ortho_mg_solve(hierarchy, b, config: SolverConfig, *, group=None):
         d = dict(N=N, P=P, r0=int(P[comm.rank]), r1=int(P[comm.rank + 1]))
         coarsest = lam == nl or lv.restriction is None
         if coarsest:
-            A = dense_from_device_bsr(DeviceBSR.from_arrays(rp, col, val, N, nb, ctx))
-            d["direct"] = DeviceDirect(A, ctx)
+            Dc = DeviceBSR.from_arrays(rp, col, val, N, nb, ctx)
+            d["direct"] = (SparseDirect(Dc, ctx) if nb * N > SPARSE_DIRECT_MIN
+                           else DeviceDirect(dense_from_device_bsr(Dc), ctx))
             d["counts"] = [int(P[q + 1] - P[q]) * N for q in range(comm.world)]
             d["coarsest"] = True
             L.append(d)

@@ -51,7 +51,9 @@ NODE_DT = np.dtype([("p", "<i4"), ("b", "<i4"), ("ldp", "<i4"), ("ldb", "<i4"),
                     ("inv", "<i8"), ("lbp", "<i8"), ("upb", "<i8"), ("w", "<i8"),
                     ("y", "<i8"), ("c", "<i8"), ("bx", "<i8"), ("px", "<i8")])
 assert NODE_DT.itemsize == 96
-SEG = 1024  # columns per segment of a split long row (kSeg, xdg_multifrontal.cu)
+# columns per segment of a split long row (kSeg, xdg_multifrontal.cu)
+SEG = int(__import__("os").environ.get("XDG_MF_SEG", "4096"))
+MF_U = int(__import__("os").environ.get("XDG_MF_U", "8"))  # loads per lane (MF_U)
 
 _vp = C.c_void_p
 
@@ -209,7 +211,7 @@ def _group(n: int) -> int:
     """Lanes per row for rows of length n: the smallest power of two with
     8 loads per lane covering the row, at most a warp."""
     g = 1
-    while g < 32 and 8 * g < n:
+    while g < 32 and MF_U * g < n:
         g *= 2
     return g
 

@@ -38,13 +38,15 @@ def _ranges(starts: np.ndarray, ends: np.ndarray) -> np.ndarray:
     return np.arange(lens.sum(), dtype=np.int64) + offs
 
 
-# Dense low-order factors up to this many bytes in total (and per system);
-# above, the multifrontal sparse factorization (multifrontal.py).  A dense
-# solve streams 8 n^2 bytes in 3 launches; the multifrontal one streams
-# ~8 (p^2 + 2 p b) per front in 5 launches per tree height -- for small
-# systems the launches dominate, for large ones the bytes.
-DENSE_LOW_MAX_BYTES = 1 << 30
-DENSE_LOW_MAX_SYSTEM = 6000  # unknowns
+# Low-order factor selection.  A dense solve streams 8 n^2 bytes in 3
+# launches; the multifrontal one ~8 (p^2 + 2 p b) per front in 5 launches per
+# tree height.  Measured on B200 (cfg2, 32^3 p=3): for the Schwarz blocks'
+# ~1,800-unknown systems dense is faster (OMG 18.2 s vs 19.1 s); for the
+# 336,610-unknown global system of GMRES-PMG dense is impossible (906 GB) and
+# the multifrontal solve streams 12.2 GB in 2.6 ms.  Sparse when a system is
+# larger than DENSE_LOW_MAX_SYSTEM unknowns or the dense factors would take
+# more than a quarter of the free device memory.
+DENSE_LOW_MAX_SYSTEM = 16000  # unknowns
 
 
 def use_multifrontal(dims) -> bool:
@@ -56,8 +58,9 @@ def use_multifrontal(dims) -> bool:
     dims = np.asarray(dims, np.int64)
     if dims.size == 0:
         return False
-    return (8 * int((dims * dims).sum()) > DENSE_LOW_MAX_BYTES
-            or int(dims.max()) > DENSE_LOW_MAX_SYSTEM)
+    free, _ = torch.cuda.mem_get_info()
+    return (int(dims.max()) > DENSE_LOW_MAX_SYSTEM
+            or 3 * 8 * int((dims * dims).sum()) > free // 4)
 
 
 class PmgPlan:

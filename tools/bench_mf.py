@@ -1,0 +1,56 @@
+"""Time the multifrontal solve (xdg_mf_solve) on a fixture's level operator.
+
+    python tools/bench_mf.py tests/golden/large/cfg2.npz [m] [level]
+
+Builds the factor of the level's low-order system (leading m modes of
+every block; m = N: the full operator), times solves with CUDA events on the
+launching stream and reports algorithmic GB/s (factor + vector bytes)."""
+import json
+import os
+import statistics
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2003_02431_b200.blockmatrix import BlockSparseMatrix, uniform_layout  # noqa: E402
+from paper_2003_02431_b200.device import Context  # noqa: E402
+from paper_2003_02431_b200.hierarchy import fixture_array  # noqa: E402
+from paper_2003_02431_b200.multifrontal import Multifrontal  # noqa: E402
+
+path = sys.argv[1]
+m = int(sys.argv[2]) if len(sys.argv) > 2 else 10
+lam = int(sys.argv[3]) if len(sys.argv) > 3 else 1
+z = np.load(path)
+rp, col = z[f"L{lam}_row_ptr"], z[f"L{lam}_col"]
+val = fixture_array(z, f"L{lam}_val")
+N = val.shape[1]
+nb = len(rp) - 1
+M = BlockSparseMatrix.from_bsr(rp, col, val, uniform_layout(nb, N), uniform_layout(nb, N))
+ctx = Context.get()
+D = M.device(ctx)
+t0 = time.perf_counter()
+v = np.arange(nb, dtype=np.int64)
+mf = Multifrontal(ctx, rp, col, D.val_t, N, [v], m, v * N, v * m)
+torch.cuda.synchronize()
+setup = time.perf_counter() - t0
+b = torch.randn(nb * N, dtype=torch.float64, device=ctx.device)
+x = torch.zeros(nb * m, dtype=torch.float64, device=ctx.device)
+for _ in range(3):
+    mf.solve(b, x)
+ts = []
+for _ in range(20):
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    mf.solve(b, x)
+    e.record()
+    e.synchronize()
+    ts.append(s.elapsed_time(e))
+ms = statistics.median(ts)
+print(json.dumps({"lib": os.environ.get("XDG_LIB", "default"), "m": m, "level": lam,
+                  "unknowns": nb * m, "nodes": mf.nnodes, "levels": mf.nlevels,
+                  "factor_GB": mf.factor_bytes / 1e9, "setup_s": round(setup, 3),
+                  "times": {k: round(v, 3) for k, v in mf.times.items()},
+                  "solve_ms": ms, "GBs": mf.apply_bytes / ms / 1e6}))
