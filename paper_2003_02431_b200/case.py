@@ -251,9 +251,11 @@ def _assemble_case(case: BenchCase, keep_terms: bool) -> Assembled:
     ctx_sync()
     times["assembly_device"] = time.perf_counter() - t0
     pidx = PieceIndex.build(cm.species_volume)
-    H, _R0 = build_hierarchy(cm, basis, pidx, raw, terms.rhs, groups, times, ctx)
+    H, R0 = build_hierarchy(cm, basis, pidx, raw, terms.rhs, groups, times, ctx)
     ctx_sync()
     lay = uniform_layout(pidx.num_blocks, basis.size)
+    H.to_level1 = BlockSparseMatrix.from_bsr(
+        R0[0], R0[1], R0[2], lay, uniform_layout(H.level(1).data.num_blocks, basis.size))
     return Assembled(cm, basis, pidx, BlockSparseMatrix.from_device(raw, lay, lay), terms.rhs,
                      H, times, terms if keep_terms else None)
 

@@ -77,6 +77,7 @@ class HierarchyLevel:
 class MultigridHierarchy:
     levels: list
     meta: dict
+    to_level1: object = None  # R0: raw (cell, species) blocks -> level-1 aggregates
 
     @property
     def num_levels(self) -> int:

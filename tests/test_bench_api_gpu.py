@@ -1,0 +1,54 @@
+"""cutdg.bench drop-in (paper_2003_02431_b200.bench): sweep rows, the
+matrix-operation micro-benchmark and the MatrixMarket export on this
+package's setup pipeline, against the reference's own outputs for the same
+case (tests/golden/sweep_case.json, made by make_sweep_golden.py)."""
+import json
+import os
+import re
+
+import pytest
+
+from conftest import GOLDEN
+from paper_2003_02431_b200.bench import (
+    MATOPS_CSV_HEADER,
+    SWEEP_CSV_HEADER,
+    BenchCase,
+    export_case_matrix,
+    format_rows,
+    micro_bench_matops,
+    run_sweep,
+)
+
+pytestmark = pytest.mark.gpu
+G = json.load(open(os.path.join(GOLDEN, "sweep_case.json")))
+
+
+def test_sweep_rows_match_reference(tmp_path):
+    base = BenchCase(**G["case"])
+    out = tmp_path / "sweep.csv"
+    rows = run_sweep([8], [2], ["direct", "omg", "gmres-pmg"], base_case=base, out=str(out))
+    assert open(out).read().splitlines()[0] == SWEEP_CSV_HEADER
+    assert len(rows) == len(G["sweep_rows"])
+    for got, ref in zip(rows, G["sweep_rows"]):
+        assert got[:4] == ref[:4]                     # grid, k, dofs (raw), solver
+        assert got[5] is True and ref[5] is True      # converged
+        assert float(got[9]) <= 1e-10 or got[3] == "direct"
+        for col in (6, 7, 8):                         # ms with 3 decimals
+            assert re.fullmatch(r"\d+\.\d{3}", got[col])
+        assert re.fullmatch(r"\d\.\d{6}e[+-]\d\d", got[9])
+        if ref[3] != "direct":  # iteration counts: chaotic at 1e-10, same regime
+            assert 0.75 * ref[4] <= got[4] <= 1.25 * ref[4], (got, ref)
+
+
+def test_matops_and_export(tmp_path):
+    base = BenchCase(**G["case"])
+    rows = micro_bench_matops(base, repetitions=3)
+    assert [r[0] for r in rows] == ["matvec", "matmat"]
+    assert rows[0][3] == G["matops_rows"][0][3]
+    assert format_rows(MATOPS_CSV_HEADER, rows).splitlines()[0] == MATOPS_CSV_HEADER
+    p = tmp_path / "m.mtx"
+    n = export_case_matrix(base, str(p))
+    assert n == G["export_dim"]
+    head = open(p).read().splitlines()
+    assert head[0] == G["export_head"][0]
+    assert [ln for ln in head if not ln.startswith("%")][0] == G["export_head"][2]
