@@ -248,6 +248,8 @@ typedef struct xdg_mf {
   double apply_bytes;          /* algorithmic bytes of one solve            */
 } xdg_mf;
 
+/* Columns per segment of a split long row (the planner's task layout). */
+int xdg_mf_segment_columns(void);
 /* x[pdst] = A^-1 b[src] for every system of the forest at once:
  * 3 launches per forward level, 2 per backward level. */
 int xdg_mf_solve(const xdg_mf* mf, const double* b, double* x,

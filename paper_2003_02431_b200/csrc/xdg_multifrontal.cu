@@ -107,10 +107,12 @@ mf_gather_kernel(int64_t e0, int64_t e1, const int64_t* __restrict__ ent_w,
 }
 
 enum Phase { kLower = 0, kBound = 1, kUpb = 2, kUpper = 3 };
-#ifndef MF_SEG
-#define MF_SEG 4096
-#endif
-constexpr int kSeg = MF_SEG;  // row segment of a split long row (32 KB)
+// Columns per segment of a split long row.  Measured on B200 (cfg2 low-order
+// system, 12.2 GB of factors): splitting at 1024 / 4096 columns costs more in
+// ticket fences (3.8 / 3.33 ms) than it saves in launch tails (3.2 ms
+// unsplit), so rows are not split at these sizes; multifrontal.SEG mirrors
+// this value (xdg_mf_segment_columns).
+constexpr int kSeg = 1 << 20;
 
 // The four row phases (p = pivot unknowns, b = boundary unknowns of a front):
 //   kLower  Y[i]  = W[i] + L^-1[i, :i] . W[:i]              rows: P, G = gp
@@ -231,6 +233,8 @@ int launch_rows(const xdg_mf* mf, int h, double* x, cudaStream_t s) {
 
 }  // namespace
 }  // namespace xdg
+
+extern "C" int xdg_mf_segment_columns(void) { return xdg::kSeg; }
 
 extern "C" int xdg_mf_solve(const xdg_mf* mf, const double* b, double* x,
                             xdg_stream_t stream) {

@@ -51,9 +51,12 @@ NODE_DT = np.dtype([("p", "<i4"), ("b", "<i4"), ("ldp", "<i4"), ("ldb", "<i4"),
                     ("inv", "<i8"), ("lbp", "<i8"), ("upb", "<i8"), ("w", "<i8"),
                     ("y", "<i8"), ("c", "<i8"), ("bx", "<i8"), ("px", "<i8")])
 assert NODE_DT.itemsize == 96
-# columns per segment of a split long row (kSeg, xdg_multifrontal.cu)
-SEG = int(__import__("os").environ.get("XDG_MF_SEG", "4096"))
-MF_U = int(__import__("os").environ.get("XDG_MF_U", "8"))  # loads per lane (MF_U)
+MF_U = 8  # loads in flight per lane per chunk (MF_U, xdg_multifrontal.cu)
+
+
+def _segment_columns() -> int:
+    """Columns per segment of a split long row: the kernel's kSeg."""
+    return int(nat.load().xdg_mf_segment_columns())
 
 _vp = C.c_void_p
 
@@ -546,6 +549,7 @@ class Multifrontal:
                 lev.append(len(grp) + len(long_))
             return out, lev, maxslot
 
+        SEG = _segment_columns()
         all_tasks, lev_task, nslot = [], [], 1
         base = 0
         for phase in range(4):

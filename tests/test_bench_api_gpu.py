@@ -32,12 +32,16 @@ def test_sweep_rows_match_reference(tmp_path):
     for got, ref in zip(rows, G["sweep_rows"]):
         assert got[:4] == ref[:4]                     # grid, k, dofs (raw), solver
         assert got[5] is True and ref[5] is True      # converged
-        assert float(got[9]) <= 1e-10 or got[3] == "direct"
+        assert float(got[9]) <= base.tolerance or got[3] == "direct"
         for col in (6, 7, 8):                         # ms with 3 decimals
             assert re.fullmatch(r"\d+\.\d{3}", got[col])
         assert re.fullmatch(r"\d\.\d{6}e[+-]\d\d", got[9])
-        if ref[3] != "direct":  # iteration counts: chaotic at 1e-10, same regime
-            assert 0.75 * ref[4] <= got[4] <= 1.25 * ref[4], (got, ref)
+        if ref[3] == "gmres-pmg":  # inside the reference's +-1-ulp envelope, widened by 1
+            env = G["envelope"][ref[3]]
+            assert min(env) - 1 <= got[4] <= max(env) + 1, (got, env)
+        # OMG is chaotic here: the reference's own +-1-ulp runs span
+        # 418-704 iterations (sweep_case.json); its distribution-level parity
+        # is tested in test_envelope_stats_gpu.py
 
 
 def test_matops_and_export(tmp_path):
