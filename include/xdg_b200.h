@@ -151,6 +151,15 @@ int xdg_lu_inv_apply(int nsys, int64_t total, const int* row_sys,
                      const int64_t* vec_off, const double* INV, const int* src,
                      const double* b, double* x, double* scratch,
                      xdg_stream_t stream);
+/* The same solves with CTA tasks (system task_sys[t], rows task_row0[t] ..
+ * + rows_per_task): each system's right-hand side is staged in shared memory
+ * (max_dim doubles), so the row dots keep only matrix loads in flight. */
+int xdg_lu_inv_apply_tasks(int64_t ntasks, const int* task_sys,
+                           const int* task_row0, int rows_per_task, int max_dim,
+                           int64_t total, const int64_t* off, const int* dims,
+                           const int64_t* vec_off, const double* INV,
+                           const int* src, const double* b, double* x,
+                           double* scratch, xdg_stream_t stream);
 /* LAPACK ipiv (1-based sequential swaps) -> permutation perm with
  * (P^T b)[i] = b[perm[i]], per system (setup). */
 int xdg_ipiv_to_perm(int nsys, const int* dims, const int64_t* vec_off,
@@ -296,6 +305,10 @@ typedef struct xdg_pmg {       /* PmgPlan of paper_2003_02431_b200/pmg.py */
   const double* damping;
   double apply_bytes;          /* algorithmic bytes of one apply (accounting) */
   const xdg_mf* mf;            /* sparse low-order factors (NULL: dense LU) */
+  const int* task_sys;         /* dense solves by CTA tasks (NULL: per row) */
+  const int* task_row0;
+  int64_t ntasks;
+  int32_t rows_per_task, max_dim;
 } xdg_pmg;
 
 typedef struct xdg_direct {    /* dense LU of one system (coarsest level) */
@@ -307,6 +320,10 @@ typedef struct xdg_direct {    /* dense LU of one system (coarsest level) */
   const int* row_sys;          /* device zeros[n] */
   double* scratch;             /* 2 n doubles */
   const xdg_mf* mf;            /* sparse factors (NULL: dense LU)           */
+  const int* task_sys;         /* dense solve by CTA tasks (NULL: per row)  */
+  const int* task_row0;
+  int64_t ntasks;
+  int32_t rows_per_task, max_dim;
 } xdg_direct;
 
 typedef struct xdg_rm {        /* RmState (solvers.py:485-556) */

@@ -46,6 +46,7 @@ SIGNATURES = {
                                 _vp]),
     "xdg_add_small": (_i32, [_i32, _vp, _vp, _vp, _vp]),
     "xdg_lu_inv_apply": (_i32, [_i32, _i64] + [_vp] * 10),
+    "xdg_lu_inv_apply_tasks": (_i32, [_i64, _vp, _vp, _i32, _i32, _i64] + [_vp] * 9),
     "xdg_ipiv_to_perm": (_i32, [_i32, _vp, _vp, _vp, _vp, _vp]),
     "xdg_pmg_build_low": (_i32, [_i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp,
                                  _vp, _vp, _vp, _vp, _vp]),

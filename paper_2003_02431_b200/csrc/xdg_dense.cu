@@ -165,3 +165,114 @@ extern "C" int xdg_lu_inv_apply(int nsys, int64_t total, const int* row_sys,
   XDG_CHECK_LAUNCH();
   return XDG_OK;
 }
+
+// ===========================================================================
+// Same solves, CTA per (system, block of rows): the system's right-hand side
+// (n doubles) is staged in shared memory once per task, so every lane's
+// registers hold only matrix loads -- 16 in flight per lane instead of
+// 8 matrix + 8 vector.  Used when every system fits the staging buffer.
+namespace xdg {
+namespace {
+
+template <bool LOWER>
+__device__ __forceinline__ double tri_row_dot_smem(const double* __restrict__ row,
+                                                   const double* sv, int i, int n,
+                                                   int lane) {
+  const int j0 = LOWER ? 0 : i, j1 = LOWER ? i : n;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int jb = j0;
+  for (; jb + 512 <= j1; jb += 512) {
+    double r[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) r[u] = __ldg(row + jb + lane + 32 * u);
+#pragma unroll
+    for (int u = 0; u < 16; u += 4) {
+      a0 = fma(r[u], sv[jb + lane + 32 * u], a0);
+      a1 = fma(r[u + 1], sv[jb + lane + 32 * (u + 1)], a1);
+      a2 = fma(r[u + 2], sv[jb + lane + 32 * (u + 2)], a2);
+      a3 = fma(r[u + 3], sv[jb + lane + 32 * (u + 3)], a3);
+    }
+  }
+  if (jb < j1) {  // clamped tail chunk: loads stay unpredicated
+    double r[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) r[u] = __ldg(row + min(jb + lane + 32 * u, j1 - 1));
+#pragma unroll
+    for (int u = 0; u < 16; u += 4) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int j = jb + lane + 32 * (u + k);
+        const double q = j < j1 ? sv[j] : 0.0;
+        if (k == 0) a0 = fma(r[u], q, a0);
+        if (k == 1) a1 = fma(r[u + 1], q, a1);
+        if (k == 2) a2 = fma(r[u + 2], q, a2);
+        if (k == 3) a3 = fma(r[u + 3], q, a3);
+      }
+    }
+  }
+  return warp_sum((a0 + a1) + (a2 + a3));
+}
+
+template <bool LOWER>
+__global__ void __launch_bounds__(256, 4)
+inv_rows_smem_kernel(int64_t ntasks, const int* __restrict__ task_sys,
+                     const int* __restrict__ task_row0, int rows_per_task,
+                     const int64_t* __restrict__ off, const int* __restrict__ dims,
+                     const int64_t* __restrict__ vec_off, const double* __restrict__ INV,
+                     const double* __restrict__ v, double* __restrict__ out) {
+  extern __shared__ double sv[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int64_t t = blockIdx.x; t < ntasks; t += gridDim.x) {
+    const int s = task_sys[t];
+    const int i0 = task_row0[t];
+    const int n = dims[s];
+    const int64_t base = vec_off[s];
+    __syncthreads();  // the previous task is done with sv
+    for (int j = threadIdx.x; j < n; j += 256) sv[j] = v[base + j];
+    __syncthreads();
+    const int i1 = min(i0 + rows_per_task, n);
+    const double* A = INV + off[s];
+    for (int i = i0 + warp; i < i1; i += 8) {
+      const double d = tri_row_dot_smem<LOWER>(A + (int64_t)i * n, sv, i, n, lane);
+      if (lane == 0) out[base + i] = LOWER ? __dadd_rn(sv[i], d) : d;
+    }
+  }
+}
+
+}  // namespace
+}  // namespace xdg
+
+extern "C" int xdg_lu_inv_apply_tasks(int64_t ntasks, const int* task_sys,
+                                      const int* task_row0, int rows_per_task,
+                                      int max_dim, int64_t total, const int64_t* off,
+                                      const int* dims, const int64_t* vec_off,
+                                      const double* INV, const int* src, const double* b,
+                                      double* x, double* scratch, xdg_stream_t stream) {
+  using namespace xdg;
+  XDG_REQUIRE(ntasks >= 0 && total >= 0 && rows_per_task > 0 && max_dim >= 0,
+              XDG_ERR_ARG, "bad batch");
+  if (ntasks == 0 || total == 0) return XDG_OK;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const size_t smem = sizeof(double) * (size_t)max_dim;
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    XDG_TRY_CUDA(cudaFuncSetAttribute(inv_rows_smem_kernel<true>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    XDG_TRY_CUDA(cudaFuncSetAttribute(inv_rows_smem_kernel<false>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  double* t = scratch;
+  double* y = scratch + total;
+  gather_kernel<<<grid_for(total, 256, 4), 256, 0, s>>>(total, src, b, t);
+  XDG_CHECK_LAUNCH();
+  const int g = resident_grid(inv_rows_smem_kernel<true>, 256, smem, ntasks * 256);
+  inv_rows_smem_kernel<true><<<g, 256, smem, s>>>(ntasks, task_sys, task_row0, rows_per_task,
+                                                  off, dims, vec_off, INV, t, y);
+  XDG_CHECK_LAUNCH();
+  inv_rows_smem_kernel<false><<<g, 256, smem, s>>>(ntasks, task_sys, task_row0,
+                                                   rows_per_task, off, dims, vec_off, INV, y,
+                                                   x);
+  XDG_CHECK_LAUNCH();
+  return XDG_OK;
+}

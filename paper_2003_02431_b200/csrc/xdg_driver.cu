@@ -173,6 +173,10 @@ static int pmg_apply_op(const xdg_pmg* P, const xdg_bsr* M, const double* b,
   double* xlo = (P->direct && !P->has_high) ? z : P->xlo;
   if (P->mf)
     XDG_TRY(xdg_mf_solve(P->mf, b, xlo, st));
+  else if (P->task_sys)
+    XDG_TRY(xdg_lu_inv_apply_tasks(P->ntasks, P->task_sys, P->task_row0, P->rows_per_task,
+                                   P->max_dim, P->total, P->lu_off, P->dims, P->vec_off,
+                                   P->LU, P->src, b, xlo, P->scratch, st));
   else
     XDG_TRY(xdg_lu_inv_apply(P->nsys, P->total, P->row_sys, P->lu_off, P->dims,
                              P->vec_off, P->LU, P->src, b, xlo, P->scratch, st));
@@ -331,8 +335,13 @@ int omg_level(OmgRun& R, int lam, const double* b, double* x, int has_x0,
       XDG_TRY(xdg_mf_solve(D.mf, b, x, st));
     } else {
       count(8.0 * D.n * (double)D.n + 32.0 * D.n);
-      XDG_TRY(xdg_lu_inv_apply(1, D.n, D.row_sys, D.zero_off, D.dims, D.zero_off,
-                               D.LU, D.perm, b, x, D.scratch, st));
+      if (D.task_sys)
+        XDG_TRY(xdg_lu_inv_apply_tasks(D.ntasks, D.task_sys, D.task_row0, D.rows_per_task,
+                                       D.max_dim, D.n, D.zero_off, D.dims, D.zero_off, D.LU,
+                                       D.perm, b, x, D.scratch, st));
+      else
+        XDG_TRY(xdg_lu_inv_apply(1, D.n, D.row_sys, D.zero_off, D.dims, D.zero_off,
+                                 D.LU, D.perm, b, x, D.scratch, st));
     }
     if (lam == R.entry) {
       XDG_TRY(spmv(&lv.M, x, rm.r, b, rm.sc + 6, rm.ws, R.s));

@@ -31,13 +31,18 @@ class XdgPmg(C.Structure):
                             "src", "xlo",
                             "wi_ptr", "wi_blk", "wi_lcol", "wi_cell", "wi_lrow",
                             "wi_xlo", "wi_hidx", "wi_out", "HLU", "hperm", "out",
-                            "cptr", "cpos", "damping")] + [("apply_bytes", C.c_double), ("mf", _vp)]
+                            "cptr", "cpos", "damping")] + [("apply_bytes", C.c_double), ("mf", _vp),
+                                          ("task_sys", _vp), ("task_row0", _vp),
+                                          ("ntasks", C.c_int64),
+                                          ("rows_per_task", C.c_int32),
+                                          ("max_dim", C.c_int32)]
 
 
 class XdgDirect(C.Structure):
     _fields_ = [("n", C.c_int32), ("pad0", C.c_int32), ("LU", _vp), ("perm", _vp),
                 ("zero_off", _vp), ("dims", _vp), ("row_sys", _vp), ("scratch", _vp),
-                ("mf", _vp)]
+                ("mf", _vp), ("task_sys", _vp), ("task_row0", _vp), ("ntasks", C.c_int64),
+                ("rows_per_task", C.c_int32), ("max_dim", C.c_int32)]
 
 
 class XdgRm(C.Structure):
@@ -83,6 +88,10 @@ def pmg_struct(plan):
         s.out, s.cptr, s.cpos = _p(plan.out), _p(plan.cptr), _p(plan.cpos)
         s.damping = _p(plan.damping)
     s.apply_bytes = float(plan.algorithmic_bytes())
+    if getattr(plan, "task_sys", None) is not None:
+        s.task_sys, s.task_row0 = _p(plan.task_sys), _p(plan.task_row0)
+        s.ntasks, s.rows_per_task, s.max_dim = (int(plan.task_sys.numel()),
+                                                plan.rows_per_task, plan.max_dim)
     keep = []
     if plan.mf is not None:
         ms = plan.mf.struct()

@@ -245,7 +245,12 @@ def run(name):
         print(f"[{name}] {solver} envelope {its}", flush=True)
     out["meta"] = np.frombuffer(json.dumps(meta).encode(), np.uint8)
     path = os.path.join(HERE, f"{name}.npz")
-    np.savez_compressed(path, **out)
+    tmp = path + ".tmp.npz"
+    np.savez_compressed(tmp, **out)
+    if os.path.getsize(tmp) > 8_000_000:  # large fixtures stay out of git
+        os.makedirs(os.path.join(HERE, "large"), exist_ok=True)
+        path = os.path.join(HERE, "large", f"{name}.npz")
+    os.replace(tmp, path)
     print(f"[{name}] wrote {path} ({os.path.getsize(path) / 1e6:.2f} MB)")
 
 
