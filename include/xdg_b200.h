@@ -40,6 +40,10 @@ enum {
 
 /* ---- library info ------------------------------------------------------ */
 int xdg_version(void);
+/* sizeof of the plain-pointer structs, in the order xdg_bsr, xdg_pmg,
+ * xdg_direct, xdg_rm, xdg_omg_level, xdg_mf, xdg_mf_node (binding checks);
+ * returns the number of entries. */
+int xdg_struct_sizes(int64_t* out, int n);
 const char* xdg_last_error(void);
 /* Bytes of reduction workspace the reduction entry points need. */
 int64_t xdg_reduce_workspace_bytes(void);

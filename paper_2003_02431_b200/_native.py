@@ -26,6 +26,7 @@ _i32, _i64, _f64, _vp = C.c_int, C.c_int64, C.c_double, C.c_void_p
 # name -> (restype, argtypes); must mirror include/xdg_b200.h
 SIGNATURES = {
     "xdg_version": (_i32, []),
+    "xdg_struct_sizes": (_i32, [_vp, _i32]),
     "xdg_last_error": (C.c_char_p, []),
     "xdg_reduce_workspace_bytes": (_i64, []),
     "xdg_blocks_transpose": (_i32, [_i64, _i32, _vp, _vp, _vp]),

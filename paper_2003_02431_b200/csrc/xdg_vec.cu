@@ -243,6 +243,16 @@ int gemv_t_parts(int64_t L) {
 using namespace xdg;
 
 extern "C" int xdg_version(void) { return 1; }
+
+extern "C" int xdg_struct_sizes(int64_t* out, int n) {
+  const int64_t sz[] = {(int64_t)sizeof(xdg_bsr),     (int64_t)sizeof(xdg_pmg),
+                        (int64_t)sizeof(xdg_direct),  (int64_t)sizeof(xdg_rm),
+                        (int64_t)sizeof(xdg_omg_level), (int64_t)sizeof(xdg_mf),
+                        (int64_t)sizeof(xdg_mf_node)};
+  const int k = (int)(sizeof(sz) / sizeof(sz[0]));
+  for (int i = 0; i < n && i < k; ++i) out[i] = sz[i];
+  return k;
+}
 extern "C" const char* xdg_last_error(void) { return g_err; }
 
 extern "C" int64_t xdg_reduce_workspace_bytes(void) {

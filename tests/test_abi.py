@@ -37,3 +37,22 @@ def test_binding_loads_without_gpu():
     lib = _native.load()
     assert lib.xdg_version() >= 1
     assert lib.xdg_reduce_workspace_bytes() > 0
+
+
+def test_ctypes_struct_layouts_match_the_header():
+    """The ctypes mirrors of the driver structs have the C sizes (a field
+    added on one side only would shift every pointer after it)."""
+    import ctypes as C
+
+    import numpy as np
+
+    from paper_2003_02431_b200 import _native as nat
+    from paper_2003_02431_b200.driver import XdgBsr, XdgDirect, XdgOmgLevel, XdgPmg, XdgRm
+    from paper_2003_02431_b200.multifrontal import NODE_DT, XdgMf
+
+    out = np.zeros(16, np.int64)
+    k = nat.load().xdg_struct_sizes(out.ctypes.data, 16)
+    assert k == 7
+    mine = [C.sizeof(XdgBsr), C.sizeof(XdgPmg), C.sizeof(XdgDirect), C.sizeof(XdgRm),
+            C.sizeof(XdgOmgLevel), C.sizeof(XdgMf), NODE_DT.itemsize]
+    assert list(out[:k]) == mine
