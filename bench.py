@@ -512,17 +512,36 @@ def run_ours(args):
     xh.copy_(x_ext[: nloc * N].cpu())
     yh = torch.empty(nloc * N, dtype=torch.float64, pin_memory=True)
     xd = x_ext  # device buffer the host copy lands in
+    if world == 1:
+        # public host-buffer matvec: transfers overlapped with the SpMV in
+        # z-slab chunks (device.HostStreamSpMV, xdg_bsr_spmv on row ranges)
+        from paper_2003_02431_b200.device import HostStreamSpMV
+
+        hs = HostStreamSpMV(D, chunks=16)
+        hs(xh, yh)
+        torch.cuda.synchronize(dev)
+        op(x_ext, y)
+        e2e_exact = bool(torch.equal(yh, y.cpu()))
+        step = (lambda: hs(xh, yh, sync=False))
+        e2e_path = ("pinned host x -> H2D (16 z-slab chunks) || xdg_bsr_spmv per chunk "
+                    "(C-ABI) || D2H y, full-duplex overlapped")
+    else:
+        def step():
+            xd[: nloc * N].copy_(xh, non_blocking=True)
+            op(xd, y)
+            yh.copy_(y, non_blocking=True)
+        e2e_exact, e2e_path = None, "pinned host x -> H2D -> halo SpMV (C-ABI) -> D2H y"
     for _ in range(2):
-        xd[: nloc * N].copy_(xh, non_blocking=True)
-        op(xd, y)
-        yh.copy_(y, non_blocking=True)
+        step()
+    if world == 1:
+        hs.wait()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
-        xd[: nloc * N].copy_(xh, non_blocking=True)
-        op(xd, y)
-        yh.copy_(y, non_blocking=True)
+        step()
+    if world == 1:
+        hs.wait()
     e1.record(stream)
     barrier()
     e2e_ms = e0.elapsed_time(e1)
@@ -556,7 +575,7 @@ def run_ours(args):
                                            "same command, dram__bytes_read+write per launch)"},
             "e2e": {"value": e2e_val, "unit": "GB/s",
                     "h2d_bytes_per_step": 8 * nloc * N, "d2h_bytes_per_step": 8 * nloc * N,
-                    "path": "pinned host x -> H2D -> xdg_bsr_spmv (C-ABI) -> D2H y"},
+                    "path": e2e_path, "bit_identical_to_device_spmv": e2e_exact},
             "gpu_launches": gpu_launches,
             "clocks": clk.summary(),
         }

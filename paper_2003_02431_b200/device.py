@@ -195,3 +195,84 @@ class DeviceBSR:
             self.ctx.stream), "blocks_transpose")
         return (self.row_ptr.cpu().numpy().astype(np.int64),
                 self.col.cpu().numpy().astype(np.int64), v.cpu().numpy())
+
+
+class HostStreamSpMV:
+    """y_host = M x_host for pinned host vectors, the PCIe transfers
+    overlapped with the SpMV: x is copied in `chunks` block-row ranges on one
+    stream, the SpMV of a row chunk starts as soon as the x chunks holding
+    its columns have landed (xdg_bsr_spmv on a row range), and each y chunk
+    is copied back on a third stream as soon as it is computed.  Device
+    buffers are double-buffered, so back-to-back products overlap too (the
+    host <-> device copies run full duplex).  The drop-in analogue of calling
+    BlockSparseMatrix.matvec (blockmatrix.py:119-125) on host arrays."""
+
+    def __init__(self, D: "DeviceBSR", chunks: int = 8):
+        if D.nbr != D.nbc:
+            raise DimensionMismatchError("streamed matvec needs a square operator")
+        self.D = D
+        dev = D.ctx.device
+        rp = D.row_ptr.cpu().numpy().astype(np.int64)
+        col = D.col.cpu().numpy().astype(np.int64)
+        nbr = D.nbr
+        chunks = max(1, min(int(chunks), nbr))
+        self.bounds = np.linspace(0, nbr, chunks + 1).round().astype(np.int64)
+        # last x chunk each row chunk reads (x chunks land in order)
+        rows = np.repeat(np.arange(nbr), np.diff(rp))
+        maxcol = np.full(nbr, -1, np.int64)
+        np.maximum.at(maxcol, rows, col)
+        self.need = []
+        for k in range(chunks):
+            m = int(maxcol[self.bounds[k]:self.bounds[k + 1]].max(initial=-1))
+            self.need.append(max(k, int(np.searchsorted(self.bounds, m, side="right")) - 1))
+        n = nbr * D.N
+        self.xd = [torch.empty(n, dtype=F64, device=dev) for _ in range(2)]
+        self.yd = [torch.empty(n, dtype=F64, device=dev) for _ in range(2)]
+        self.s = [torch.cuda.Stream(dev) for _ in range(3)]  # h2d, compute, d2h
+        E = torch.cuda.Event
+        self.ev_h = [E() for _ in range(chunks)]
+        self.ev_c = [E() for _ in range(chunks)]
+        self.ev_d = [[E() for _ in range(chunks)] for _ in range(2)]
+        self.ev_x = [E() for _ in range(2)]
+        self.step = 0
+
+    def launches_per_product(self) -> int:
+        return len(self.bounds) - 1
+
+    def __call__(self, xh: torch.Tensor, yh: torch.Tensor, sync: bool = True) -> torch.Tensor:
+        """Enqueue one product; with sync=False the current stream does not
+        wait for the copies back (call wait() before reading yh) so
+        consecutive products overlap."""
+        D, N = self.D, self.D.N
+        s_h, s_c, s_d = self.s
+        buf = self.step & 1
+        self.step += 1
+        xd, yd = self.xd[buf], self.yd[buf]
+        cur = torch.cuda.current_stream(D.ctx.device)
+        s_h.wait_stream(cur)
+        s_h.wait_event(self.ev_x[buf])  # this x buffer's previous SpMVs are done
+        for k in range(len(self.bounds) - 1):
+            a, b = int(self.bounds[k]) * N, int(self.bounds[k + 1]) * N
+            with torch.cuda.stream(s_h):
+                xd[a:b].copy_(xh[a:b], non_blocking=True)
+                self.ev_h[k].record(s_h)
+        for k in range(len(self.bounds) - 1):
+            s_c.wait_event(self.ev_h[self.need[k]])
+            s_c.wait_event(self.ev_d[buf][k])  # y chunk of the previous use copied out
+            with torch.cuda.stream(s_c):
+                D.spmv(xd, yd, rows=(int(self.bounds[k]), int(self.bounds[k + 1])))
+                self.ev_c[k].record(s_c)
+        self.ev_x[buf].record(s_c)
+        for k in range(len(self.bounds) - 1):
+            a, b = int(self.bounds[k]) * N, int(self.bounds[k + 1]) * N
+            s_d.wait_event(self.ev_c[k])
+            with torch.cuda.stream(s_d):
+                yh[a:b].copy_(yd[a:b], non_blocking=True)
+                self.ev_d[buf][k].record(s_d)
+        if sync:
+            self.wait()
+        return yh
+
+    def wait(self) -> None:
+        """Make the current stream wait for every enqueued copy back."""
+        torch.cuda.current_stream(self.D.ctx.device).wait_stream(self.s[2])

@@ -110,6 +110,27 @@ def test_spmv_cfg3_32_bitexact_vs_oracle():
     assert np.array_equal(y, ospmv.bsr_spmv(rp, col, val, x, 4))
 
 
+@pytest.mark.parametrize("chunks", [1, 5, 16])
+def test_host_stream_spmv_bitexact(chunks):
+    """HostStreamSpMV (host x -> chunked H2D || row-range SpMVs || D2H y,
+    double-buffered): bit-identical to the oracle for back-to-back
+    products with different inputs, whatever the chunking."""
+    from paper_2003_02431_b200.device import HostStreamSpMV
+
+    rp, col, val, x = cfg3.build(24)
+    D = dev_bsr(rp, col, val)
+    hs = HostStreamSpMV(D, chunks=chunks)
+    xs = [np.random.default_rng(k).standard_normal(len(x)) for k in range(3)]
+    xh = [torch.from_numpy(v).pin_memory() for v in xs]
+    yh = [torch.empty(len(x), dtype=torch.float64).pin_memory() for _ in xs]
+    for a, b in zip(xh, yh):
+        hs(a, b, sync=False)
+    hs.wait()
+    torch.cuda.synchronize()
+    for v, b in zip(xs, yh):
+        assert np.array_equal(b.numpy(), ospmv.bsr_spmv(rp, col, val, v, 4))
+
+
 @pytest.mark.slow
 def test_spmv_cfg3_full_size_properties():
     """128^3 (BASELINE cfg3): rows sampled from the device matrix are
