@@ -263,6 +263,8 @@ typedef struct xdg_mf {
 
 /* Columns per segment of a split long row (the planner's task layout). */
 int xdg_mf_segment_columns(void);
+/* Rows per warp task of a front whose rows take a whole warp. */
+int xdg_mf_rows_per_warp(void);
 /* x[pdst] = A^-1 b[src] for every system of the forest at once:
  * 3 launches per forward level, 2 per backward level. */
 int xdg_mf_solve(const xdg_mf* mf, const double* b, double* x,

@@ -72,6 +72,50 @@ __device__ __forceinline__ double group_dot(const double* __restrict__ row, V v,
   return s;
 }
 
+// MR rows of one front against the same vector (whole warp, lanes stride
+// 32): the vector is loaded once for all of them, so MU vector + MR*MU
+// factor loads are in flight per lane.  Row q covers [r0[q], r1[q]) inside
+// [lo, hi); loads are clamped to hi - 1 (inside the padded rows) and masked.
+// Used for fronts whose rows get a whole warp (G = 32).
+#ifndef MF_MR
+#define MF_MR 2
+#endif
+#ifndef MF_MU
+#define MF_MU 8
+#endif
+constexpr int kMR = MF_MR;
+constexpr int kMU = MF_MU;
+
+template <typename V>
+__device__ __forceinline__ void multi_dot(const double* const* rows, V v, int lo, int hi,
+                                          const int* r0, const int* r1, int lane,
+                                          double* d) {
+  double acc[kMR][2];
+#pragma unroll
+  for (int q = 0; q < kMR; ++q) acc[q][0] = acc[q][1] = 0.0;
+  for (int jb = lo; jb < hi; jb += 32 * kMU) {
+    double m[kMR][kMU], x[kMU];
+#pragma unroll
+    for (int u = 0; u < kMU; ++u) {
+      const int j = min(jb + lane + 32 * u, hi - 1);
+#pragma unroll
+      for (int q = 0; q < kMR; ++q) m[q][u] = __ldg(rows[q] + j);
+      x[u] = v(j);
+    }
+#pragma unroll
+    for (int u = 0; u < kMU; ++u) {
+      const int j = jb + lane + 32 * u;
+#pragma unroll
+      for (int q = 0; q < kMR; ++q) {
+        const double xq = (j >= r0[q] && j < r1[q]) ? x[u] : 0.0;
+        acc[q][u & 1] = fma(m[q][u], xq, acc[q][u & 1]);
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < kMR; ++q) d[q] = warp_sum(acc[q][0] + acc[q][1]);
+}
+
 struct Direct {
   const double* p;
   __device__ __forceinline__ double operator()(int j) const { return p[j]; }
@@ -184,7 +228,41 @@ mf_rows_kernel(int64_t t0, int64_t ntasks, const int4* __restrict__ tasks, Ctx c
        w += nw) {
     const int4 tk = tasks[t0 + interleave(w, ntasks)];
     const xdg_mf_node nd = c.nodes[tk.x];
-    if (tk.w < 0) {
+    if (tk.w < 0 && tk.z == kMR) {  // kMR rows r, r + 1, ... of a G = 32 front
+      const int r = tk.y;
+      const int nrows = (PH == kBound) ? nd.b : nd.p;
+      const double* rows[kMR];
+      int r0[kMR], r1[kMR];
+      int lo = 1 << 30, hi = 0;
+      const int64_t mat = (PH == kBound) ? nd.lbp : (PH == kUpb ? nd.upb : nd.inv);
+      const int ld = (PH == kUpb) ? nd.ldb : nd.ldp;
+#pragma unroll
+      for (int q = 0; q < kMR; ++q) {
+        const int rq = min(r + q, nrows - 1);
+        rows[q] = c.F + mat + (int64_t)rq * ld;
+        row_span<PH>(nd, rq, r0[q], r1[q]);
+        if (r + q >= nrows) r1[q] = r0[q];  // past the front: empty row
+        if (r1[q] > r0[q]) {
+          lo = min(lo, r0[q]);
+          hi = max(hi, r1[q]);
+        }
+      }
+      double d[kMR];
+#pragma unroll
+      for (int q = 0; q < kMR; ++q) d[q] = 0.0;
+      if (hi > lo) {
+        if (PH == kUpb)
+          multi_dot(rows, Gathered{c.Y, c.bidx + nd.bx}, lo, hi, r0, r1, lane, d);
+        else
+          multi_dot(rows, Direct{(PH == kBound) ? c.Y + nd.y : c.W + nd.w}, lo, hi, r0, r1,
+                    lane, d);
+      }
+      if (lane == 0) {
+#pragma unroll
+        for (int q = 0; q < kMR; ++q)
+          if (r + q < nrows) row_done<PH>(c, nd, r + q, d[q]);
+      }
+    } else if (tk.w < 0) {
       const int G = (PH == kUpb) ? nd.gb : nd.gp;
       const int gl = lane & (G - 1);
       const int r = tk.y + lane / G;
@@ -235,6 +313,7 @@ int launch_rows(const xdg_mf* mf, int h, double* x, cudaStream_t s) {
 }  // namespace xdg
 
 extern "C" int xdg_mf_segment_columns(void) { return xdg::kSeg; }
+extern "C" int xdg_mf_rows_per_warp(void) { return xdg::kMR; }
 
 extern "C" int xdg_mf_solve(const xdg_mf* mf, const double* b, double* x,
                             xdg_stream_t stream) {

@@ -54,6 +54,11 @@ assert NODE_DT.itemsize == 96
 MF_U = 8  # loads in flight per lane per chunk (MF_U, xdg_multifrontal.cu)
 
 
+def _rows_per_warp() -> int:
+    """Rows a warp task of a whole-warp front covers: the kernel's kMR."""
+    return int(nat.load().xdg_mf_rows_per_warp())
+
+
 def _segment_columns() -> int:
     """Columns per segment of a split long row: the kernel's kSeg."""
     return int(nat.load().xdg_mf_segment_columns())
@@ -529,6 +534,14 @@ class Multifrontal:
                 grp = np.stack([np.repeat(sh, cnt), first, np.zeros_like(first),
                                 np.full_like(first, -1)], 1)
                 lg = ts[g[ts] == 32]
+                if SEG >= 1 << 20:  # rows unsplit: MR rows per warp task
+                    MR = _rows_per_warp()
+                    cnt2 = (nrows[lg] + MR - 1) // MR
+                    r2 = _ranges(np.zeros(len(lg), np.int64), cnt2) * MR
+                    out += [grp, np.stack([np.repeat(lg, cnt2), r2, np.full_like(r2, MR),
+                                           np.full_like(r2, -1)], 1)]
+                    lev.append(len(grp) + len(r2))
+                    continue
                 rn = np.repeat(lg, nrows[lg])
                 rr = _ranges(np.zeros(len(lg), np.int64), nrows[lg])
                 if phase == 0:

@@ -20,6 +20,9 @@ def emulate_solve(mf, b, xlen):
         out = []
         for t, r0, seg, slot in tasks[lev[h]:lev[h + 1]]:
             nd = nodes[t]
+            if slot < 0 and seg > 0:  # seg rows of a whole-warp front
+                out += [(t, r) for r in range(r0, r0 + seg) if r < nd[count]]
+                continue
             if slot >= 0:
                 if seg == 0:
                     out.append((t, r0))

@@ -99,5 +99,9 @@ def test_solves_with_sparse_factors(solver, monkeypatch):
     else:
         x, rep = gmres_pmg_solve(lv.matrix, lv.rhs, cfg, dim=meta["dim"])
     assert rep.converged
-    assert env.min() - 1 <= rep.iterations <= env.max() + 1, (rep.iterations, env)
+    # chaotic envelopes (width > 2) get the suite's 10 % slack
+    # (test_setup_gpu._slack)
+    lo, hi = int(env.min()), int(env.max())
+    s = 1 if hi - lo <= 2 else max(1, int(round(0.10 * np.median(env))))
+    assert lo - s <= rep.iterations <= hi + s, (rep.iterations, env)
     assert rel(x, z[f"{solver}_x"]) <= 1e-8
