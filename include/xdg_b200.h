@@ -246,7 +246,7 @@ typedef struct xdg_mf {
   const int64_t* ent_src;      /* -> index into b, or -1                    */
   const int64_t* ent_cptr;     /* CSR of child contributions (into C)       */
   const int64_t* ent_cidx;
-  const int32_t* tasks;        /* int4 (node, row, seg, slot) warp tasks    */
+  const int32_t* tasks;        /* int4 (node, first row, rows, -1) warp tasks */
   const xdg_mf_node* nodes;
   const int64_t* bidx;         /* Y index of each boundary unknown          */
   const int64_t* pdst;         /* x index of each pivot unknown             */
@@ -256,13 +256,9 @@ typedef struct xdg_mf {
   double* W;
   double* Y;
   double* C;
-  double* part;                /* partial sums of split long rows           */
-  int32_t* cnt;                /* their tickets (zero between launches)     */
   double apply_bytes;          /* algorithmic bytes of one solve            */
 } xdg_mf;
 
-/* Columns per segment of a split long row (the planner's task layout). */
-int xdg_mf_segment_columns(void);
 /* Rows per warp task of a front whose rows take a whole warp. */
 int xdg_mf_rows_per_warp(void);
 /* x[pdst] = A^-1 b[src] for every system of the forest at once:

@@ -72,7 +72,6 @@ SIGNATURES = {
                         + [_vp] * 14),
     "xdg_mgs": (_i32, [_i64, _i32, _vp, _i64, _vp, _vp, _vp, _vp]),
     "xdg_mf_solve": (_i32, [_vp, _vp, _vp, _vp]),
-    "xdg_mf_segment_columns": (_i32, []),
     "xdg_mf_rows_per_warp": (_i32, []),
 }
 

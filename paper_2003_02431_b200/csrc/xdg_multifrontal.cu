@@ -151,12 +151,6 @@ mf_gather_kernel(int64_t e0, int64_t e1, const int64_t* __restrict__ ent_w,
 }
 
 enum Phase { kLower = 0, kBound = 1, kUpb = 2, kUpper = 3 };
-// Columns per segment of a split long row.  Measured on B200 (cfg2 low-order
-// system, 12.2 GB of factors): splitting at 1024 / 4096 columns costs more in
-// ticket fences (3.8 / 3.33 ms) than it saves in launch tails (3.2 ms
-// unsplit), so rows are not split at these sizes; multifrontal.SEG mirrors
-// this value (xdg_mf_segment_columns).
-constexpr int kSeg = 1 << 20;
 
 // The four row phases (p = pivot unknowns, b = boundary unknowns of a front):
 //   kLower  Y[i]  = W[i] + L^-1[i, :i] . W[:i]              rows: P, G = gp
@@ -175,8 +169,6 @@ struct Ctx {
   double* Y;
   double* C;
   double* x;
-  double* part;
-  int* cnt;
 };
 
 template <int PH>
@@ -213,12 +205,9 @@ __device__ __forceinline__ void row_done(const Ctx& c, const xdg_mf_node& nd, in
   }
 }
 
-// Warp tasks (node, row, seg, slot).  slot < 0: 32/G rows from `row`, G
-// lanes each.  slot >= 0: segment `seg` of a long row (whole warp, kSeg
-// columns); the partial goes to part[slot + seg] and the last segment to
-// finish (ticket in cnt[slot]) sums the partials in segment order --
-// deterministic -- and finishes the row.  Equal-sized segments keep every
-// launch free of long-row tails.
+// Warp tasks (node, row, nrows, -1): fronts whose rows take a whole warp
+// (G = 32) get kMR rows per task (multi_dot, shared vector loads); shorter
+// rows get 32/G rows per task, G lanes each (nrows field 0).
 template <int PH>
 __global__ void __launch_bounds__(kT, MF_MINB)
 mf_rows_kernel(int64_t t0, int64_t ntasks, const int4* __restrict__ tasks, Ctx c) {
@@ -228,7 +217,7 @@ mf_rows_kernel(int64_t t0, int64_t ntasks, const int4* __restrict__ tasks, Ctx c
        w += nw) {
     const int4 tk = tasks[t0 + interleave(w, ntasks)];
     const xdg_mf_node nd = c.nodes[tk.x];
-    if (tk.w < 0 && tk.z == kMR) {  // kMR rows r, r + 1, ... of a G = 32 front
+    if (tk.z == kMR) {  // kMR rows r, r + 1, ... of a G = 32 front
       const int r = tk.y;
       const int nrows = (PH == kBound) ? nd.b : nd.p;
       const double* rows[kMR];
@@ -262,7 +251,7 @@ mf_rows_kernel(int64_t t0, int64_t ntasks, const int4* __restrict__ tasks, Ctx c
         for (int q = 0; q < kMR; ++q)
           if (r + q < nrows) row_done<PH>(c, nd, r + q, d[q]);
       }
-    } else if (tk.w < 0) {
+    } else {
       const int G = (PH == kUpb) ? nd.gb : nd.gp;
       const int gl = lane & (G - 1);
       const int r = tk.y + lane / G;
@@ -272,26 +261,6 @@ mf_rows_kernel(int64_t t0, int64_t ntasks, const int4* __restrict__ tasks, Ctx c
       if (act) row_span<PH>(nd, r, j0, j1);
       const double d = row_part<PH>(c, nd, r, j0, j1, gl, G, act && j1 > j0);
       if (act && gl == 0) row_done<PH>(c, nd, r, d);
-    } else {
-      const int r = tk.y;
-      int j0, j1;
-      row_span<PH>(nd, r, j0, j1);
-      const int js = j0 + tk.z * kSeg;
-      const int je = min(js + kSeg, j1);
-      const double d = row_part<PH>(c, nd, r, js, je, lane, 32, true);
-      if (lane == 0) {
-        c.part[tk.w + tk.z] = d;
-        __threadfence();
-        const int nseg = (j1 - j0 + kSeg - 1) / kSeg;
-        if (atomicAdd(c.cnt + tk.w, 1) == nseg - 1) {
-          __threadfence();
-          const volatile double* pv = c.part + tk.w;
-          double sum = 0.0;
-          for (int q = 0; q < nseg; ++q) sum = __dadd_rn(sum, pv[q]);
-          c.cnt[tk.w] = 0;
-          row_done<PH>(c, nd, r, sum);
-        }
-      }
     }
   }
 }
@@ -301,8 +270,7 @@ int launch_rows(const xdg_mf* mf, int h, double* x, cudaStream_t s) {
   const int64_t* lev = mf->lev_task + (int64_t)PH * (mf->nlevels + 1);
   const int64_t t0 = lev[h], nt = lev[h + 1] - t0;
   if (nt <= 0) return XDG_OK;
-  Ctx c{mf->nodes, mf->F, mf->bidx, mf->pdst, mf->pscale, mf->W, mf->Y, mf->C, x,
-        mf->part, mf->cnt};
+  Ctx c{mf->nodes, mf->F, mf->bidx, mf->pdst, mf->pscale, mf->W, mf->Y, mf->C, x};
   const int g = resident_grid(mf_rows_kernel<PH>, kT, 0, nt * 32);
   mf_rows_kernel<PH><<<g, kT, 0, s>>>(t0, nt, reinterpret_cast<const int4*>(mf->tasks), c);
   XDG_CHECK_LAUNCH();
@@ -312,7 +280,6 @@ int launch_rows(const xdg_mf* mf, int h, double* x, cudaStream_t s) {
 }  // namespace
 }  // namespace xdg
 
-extern "C" int xdg_mf_segment_columns(void) { return xdg::kSeg; }
 extern "C" int xdg_mf_rows_per_warp(void) { return xdg::kMR; }
 
 extern "C" int xdg_mf_solve(const xdg_mf* mf, const double* b, double* x,

@@ -59,10 +59,6 @@ def _rows_per_warp() -> int:
     return int(nat.load().xdg_mf_rows_per_warp())
 
 
-def _segment_columns() -> int:
-    """Columns per segment of a split long row: the kernel's kSeg."""
-    return int(nat.load().xdg_mf_segment_columns())
-
 _vp = C.c_void_p
 
 
@@ -70,7 +66,8 @@ class XdgMf(C.Structure):
     _fields_ = [("nlevels", C.c_int32), ("nnodes", C.c_int32), ("total", C.c_int64)] + \
         [(f, _vp) for f in ("lev_ent", "lev_task", "ent_w", "ent_src", "ent_cptr",
                             "ent_cidx", "tasks", "nodes", "bidx",
-                            "pdst", "ent_scale", "pscale", "F", "W", "Y", "C", "part", "cnt")] + [("apply_bytes", C.c_double)]
+                            "pdst", "ent_scale", "pscale", "F", "W", "Y", "C")] + \
+        [("apply_bytes", C.c_double)]
 
 
 def _ranges(starts: np.ndarray, ends: np.ndarray) -> np.ndarray:
@@ -518,13 +515,12 @@ class Multifrontal:
         gb = np.array([_group(int(x)) if x else g for x, g in zip(bn, gp)], np.int64)
 
         def tasks(phase):
-            """int4 warp tasks (node, row, seg, slot) of one phase, level by
-            level: fronts with short rows (G < 32) get 32/G rows per task;
-            rows of G = 32 fronts longer than SEG are split into SEG-column
-            segments (slot = first partial of the row, per level)."""
+            """int4 warp tasks (node, first row, rows, -1) of one phase, level
+            by level: fronts whose rows take a whole warp (G = 32) get MR rows
+            per task; shorter rows 32/G rows per task (rows field 0)."""
             g = gb if phase == 2 else gp
             nrows = bn if phase == 1 else pn
-            out, lev, maxslot = [], [], 0
+            out, lev = [], []
             for h in range(H):
                 ts = order[height[order] == h]
                 sh = ts[g[ts] < 32]
@@ -534,43 +530,22 @@ class Multifrontal:
                 grp = np.stack([np.repeat(sh, cnt), first, np.zeros_like(first),
                                 np.full_like(first, -1)], 1)
                 lg = ts[g[ts] == 32]
-                if SEG >= 1 << 20:  # rows unsplit: MR rows per warp task
-                    MR = _rows_per_warp()
-                    cnt2 = (nrows[lg] + MR - 1) // MR
-                    r2 = _ranges(np.zeros(len(lg), np.int64), cnt2) * MR
-                    out += [grp, np.stack([np.repeat(lg, cnt2), r2, np.full_like(r2, MR),
-                                           np.full_like(r2, -1)], 1)]
-                    lev.append(len(grp) + len(r2))
-                    continue
-                rn = np.repeat(lg, nrows[lg])
-                rr = _ranges(np.zeros(len(lg), np.int64), nrows[lg])
-                if phase == 0:
-                    ln = rr
-                elif phase == 3:
-                    ln = pn[rn] - rr
-                else:
-                    ln = np.repeat((pn if phase == 1 else bn)[lg], nrows[lg])
-                nseg = np.maximum(1, (ln + SEG - 1) // SEG)
-                multi = nseg > 1
-                slot = np.full(len(rn), -1, np.int64)
-                slot[multi] = np.cumsum(nseg[multi]) - nseg[multi]
-                maxslot = max(maxslot, int(nseg[multi].sum()))
-                seg = _ranges(np.zeros(len(rn), np.int64), nseg)
-                long_ = np.stack([np.repeat(rn, nseg), np.repeat(rr, nseg), seg,
-                                  np.repeat(slot, nseg)], 1)
+                cnt2 = (nrows[lg] + MR - 1) // MR
+                r2 = _ranges(np.zeros(len(lg), np.int64), cnt2) * MR
+                long_ = np.stack([np.repeat(lg, cnt2), r2, np.full_like(r2, MR),
+                                  np.full_like(r2, -1)], 1)
                 out += [grp, long_]
                 lev.append(len(grp) + len(long_))
-            return out, lev, maxslot
+            return out, lev
 
-        SEG = _segment_columns()
-        all_tasks, lev_task, nslot = [], [], 1
+        MR = _rows_per_warp()
+        all_tasks, lev_task = [], []
         base = 0
         for phase in range(4):
-            tl, lv, ms = tasks(phase)
+            tl, lv = tasks(phase)
             all_tasks += tl
             lev_task.append(base + np.concatenate([[0], np.cumsum(lv)]))
             base += int(np.sum(lv))
-            nslot = max(nslot, ms)
         task_arr = (np.concatenate(all_tasks) if all_tasks
                     else np.zeros((0, 4), np.int64))
         bidx = np.zeros(int(bn.sum()), np.int64)
@@ -599,8 +574,6 @@ class Multifrontal:
         self.ent_w, self.ent_src = up(ent_w, I64), up(ent_src, I64)
         self.ent_cptr, self.ent_cidx = up(ent_cptr, I64), up(c_src, I64)
         self.tasks = up(task_arr, I32)
-        self.part = torch.zeros(nslot, dtype=F64, device=dev)
-        self.cnt = torch.zeros(nslot, dtype=I32, device=dev)
         self.nodes_host = nodes
         self.nodes = torch.from_numpy(nodes.view(np.uint8).copy()).to(dev)
         self.bidx, self.pdst = up(bidx, I64), up(pdst, I64)
@@ -623,8 +596,7 @@ class Multifrontal:
             s.lev_ent = self.lev_ent.ctypes.data
             s.lev_task = self.lev_task.ctypes.data
             for f in ("ent_w", "ent_src", "ent_cptr", "ent_cidx", "tasks", "nodes",
-                      "ent_scale", "pscale", "bidx", "pdst", "F", "W", "Y", "C", "part",
-                      "cnt"):
+                      "ent_scale", "pscale", "bidx", "pdst", "F", "W", "Y", "C"):
                 setattr(s, f, getattr(self, f).data_ptr())
             s.apply_bytes = float(self.apply_bytes)
             self._s = s

@@ -18,17 +18,10 @@ def emulate_solve(mf, b, xlen):
         lev = mf.lev_task[phase * (H + 1):(phase + 1) * (H + 1)]
         g, count = ("gb" if phase == 2 else "gp"), ("b" if phase == 1 else "p")
         out = []
-        for t, r0, seg, slot in tasks[lev[h]:lev[h + 1]]:
+        for t, r0, nr, _ in tasks[lev[h]:lev[h + 1]]:
             nd = nodes[t]
-            if slot < 0 and seg > 0:  # seg rows of a whole-warp front
-                out += [(t, r) for r in range(r0, r0 + seg) if r < nd[count]]
-                continue
-            if slot >= 0:
-                if seg == 0:
-                    out.append((t, r0))
-                continue
-            for r in range(r0, min(r0 + 32 // nd[g], nd[count])):
-                out.append((t, r))
+            n = nr if nr > 0 else 32 // nd[g]  # MR rows, or 32/G rows of G lanes
+            out += [(t, r) for r in range(r0, min(r0 + n, nd[count]))]
         return out
 
     W, Y, Cb = np.zeros(mf.W.numel()), np.zeros(mf.Y.numel()), np.zeros(mf.C.numel())
