@@ -51,9 +51,9 @@ DENSE_LOW_MAX_SYSTEM = 16000  # unknowns
 # there are enough tasks to fill the GPU (4 CTAs per SM) and each system fits
 # 48 KB.  Measured at cfg2 level 1 (337 systems of ~1,810 unknowns): 5.0 TB/s
 # vs 4.2 TB/s for the per-row kernel.
-TASK_MIN_TASKS = 4 * 148
+TASK_MIN_TASKS = 8 * 148
 TASK_MAX_DIM = 6144
-ROWS_PER_TASK = 64
+ROWS_PER_TASK = 32  # measured: 32 / 64 / 128 / 256 rows -> cfg2 OMG 17.29 / 17.47 / 17.79 / 18.81 s
 
 
 def use_multifrontal(dims) -> bool:
