@@ -545,6 +545,25 @@ def run_ours(args):
     e1.record(stream)
     barrier()
     e2e_ms = e0.elapsed_time(e1)
+    # the e2e roofline: the same bytes as raw concurrent pinned H2D + D2H
+    # copies (PCIe full duplex), no compute
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    yd_raw = torch.empty_like(y)
+    for rep in range(2):
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        s1.wait_stream(stream)
+        s2.wait_stream(stream)
+        for _ in range(args.steps):
+            with torch.cuda.stream(s1):
+                yd_raw.copy_(xh, non_blocking=True)
+            with torch.cuda.stream(s2):
+                yh.copy_(y, non_blocking=True)
+        stream.wait_stream(s1)
+        stream.wait_stream(s2)
+        f1.record(stream)
+        f1.synchronize()
+    pcie_ms = f0.elapsed_time(f1)
     t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -575,7 +594,12 @@ def run_ours(args):
                                            "same command, dram__bytes_read+write per launch)"},
             "e2e": {"value": e2e_val, "unit": "GB/s",
                     "h2d_bytes_per_step": 8 * nloc * N, "d2h_bytes_per_step": 8 * nloc * N,
-                    "path": e2e_path, "bit_identical_to_device_spmv": e2e_exact},
+                    "path": e2e_path, "bit_identical_to_device_spmv": e2e_exact,
+                    "pcie_duplex_floor": {
+                        "value": B_global * args.steps / (pcie_ms * 1e-3) / 1e9,
+                        "unit": "GB/s", "what": "the step's H2D + D2H bytes as raw "
+                                                "concurrent pinned copies, no compute"},
+                    "frac_of_pcie_floor": pcie_ms / e2e_ms},
             "gpu_launches": gpu_launches,
             "clocks": clk.summary(),
         }
