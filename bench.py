@@ -328,6 +328,8 @@ def time_solves(torch, budget_s: float):
                 "loop_GBs": loop["bytes"] / max(loop["seconds"], 1e-12) / 1e9,
                 "loop_frac_of_hbm_peak": loop["bytes"] / max(loop["seconds"], 1e-12)
                 / 1e9 / peak,
+                "loop_frac_of_nominal_8TBs": loop["bytes"] / max(loop["seconds"], 1e-12)
+                / 1e9 / NOMINAL_HBM_GBS,
                 "rel_err_vs_reference": rel,
                 "reference_cpu_s_build_container": ref_s,
                 "cpu_oracle_s_this_host": cpu_here,
