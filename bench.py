@@ -216,6 +216,28 @@ CFG2_META = {  # BASELINE config 2: 32^3, p=3, sphere r=0.6, mu 1/
     "gmres": {"tolerance": 1e-10, "max_iterations": 10000, "k_lo": 2, "gmres_restart": 50}}
 
 
+def reference_cfg2_estimate(solver: str, iterations: int):
+    """The reference's cfg2 solve time extrapolated from a bounded run of
+    the reference itself in the build container
+    (tests/golden/time_reference_cfg2.py: 1 and 3 iterations, the first
+    including the lazy factorizations inside its solve timer): first +
+    (iterations - 1) x per-iteration.  A lower bound for OMG (its RM space
+    grows to 800 columns later in the solve)."""
+    path = os.path.join(ROOT, "tests", "golden", "reference_cfg2_timing.json")
+    if not os.path.exists(path):
+        return None
+    t = json.load(open(path))
+    k = "omg" if solver == "omg" else "gmres"
+    if f"{k}_1it_s" not in t or f"{k}_3it_s" not in t:
+        return None
+    first, per = t[f"{k}_1it_s"], (t[f"{k}_3it_s"] - t[f"{k}_1it_s"]) / 2
+    est = first + max(iterations - 1, 0) * per
+    return {"seconds": est, "first_iteration_s": first, "per_iteration_s": per,
+            "iterations": iterations, "cores": t.get("cores"),
+            "where": "build container (reference cutdg, scipy/numpy)",
+            "source": "tests/golden/reference_cfg2_timing.json"}
+
+
 def native_cfg2(world: int = 1):
     """BASELINE config 2 built by this package's own setup pipeline
     (case.assemble_case: geometry, agglomeration, SIP assembly, hierarchy);
@@ -306,6 +328,9 @@ def time_solves(torch, budget_s: float):
             else:  # large fixtures: no reference solve (hours on the CPU)
                 rel = None
             ref_s = meta.get(f"{solver}_seconds")
+            ref_extrap = None
+            if case.endswith("cfg2") or case.startswith("cfg2"):
+                ref_extrap = reference_cfg2_estimate(solver, rep.iterations)
             cpu_here = None
             if case == "cfg1":  # bounded: ~10 s of CPU per solver
                 from oracle import solvers_np
@@ -338,6 +363,7 @@ def time_solves(torch, budget_s: float):
                 "cpu_oracle_cores": os.cpu_count(),
                 "reference_cpu_dof_per_s_build_container":
                     (meta["dofs_raw"] / ref_s) if ref_s else None,
+                "reference_cpu_extrapolated": ref_extrap,
             })
     return out
 

@@ -51,7 +51,7 @@ def main():
            "raw_dofs": int(len(A.rhs)), "L1_dofs": H.level(1).num_dofs,
            "level_blocks": [H.level(l).data.num_blocks for l in range(1, H.num_levels + 1)],
            "cut_cells": len(A.cutmesh.interface_rules), "cache_hits": H.meta["carrier_cache_hits"]}
-    if a.solve:
+    for solver in [v for v in a.solve.split(",") if v]:
         lv = H.level(1)
         cfg = SolverConfig(tolerance=a.tol, max_iterations=a.max_it,
                            k_lo=(case.resolved_k_lo if a.k_lo is None else a.k_lo,),
@@ -60,14 +60,21 @@ def main():
         from paper_2003_02431_b200 import solvers as S
 
         t0 = time.perf_counter()
-        if a.solve == "omg":
-            x, rep = ortho_mg_solve(H, lv.rhs, None, cfg, 1)
+        if solver == "omg":
+            octx = S._OmgContext(cfg, 1)
+            x, rep = ortho_mg_solve(H, lv.rhs, None, cfg, 1, octx)
+            loop = dict(octx.last_loop)
         else:
             x, rep = gmres_pmg_solve(lv.matrix, lv.rhs, cfg, dim=a.dim)
-        out.update(solve=a.solve, solve_s=round(time.perf_counter() - t0, 3),
-                   iterations=rep.iterations, converged=rep.converged,
-                   final_residual=rep.final_residual,
-                   loop=(dict(S.LAST_LOOP) if a.solve != "omg" else None))
+            loop = dict(S.LAST_LOOP)
+        dt = time.perf_counter() - t0
+        out[solver] = dict(solve_s=round(dt, 3), iterations=rep.iterations,
+                           converged=rep.converged, final_residual=rep.final_residual,
+                           dof_per_s=out["raw_dofs"] / rep.time_iterations,
+                           loop_s=loop.get("seconds"),
+                           loop_GBs=loop.get("bytes", 0) / max(loop.get("seconds", 1), 1e-12)
+                           / 1e9)
+        print(json.dumps(out), flush=True)
     print(json.dumps(out), flush=True)
 
 
