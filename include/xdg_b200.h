@@ -261,6 +261,31 @@ typedef struct xdg_mf {
 
 /* Rows per warp task of a front whose rows take a whole warp. */
 int xdg_mf_rows_per_warp(void);
+/* Host-side symbolic analysis (csrc/xdg_ordering.cu).  Nested dissection
+ * of the graph (ptr, col) with nv vertices into a post-ordered forest:
+ * node_ptr[nnodes+1], node_verts[nv], parent[nnodes] (capacities nv+1, nv,
+ * nv); returns nnodes. */
+int64_t xdg_nd_order(int64_t nv, const int64_t* ptr, const int64_t* col,
+                     int64_t leaf, int64_t* node_ptr, int64_t* node_verts,
+                     int64_t* parent);
+/* Boundary sets of the fronts (ancestor vertices adjacent to the subtree,
+ * sorted by (owner, vertex)); returns their total size, copied out by
+ * xdg_nd_boundaries_copy(b_ptr[nnodes+1], b_verts[total]). */
+int64_t xdg_nd_boundaries(int64_t nv, const int64_t* ptr, const int64_t* col,
+                          int64_t nnodes, const int64_t* node_ptr,
+                          const int64_t* node_verts, const int64_t* parent);
+int xdg_nd_boundaries_copy(int64_t* b_ptr, int64_t* b_verts);
+/* Overlapping Schwarz partition (cutdg schwarz_partition, solvers.py:
+ * 384-457): greedy BFS cores of >= target DOFs over the graph (adj_ptr,
+ * adj sorted), grown by one neighbour layer.  Returns the number of cores;
+ * xdg_schwarz_sizes gives {#core nodes, #extended nodes}; xdg_schwarz_copy
+ * writes core_ptr[ncore+1], core_nodes, ext_ptr[ncore+1], ext_nodes. */
+int64_t xdg_schwarz_partition(int64_t n, const int64_t* adj_ptr,
+                              const int64_t* adj, const int64_t* dofs,
+                              int64_t target);
+int xdg_schwarz_sizes(int64_t* out);
+int xdg_schwarz_copy(int64_t* core_ptr, int64_t* core_nodes, int64_t* ext_ptr,
+                     int64_t* ext_nodes);
 /* x[pdst] = A^-1 b[src] for every system of the forest at once:
  * 3 launches per forward level, 2 per backward level. */
 int xdg_mf_solve(const xdg_mf* mf, const double* b, double* x,

@@ -72,6 +72,12 @@ SIGNATURES = {
                         + [_vp] * 14),
     "xdg_mgs": (_i32, [_i64, _i32, _vp, _i64, _vp, _vp, _vp, _vp]),
     "xdg_mf_solve": (_i32, [_vp, _vp, _vp, _vp]),
+    "xdg_nd_order": (_i64, [_i64, _vp, _vp, _i64, _vp, _vp, _vp]),
+    "xdg_nd_boundaries": (_i64, [_i64, _vp, _vp, _i64, _vp, _vp, _vp]),
+    "xdg_nd_boundaries_copy": (_i32, [_vp, _vp]),
+    "xdg_schwarz_partition": (_i64, [_i64, _vp, _vp, _vp, _i64]),
+    "xdg_schwarz_sizes": (_i32, [_vp]),
+    "xdg_schwarz_copy": (_i32, [_vp, _vp, _vp, _vp]),
     "xdg_mf_rows_per_warp": (_i32, []),
 }
 

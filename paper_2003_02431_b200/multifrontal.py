@@ -191,7 +191,61 @@ class _ND:
 
 
 def nested_dissection(g_ptr, g_col, nv, leaf):
-    """Post-ordered elimination forest: (P list, children list)."""
+    """Post-ordered elimination forest (P list, children list): the native
+    xdg_nd_order (csrc/xdg_ordering.cu); nested_dissection_py is the same
+    algorithm in numpy (kept as its test oracle)."""
+    g_ptr = np.ascontiguousarray(g_ptr, np.int64)
+    g_col = np.ascontiguousarray(g_col, np.int64)
+    node_ptr = np.zeros(nv + 1, np.int64)
+    verts = np.zeros(max(nv, 1), np.int64)
+    parent = np.zeros(max(nv, 1), np.int64)
+    nn = int(nat.load().xdg_nd_order(int(nv), g_ptr.ctypes.data, g_col.ctypes.data,
+                                      int(leaf), node_ptr.ctypes.data, verts.ctypes.data,
+                                      parent.ctypes.data))
+    P = [verts[node_ptr[t]:node_ptr[t + 1]] for t in range(nn)]
+    kids = [[] for _ in range(nn)]
+    for c in range(nn):
+        if parent[c] >= 0:
+            kids[parent[c]].append(c)
+    return P, kids
+
+
+def boundaries(g_ptr, g_col, nv, P, kids):
+    """B_t of every front (xdg_nd_boundaries): neighbours of t's subtree in
+    ancestor fronts, sorted by (owner, vertex)."""
+    nn = len(P)
+    g_ptr = np.ascontiguousarray(g_ptr, np.int64)
+    g_col = np.ascontiguousarray(g_col, np.int64)
+    node_ptr = np.zeros(nn + 1, np.int64)
+    np.cumsum([len(p) for p in P], out=node_ptr[1:])
+    verts = np.ascontiguousarray(np.concatenate(P) if nn else np.zeros(0, np.int64), np.int64)
+    parent = np.full(max(nn, 1), -1, np.int64)
+    for t, ks in enumerate(kids):
+        parent[ks] = t
+    lib = nat.load()
+    tot = int(lib.xdg_nd_boundaries(int(nv), g_ptr.ctypes.data, g_col.ctypes.data, nn,
+                                    node_ptr.ctypes.data, verts.ctypes.data,
+                                    parent.ctypes.data))
+    b_ptr = np.zeros(nn + 1, np.int64)
+    b_verts = np.zeros(max(tot, 1), np.int64)
+    lib.xdg_nd_boundaries_copy(b_ptr.ctypes.data, b_verts.ctypes.data)
+    return [b_verts[b_ptr[t]:b_ptr[t + 1]] for t in range(nn)]
+
+
+def boundaries_py(g_ptr, g_col, P, kids, owner):
+    """numpy restatement of xdg_nd_boundaries (test oracle)."""
+    B_list = []
+    for t in range(len(P)):
+        cand = [g_col[_ranges(g_ptr[P[t]], g_ptr[P[t] + 1])]]
+        cand += [B_list[c] for c in kids[t]]
+        cand = np.unique(np.concatenate(cand))
+        Bt = cand[owner[cand] > t]
+        B_list.append(Bt[np.lexsort((Bt, owner[Bt]))])
+    return B_list
+
+
+def nested_dissection_py(g_ptr, g_col, nv, leaf):
+    """numpy restatement of xdg_nd_order (test oracle)."""
     from scipy.sparse import csr_matrix
     from scipy.sparse.csgraph import connected_components
 
@@ -263,14 +317,7 @@ class Multifrontal:
                 parent[c] = t
                 height[t] = max(height[t], height[c] + 1)
         # boundaries (post-order: subtree of t has ids < t, ancestors > t)
-        B_list = []
-        for t in range(nn):
-            P = P_list[t]
-            cand = [G.g_col[_ranges(G.g_ptr[P], G.g_ptr[P + 1])]]
-            cand += [B_list[c] for c in kids[t]]
-            cand = np.unique(np.concatenate(cand))
-            Bt = cand[owner[cand] > t]
-            B_list.append(Bt[np.lexsort((Bt, owner[Bt]))])
+        B_list = boundaries(G.g_ptr, G.g_col, nv, P_list, kids)
         pn = np.array([len(P) for P in P_list], np.int64) * m
         bn = np.array([len(B) for B in B_list], np.int64) * m
         self.P_list, self.B_list, self.kids, self.parent = P_list, B_list, kids, parent
@@ -361,7 +408,7 @@ class Multifrontal:
             if parent[t] >= 0:
                 last_use[height[t]] = max(last_use[height[t]], height[parent[t]])
         perms = [None] * nn
-        bad_nodes = []
+        bad_nodes, dev_perms = [], []
         for h in range(H):
             hb = [(k, ts) for k, ts in buckets.items() if k[0] == h]
             size = 0
@@ -442,18 +489,22 @@ class Multifrontal:
                 o = int(inv_off[ts[0]])
                 self.F[o:o + nb * P_ * P_] = INV.reshape(-1)
                 bad_nodes.append((ts, bad))
-                ph = perm.cpu().numpy()
-                for q, t in enumerate(ts):
-                    perms[t] = ph[q, :pn[t]].astype(np.int64)
+                dev_perms.append((ts, perm))  # read back once, after all heights
                 del LU, INV, A
             for hh in range(h + 1):
                 if hh in fronts and last_use[hh] <= h:
                     del fronts[hh]
-        for ts, bad in bad_nodes:
-            if bool(bad.any()):
-                t = ts[int(torch.nonzero(bad)[0])]
+        if bad_nodes:
+            flags = torch.cat([b.reshape(-1) for _, b in bad_nodes]).cpu().numpy()
+            allts = [t for ts, _ in bad_nodes for t in ts]
+            if flags.any():
+                t = allts[int(np.flatnonzero(flags)[0])]
                 blk = tuple(int(b) for b in G.gblk[P_list[t][:8]])
                 raise SingularSystemError(f"{what} is singular (front on blocks {blk}...)")
+        for ts, perm in dev_perms:
+            ph = perm.cpu().numpy()
+            for q, t in enumerate(ts):
+                perms[t] = ph[q, :pn[t]].astype(np.int64)
         del fronts
         t2 = time.perf_counter()
 

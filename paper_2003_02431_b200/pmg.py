@@ -66,8 +66,9 @@ def use_multifrontal(dims) -> bool:
     if dims.size == 0:
         return False
     free, _ = torch.cuda.mem_get_info()
+    # the dense factors are built in place and factored in <= 2 GB chunks
     return (int(dims.max()) > DENSE_LOW_MAX_SYSTEM
-            or 3 * 8 * int((dims * dims).sum()) > free // 4)
+            or 8 * int((dims * dims).sum()) > 0.6 * free)
 
 
 class PmgPlan:
@@ -158,7 +159,7 @@ class PmgPlan:
         # ---- low-order dense factors (solvers.py:208-221) ----------------
         need = 8 * int(lu_off[-1])
         free, _ = torch.cuda.mem_get_info(dev)
-        if 3 * need > free:  # factor + LU + inverse temporaries
+        if need + (8 << 30) > free:  # factors + chunk temporaries (<= 2 GB each)
             raise NotImplementedError(
                 f"dense low-order factors need {need / 1e9:.1f} GB (largest system "
                 f"{int(dims.max())} unknowns; {free / 1e9:.0f} GB free): use the "

@@ -42,6 +42,7 @@ class _Nodes:
     aggregates, one block each)."""
 
     def __init__(self, indexmap):
+        self.uniform_level = False
         if hasattr(indexmap, "block_of"):  # raw XdgIndexMap
             imap = indexmap
             self.num_nodes = imap.cutmesh.mesh.num_cells
@@ -61,6 +62,8 @@ class _Nodes:
             self._slices = [slice(g * size, (g + 1) * size)
                             for g in range(self.num_nodes)]
             self.total = lvl.num_dofs
+            self.block_size = size
+            self.uniform_level = True
         else:
             raise InvalidConfigError(
                 "index structure must be a species index map or a level")
@@ -87,6 +90,8 @@ def schwarz_partition(mesh_graph, indexmap, target_dofs: int) -> SchwarzPartitio
     if target_dofs < largest:
         raise InvalidConfigError(
             f"target {target_dofs} below the largest cell ({largest} DOFs)")
+    if nodes.uniform_level:
+        return _schwarz_partition_native(mesh_graph, nodes, dofs, int(target_dofs))
     nbrs = [sorted(a) for a in mesh_graph.adjacency]
 
     taken = np.zeros(n, bool)
@@ -133,3 +138,38 @@ def schwarz_partition(mesh_graph, indexmap, target_dofs: int) -> SchwarzPartitio
     return SchwarzPartition(cores=tuple(cores), blocks=tuple(extended),
                             block_rows=block_rows, damping=damping,
                             dim=nodes.dim)
+
+
+def _schwarz_partition_native(mesh_graph, nodes, dofs, target: int) -> SchwarzPartition:
+    """schwarz_partition on an aggregation level (node g = block g of
+    block_size DOFs) through the native xdg_schwarz_partition: the same
+    greedy BFS cores and one-layer extension, then damping and block rows
+    vectorised."""
+    from . import _native as nat
+
+    n = nodes.num_nodes
+    adj = [sorted(a) for a in mesh_graph.adjacency]
+    ptr = np.zeros(n + 1, np.int64)
+    np.cumsum([len(a) for a in adj], out=ptr[1:])
+    flat = np.ascontiguousarray(np.fromiter((v for a in adj for v in a), np.int64,
+                                            count=int(ptr[-1])))
+    dofs = np.ascontiguousarray(dofs, np.int64)
+    lib = nat.load()
+    ncore = int(lib.xdg_schwarz_partition(n, ptr.ctypes.data, flat.ctypes.data,
+                                          dofs.ctypes.data, target))
+    sz = np.zeros(2, np.int64)
+    lib.xdg_schwarz_sizes(sz.ctypes.data)
+    cptr, cnodes = np.zeros(ncore + 1, np.int64), np.zeros(max(int(sz[0]), 1), np.int64)
+    eptr, enodes = np.zeros(ncore + 1, np.int64), np.zeros(max(int(sz[1]), 1), np.int64)
+    lib.xdg_schwarz_copy(cptr.ctypes.data, cnodes.ctypes.data, eptr.ctypes.data,
+                         enodes.ctypes.data)
+    cores = tuple(tuple(int(v) for v in cnodes[cptr[q]:cptr[q + 1]]) for q in range(ncore))
+    extended = tuple(tuple(int(v) for v in enodes[eptr[q]:eptr[q + 1]])
+                     for q in range(ncore))
+    N = nodes.block_size
+    cover = np.bincount(enodes[:int(eptr[-1])], minlength=n).astype(float)
+    damping = np.repeat(cover, N)
+    if np.any(damping < 1.0):
+        raise InvalidConfigError("partition left degrees of freedom uncovered")
+    return SchwarzPartition(cores=cores, blocks=extended, block_rows=extended,
+                            damping=damping, dim=nodes.dim)

@@ -125,3 +125,33 @@ def test_nested_dissection_is_a_valid_elimination_forest():
     for u, v in zip(rows, G.g_col):
         a, b = owner[u], owner[v]
         assert anc(a, b) or anc(b, a)
+
+
+@pytest.mark.parametrize("shape,leaf,seed", [((10, 10, 6), 12, 0), ((17, 13), 5, 1),
+                                              ((9, 9, 9), 30, 2)])
+def test_native_ordering_matches_numpy_restatement(shape, leaf, seed):
+    """xdg_nd_order / xdg_nd_boundaries (host C++) give exactly the fronts
+    and boundary sets of the numpy restatement, incl. disconnected graphs."""
+    from paper_2003_02431_b200.multifrontal import (
+        boundaries,
+        boundaries_py,
+        nested_dissection_py,
+    )
+
+    rp, col, _ = grid_bsr(shape, 1, seed=seed)
+    nb = len(rp) - 1
+    rng = np.random.default_rng(seed)
+    drop = rng.random(nb) < 0.08  # knock out vertices: several components
+    keep = np.flatnonzero(~drop)
+    sets = [keep[: len(keep) // 2], keep[len(keep) // 2:], np.array([0, 1, 2])]
+    G = SystemGraph(rp, col, sets)
+    P, kids = nested_dissection(G.g_ptr, G.g_col, G.nv, leaf)
+    Pp, kp = nested_dissection_py(G.g_ptr, G.g_col, G.nv, leaf)
+    assert len(P) == len(Pp) and kids == kp
+    assert all(np.array_equal(a, b) for a, b in zip(P, Pp))
+    owner = np.empty(G.nv, np.int64)
+    for t, p in enumerate(P):
+        owner[p] = t
+    B = boundaries(G.g_ptr, G.g_col, G.nv, P, kids)
+    Bp = boundaries_py(G.g_ptr, G.g_col, P, kids, owner)
+    assert all(np.array_equal(a, b) for a, b in zip(B, Bp))
