@@ -1,6 +1,7 @@
 """Time the multifrontal solve (xdg_mf_solve) on a fixture's level operator.
 
     python tools/bench_mf.py tests/golden/large/cfg2.npz [m] [level]
+    python tools/bench_mf.py native [m] [level]   # cfg2 from this package's setup
 
 Builds the factor of the level's low-order system (leading m modes of
 every block; m = N: the full operator), times solves with CUDA events on the
@@ -23,14 +24,26 @@ from paper_2003_02431_b200.multifrontal import Multifrontal  # noqa: E402
 path = sys.argv[1]
 m = int(sys.argv[2]) if len(sys.argv) > 2 else 10
 lam = int(sys.argv[3]) if len(sys.argv) > 3 else 1
-z = np.load(path)
-rp, col = z[f"L{lam}_row_ptr"], z[f"L{lam}_col"]
-val = fixture_array(z, f"L{lam}_val")
-N = val.shape[1]
-nb = len(rp) - 1
-M = BlockSparseMatrix.from_bsr(rp, col, val, uniform_layout(nb, N), uniform_layout(nb, N))
+if path == "native":  # BASELINE cfg2 built by this package's own setup
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from bench import native_cfg2  # noqa: E402
+
+    hier, _, _ = native_cfg2()
+    rp = col = None
+    M = hier.level(lam).matrix
+    N = M.row_layout.sizes[0]
+    nb = M.row_layout.num_blocks
+else:
+    z = np.load(path)
+    rp, col = z[f"L{lam}_row_ptr"], z[f"L{lam}_col"]
+    val = fixture_array(z, f"L{lam}_val")
+    N = val.shape[1]
+    nb = len(rp) - 1
+    M = BlockSparseMatrix.from_bsr(rp, col, val, uniform_layout(nb, N), uniform_layout(nb, N))
 ctx = Context.get()
 D = M.device(ctx)
+if rp is None or path == "native":
+    rp, col = D.row_ptr.cpu().numpy(), D.col.cpu().numpy()
 t0 = time.perf_counter()
 v = np.arange(nb, dtype=np.int64)
 mf = Multifrontal(ctx, rp, col, D.val_t, N, [v], m, v * N, v * m)
