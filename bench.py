@@ -545,13 +545,13 @@ def run_ours(args):
         # z-slab chunks (device.HostStreamSpMV, xdg_bsr_spmv on row ranges)
         from paper_2003_02431_b200.device import HostStreamSpMV
 
-        hs = HostStreamSpMV(D, chunks=16)
+        hs = HostStreamSpMV(D, chunks=8)
         hs(xh, yh)
         torch.cuda.synchronize(dev)
         op(x_ext, y)
         e2e_exact = bool(torch.equal(yh, y.cpu()))
         step = (lambda: hs(xh, yh, sync=False))
-        e2e_path = ("pinned host x -> H2D (16 z-slab chunks) || xdg_bsr_spmv per chunk "
+        e2e_path = ("pinned host x -> H2D (8 z-slab chunks) || xdg_bsr_spmv per chunk "
                     "(C-ABI) || D2H y, full-duplex overlapped")
     else:
         def step():

@@ -41,6 +41,24 @@ def timed(fn, reps=10):
 out = {"bytes_per_vector": 8 * L}
 out["h2d_ms"] = timed(lambda: xd.copy_(xh, non_blocking=True))
 out["d2h_ms"] = timed(lambda: yh.copy_(xd, non_blocking=True))
+s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+xd2 = torch.empty_like(xd)
+
+
+def duplex():
+    cur = torch.cuda.current_stream()
+    s1.wait_stream(cur)
+    s2.wait_stream(cur)
+    with torch.cuda.stream(s1):
+        xd.copy_(xh, non_blocking=True)
+    with torch.cuda.stream(s2):
+        yh.copy_(xd2, non_blocking=True)
+    cur.wait_stream(s1)
+    cur.wait_stream(s2)
+
+
+out["duplex_ms"] = timed(duplex)
+out["duplex_floor_GBs"] = B / out["duplex_ms"] / 1e6
 for c in chunk_list:
     hs = HostStreamSpMV(D, chunks=c)
 
@@ -50,4 +68,18 @@ for c in chunk_list:
     ms = timed(lambda: (step(), hs.wait()))
     out[f"chunks{c}_ms"] = ms
     out[f"chunks{c}_GBs"] = B / ms / 1e6
+    # back-to-back products (the bench's e2e loop: one wait after K steps)
+    for _ in range(2):
+        step()
+    hs.wait()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(10):
+        step()
+    hs.wait()
+    b.record()
+    b.synchronize()
+    ms = a.elapsed_time(b) / 10
+    out[f"chunks{c}_overlapped_GBs"] = B / ms / 1e6
 print(json.dumps(out))
