@@ -184,10 +184,32 @@ class _ND:
         ks = np.arange(1, len(levels) - 1)
         left, right = cum[ks - 1], n - cum[ks]
         k = int(ks[np.argmin(np.maximum(left, right) * 2 + sizes[ks])])
-        L = np.sort(np.concatenate(levels[:k]))
-        R = np.sort(np.concatenate(levels[k + 1:]))
-        kids = self.run(L) + self.run(R)
-        return [self._node(levels[k], kids)]
+        # thinned separator: the smaller one-sided cut between levels k, k+1
+        nxt = np.zeros(len(self.dist), bool)
+        nxt[levels[k + 1]] = True
+        a1 = self._adjacent(levels[k], nxt)
+        cur = np.zeros(len(self.dist), bool)
+        cur[levels[k]] = True
+        a2 = self._adjacent(levels[k + 1], cur)
+        if a2.sum() < a1.sum():
+            S = levels[k + 1][a2]
+            L = np.concatenate(levels[:k + 1])
+            R = np.concatenate([levels[k + 1][~a2]] + levels[k + 2:])
+        else:
+            S = levels[k][a1]
+            L = np.concatenate(levels[:k] + [levels[k][~a1]])
+            R = np.concatenate(levels[k + 1:])
+        kids = self.run(np.sort(L)) + self.run(np.sort(R))
+        return [self._node(S, kids)]
+
+    def _adjacent(self, verts, mark):
+        """per vertex of verts: has a neighbour with mark set"""
+        if verts.size == 0:
+            return np.zeros(0, bool)
+        cnt = self.ptr[verts + 1] - self.ptr[verts]
+        hit = mark[self.col[_ranges(self.ptr[verts], self.ptr[verts + 1])]]
+        owner = np.repeat(np.arange(len(verts)), cnt)
+        return np.bincount(owner, weights=hit, minlength=len(verts)) > 0
 
 
 def nested_dissection(g_ptr, g_col, nv, leaf):
@@ -292,7 +314,7 @@ class Multifrontal:
     input b / output x (mode a adds a)."""
 
     def __init__(self, ctx, rp, col, val_t, N, sets, m, vsrc, vdst,
-                 leaf_unknowns: int = 192, what: str = "system",
+                 leaf_unknowns: int = 100, what: str = "system",
                  equilibrate: bool = True):
         import time
 
