@@ -72,6 +72,50 @@ __device__ __forceinline__ double group_dot(const double* __restrict__ row, V v,
   return s;
 }
 
+// Two rows per lane group (row sets a and b of a two-set task) of the bound
+// or upb phase, whose rows all span the same columns [0, n): one vector load
+// per element serves both rows, and both rows' factor loads are issued
+// together (2 x MF_U per lane in flight).  Each row keeps group_dot's
+// chunking and accumulation order: bit-identical to two group_dot calls.
+template <typename V>
+__device__ __forceinline__ void group_dot2(const double* __restrict__ ra,
+                                           const double* __restrict__ rb, V v, int j1,
+                                           int gl, int G, bool acta, bool actb, double& da,
+                                           double& db) {
+  double x[4] = {0.0, 0.0, 0.0, 0.0}, y[4] = {0.0, 0.0, 0.0, 0.0};
+  if (acta && j1 > 0) {
+    const int step = MF_U * G;
+    const double* rbb = actb ? rb : ra;
+    for (int jb = 0; jb < j1; jb += step) {
+      double p[MF_U], s[MF_U], q[MF_U];
+#pragma unroll
+      for (int u = 0; u < MF_U; ++u) {
+        const int j = min(jb + gl + G * u, j1 - 1);
+        p[u] = __ldg(ra + j);
+        s[u] = __ldg(rbb + j);
+        q[u] = v(j);
+      }
+#pragma unroll
+      for (int u = 0; u < MF_U; ++u)
+        if (jb + gl + G * u >= j1) q[u] = 0.0;
+#pragma unroll
+      for (int u = 0; u < MF_U; ++u) {
+        x[u & 3] = fma(p[u], q[u], x[u & 3]);
+        y[u & 3] = fma(s[u], q[u], y[u & 3]);
+      }
+    }
+  }
+  double sa = (x[0] + x[1]) + (x[2] + x[3]);
+  double sb = (y[0] + y[1]) + (y[2] + y[3]);
+  for (int o = 16; o > 0; o >>= 1)
+    if (o < G) {
+      sa += __shfl_xor_sync(0xffffffffu, sa, o);
+      sb += __shfl_xor_sync(0xffffffffu, sb, o);
+    }
+  da = sa;
+  db = actb ? sb : 0.0;
+}
+
 // MR rows of one front against the same vector (whole warp, lanes stride
 // 32): the vector is loaded once for all of them, so MU vector + MR*MU
 // factor loads are in flight per lane.  Row q covers [r0[q], r1[q]) inside
@@ -194,6 +238,20 @@ __device__ __forceinline__ double row_part(const Ctx& c, const xdg_mf_node& nd, 
 }
 
 template <int PH>
+__device__ __forceinline__ void row_part2(const Ctx& c, const xdg_mf_node& nd, int ra,
+                                          int rb, int gl, int G, bool acta, bool actb,
+                                          double& da, double& db) {
+  const int64_t mat = (PH == kBound) ? nd.lbp : nd.upb;
+  const int ld = (PH == kUpb) ? nd.ldb : nd.ldp;
+  const double* pa = c.F + mat + (int64_t)ra * ld;
+  const double* pb = c.F + mat + (int64_t)rb * ld;
+  if (PH == kUpb)
+    group_dot2(pa, pb, Gathered{c.Y, c.bidx + nd.bx}, nd.b, gl, G, acta, actb, da, db);
+  else
+    group_dot2(pa, pb, Direct{c.Y + nd.y}, nd.p, gl, G, acta, actb, da, db);
+}
+
+template <int PH>
 __device__ __forceinline__ void row_done(const Ctx& c, const xdg_mf_node& nd, int r,
                                          double d) {
   if (PH == kLower) c.Y[nd.y + r] = __dadd_rn(c.W[nd.w + r], d);
@@ -251,6 +309,17 @@ mf_rows_kernel(int64_t t0, int64_t ntasks, const int4* __restrict__ tasks, Ctx c
         for (int q = 0; q < kMR; ++q)
           if (r + q < nrows) row_done<PH>(c, nd, r + q, d[q]);
       }
+    } else if ((PH == kBound || PH == kUpb) && tk.z == -2) {
+      // two row sets of 32/G rows: rows a and b = a + 32/G share the vector
+      const int G = (PH == kUpb) ? nd.gb : nd.gp;
+      const int gl = lane & (G - 1);
+      const int ra = tk.y + lane / G, rb = ra + 32 / G;
+      const int nrows = (PH == kBound) ? nd.b : nd.p;
+      const bool acta = ra < nrows, actb = rb < nrows;
+      double da, db;
+      row_part2<PH>(c, nd, acta ? ra : 0, actb ? rb : 0, gl, G, acta, actb, da, db);
+      if (acta && gl == 0) row_done<PH>(c, nd, ra, da);
+      if (actb && gl == 0) row_done<PH>(c, nd, rb, db);
     } else {
       const int G = (PH == kUpb) ? nd.gb : nd.gp;
       const int gl = lane & (G - 1);

@@ -54,6 +54,17 @@ assert NODE_DT.itemsize == 96
 MF_U = 8  # loads in flight per lane per chunk (MF_U, xdg_multifrontal.cu)
 
 
+def _row_sets() -> int:
+    """Row sets per warp task of a short-row front (G < 32 lanes per row):
+    2 issues both sets' loads together (bit-identical sums).  XDG_MF_SETS."""
+    import os
+
+    v = int(os.environ.get("XDG_MF_SETS", "2"))
+    if v not in (1, 2):
+        raise ValueError(f"XDG_MF_SETS={v}: expected 1 or 2")
+    return v
+
+
 def _rows_per_warp() -> int:
     """Rows a warp task of a whole-warp front covers: the kernel's kMR."""
     return int(nat.load().xdg_mf_rows_per_warp())
@@ -597,10 +608,14 @@ class Multifrontal:
             for h in range(H):
                 ts = order[height[order] == h]
                 sh = ts[g[ts] < 32]
-                per = 32 // g[sh]
+                # bound / upb rows all span the same columns: two row sets
+                # per task share the vector loads (kernel: group_dot2)
+                sets = SETS if phase in (1, 2) else 1
+                per = (32 // g[sh]) * sets
                 cnt = (nrows[sh] + per - 1) // per
                 first = _ranges(np.zeros(len(sh), np.int64), cnt) * np.repeat(per, cnt)
-                grp = np.stack([np.repeat(sh, cnt), first, np.zeros_like(first),
+                grp = np.stack([np.repeat(sh, cnt), first,
+                                np.full_like(first, 0 if sets == 1 else -2),
                                 np.full_like(first, -1)], 1)
                 lg = ts[g[ts] == 32]
                 cnt2 = (nrows[lg] + MR - 1) // MR
@@ -612,6 +627,7 @@ class Multifrontal:
             return out, lev
 
         MR = _rows_per_warp()
+        SETS = _row_sets()
         all_tasks, lev_task = [], []
         base = 0
         for phase in range(4):

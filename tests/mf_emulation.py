@@ -20,7 +20,8 @@ def emulate_solve(mf, b, xlen):
         out = []
         for t, r0, nr, _ in tasks[lev[h]:lev[h + 1]]:
             nd = nodes[t]
-            n = nr if nr > 0 else 32 // nd[g]  # MR rows, or 32/G rows of G lanes
+            # MR rows, or 32/G rows of G lanes (two such sets: nr == -2)
+            n = nr if nr > 0 else (32 // nd[g]) * (2 if nr == -2 else 1)
             out += [(t, r) for r in range(r0, min(r0 + n, nd[count]))]
         return out
 

@@ -105,3 +105,21 @@ def test_solves_with_sparse_factors(solver, monkeypatch):
     s = 1 if hi - lo <= 2 else max(1, int(round(0.10 * np.median(env))))
     assert lo - s <= rep.iterations <= hi + s, (rep.iterations, env)
     assert rel(x, z[f"{solver}_x"]) <= 1e-8
+
+
+@pytest.mark.parametrize("case", ["bench4", "cfg1", "sphere8p3"])
+def test_two_set_tasks_bit_identical(case, monkeypatch):
+    """Bound / upb warp tasks with two row sets sharing the vector loads
+    (group_dot2) keep every row's accumulation order: bit-identical to the
+    one-set tasks."""
+    z, meta, hier = load(case)
+    ctx = Context.get()
+    for lam in range(1, hier.num_levels + 1):
+        D = hier.level(lam).matrix.device(ctx)
+        g = torch.Generator(device=ctx.device).manual_seed(lam)
+        b = torch.randn(D.nbr * D.N, dtype=torch.float64, device=ctx.device, generator=g)
+        out = []
+        for sets in ("1", "2"):
+            monkeypatch.setenv("XDG_MF_SETS", sets)
+            out.append(SparseDirect(D, ctx).apply(b))
+        assert torch.equal(out[0], out[1]), (case, lam)
