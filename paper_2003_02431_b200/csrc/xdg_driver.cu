@@ -131,6 +131,78 @@ mgs_kernel(int64_t n, int j, double* __restrict__ V, int64_t ldv,
     Vj1[e] = hn > 0.0 ? __ddiv_rn(w[e], hn) : 0.0;
 }
 
+// Same steps, same arithmetic and order, with each thread's w and current
+// basis column elements (at most K per thread) held in registers across the
+// grid syncs: a step streams only V_{i+1} (the axpy's V_i is the previous
+// step's V_{i+1}, w never leaves the SM) -- 1 instead of 3-4 vector passes
+// per step, bit-identical to mgs_kernel on the same grid.
+constexpr int kMgsK = 16;
+
+__global__ void __launch_bounds__(kT, 2)
+mgs_reg_kernel(int64_t n, int j, double* __restrict__ V, int64_t ldv,
+               double* __restrict__ w, double* __restrict__ h,
+               double* __restrict__ parts) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double red[kT / 32];
+  const int G = gridDim.x;
+  const int64_t stride = (int64_t)G * kT;
+  const int64_t i0 = (int64_t)blockIdx.x * kT + threadIdx.x;
+  double wr[kMgsK], vr[kMgsK];
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < kMgsK; ++k) {
+    const int64_t e = i0 + k * stride;
+    wr[k] = vr[k] = 0.0;
+    if (e < n) {
+      wr[k] = w[e];
+      vr[k] = V[e];
+      s = fma(vr[k], wr[k], s);
+    }
+  }
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) parts[blockIdx.x] = s;
+  grid.sync();
+  for (int i = 0; i <= j; ++i) {
+    const double* P = parts + (int64_t)(i & 1) * G;
+    double hi = 0.0;
+    for (int g = 0; g < G; ++g) hi += P[g];  // same order in every CTA
+    if (blockIdx.x == 0 && threadIdx.x == 0) h[i] = hi;
+    const double* Vn = V + (int64_t)(i + 1) * ldv;
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < kMgsK; ++k) {
+      const int64_t e = i0 + k * stride;
+      if (e < n) {
+        const double we = __dadd_rn(wr[k], -__dmul_rn(hi, vr[k]));
+        wr[k] = we;
+        if (i < j) {
+          vr[k] = Vn[e];
+          t = fma(vr[k], we, t);
+        } else {
+          t = fma(we, we, t);
+        }
+      }
+    }
+    t = block_sum(t, red);
+    if (threadIdx.x == 0) parts[(int64_t)((i + 1) & 1) * G + blockIdx.x] = t;
+    grid.sync();
+  }
+  const double* P = parts + (int64_t)((j + 1) & 1) * G;
+  double nrm2 = 0.0;
+  for (int g = 0; g < G; ++g) nrm2 += P[g];
+  const double hn = sqrt(nrm2);
+  if (blockIdx.x == 0 && threadIdx.x == 0) h[j + 1] = hn;
+  double* Vj1 = V + (int64_t)(j + 1) * ldv;
+#pragma unroll
+  for (int k = 0; k < kMgsK; ++k) {
+    const int64_t e = i0 + k * stride;
+    if (e < n) {
+      w[e] = wr[k];
+      Vj1[e] = hn > 0.0 ? __ddiv_rn(wr[k], hn) : 0.0;
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // host helpers
 
@@ -434,8 +506,23 @@ extern "C" int xdg_mgs(int64_t n, int j, double* V, int64_t ldv, double* w,
   // partials: 2 x grid doubles after the reduction counter slot
   double* parts = static_cast<double*>(ws) + 1;
   void* args[] = {&n, &j, &V, &ldv, &w, &h, &parts};
-  XDG_TRY_CUDA(cudaLaunchCooperativeKernel((const void*)mgs_kernel, dim3(grid),
-                                           dim3(kT), args, 0, s));
+  // register-resident variant on the same grid when it fits (XDG_MGS_REG=0
+  // forces the streaming kernel)
+  static thread_local int reg_per_sm = -1;
+  static const bool reg_ok = [] {
+    const char* e = getenv("XDG_MGS_REG");
+    return e == nullptr || atoi(e) != 0;
+  }();
+  if (reg_per_sm < 0 &&
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&reg_per_sm, mgs_reg_kernel, kT, 0) !=
+          cudaSuccess)
+    reg_per_sm = 0;
+  const bool use_reg = reg_ok && n >= 32768 &&  // small n: grid-sync bound either way
+                       (int64_t)grid <= (int64_t)sm_count() * reg_per_sm &&
+                       n <= (int64_t)kMgsK * grid * kT;
+  XDG_TRY_CUDA(cudaLaunchCooperativeKernel(
+      use_reg ? (const void*)mgs_reg_kernel : (const void*)mgs_kernel, dim3(grid), dim3(kT),
+      args, 0, s));
   return XDG_OK;
 }
 

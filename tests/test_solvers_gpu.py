@@ -166,3 +166,37 @@ def test_iterations_inside_reference_envelope(case, solver, tol):
         slack = max(1, int(round(0.10 * np.median(env))))  # up to ~12 %
     assert lo - slack <= rep.iterations <= hi + slack, (rep.iterations, sorted(env))
     assert rel(x, z["L1_direct_rhs"]) <= max(1e-8, 100 * tol)
+
+
+def test_register_resident_mgs_is_bit_identical():
+    """GMRES with the register-resident MGS kernel (mgs_reg_kernel, used
+    from 32,768 unknowns: the 16^3 p=3 hierarchy) and with the streaming one
+    (XDG_MGS_REG=0) gives identical histories and solutions (same arithmetic
+    in the same order on the same grid)."""
+    import subprocess
+    import sys
+
+    code = (
+        "import hashlib, json, numpy as np\n"
+        "from conftest import golden_path\n"
+        "from paper_2003_02431_b200.hierarchy import load_hierarchy\n"
+        "from paper_2003_02431_b200.solvers import SolverConfig, gmres_pmg_solve\n"
+        "z = np.load(golden_path('large/s16p3'))\n"
+        "h = load_hierarchy(z)\n"
+        "lv = h.level(1)\n"
+        "x, r = gmres_pmg_solve(lv.matrix, np.asarray(lv.rhs), SolverConfig(tolerance=1e-8,"
+        " max_iterations=300, k_lo=2, gmres_restart=50), dim=3)\n"
+        "print(json.dumps([r.iterations, hashlib.sha1(np.asarray(x).tobytes()).hexdigest(),"
+        " hashlib.sha1(np.asarray(r.residual_history).tobytes()).hexdigest()]))\n")
+    here = os.path.dirname(os.path.abspath(__file__))
+    if not os.path.exists(golden_path("large/s16p3")):
+        pytest.skip("large/s16p3 fixture absent (tests/golden/make_large.py)")
+    outs = []
+    for flag in ("1", "0"):
+        env = dict(os.environ, XDG_MGS_REG=flag,
+                   PYTHONPATH=os.pathsep.join([here, os.path.dirname(here)]))
+        p = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True,
+                           text=True, timeout=600, cwd=here)
+        assert p.returncode == 0, p.stderr[-2000:]
+        outs.append(json.loads(p.stdout.strip().splitlines()[-1]))
+    assert outs[0] == outs[1]
