@@ -257,6 +257,17 @@ typedef struct xdg_mf {
   double* Y;
   double* C;
   double apply_bytes;          /* algorithmic bytes of one solve            */
+  /* Fused low levels: heights [0, fuse_levels) run as nfbatch launches per
+   * sweep, one CTA per group of fronts, each group a sequence of stages
+   * (fronts of one height, children in earlier stages of the group).      */
+  int32_t fuse_levels, nfbatch;
+  int64_t nfstages;
+  const int64_t* fb_grp;       /* HOST [nfbatch+1] group ranges per launch   */
+  const int64_t* g_stage;      /* [ngroups+1] stage ranges per group         */
+  const int64_t* st_ent;       /* [nfstages+1] ranges into fent              */
+  const int64_t* st_task;      /* [4][nfstages+1] ranges into ftask per phase */
+  const int64_t* fent;         /* gather entry ids, stage by stage           */
+  const int32_t* ftask;        /* int4 warp tasks, stage by stage            */
 } xdg_mf;
 
 /* Rows per warp task of a front whose rows take a whole warp. */

@@ -267,13 +267,7 @@ __device__ __forceinline__ void row_done(const Ctx& c, const xdg_mf_node& nd, in
 // (G = 32) get kMR rows per task (multi_dot, shared vector loads); shorter
 // rows get 32/G rows per task, G lanes each (nrows field 0).
 template <int PH>
-__global__ void __launch_bounds__(kT, MF_MINB)
-mf_rows_kernel(int64_t t0, int64_t ntasks, const int4* __restrict__ tasks, Ctx c) {
-  const int lane = threadIdx.x & 31;
-  const int64_t nw = (int64_t)gridDim.x * (kT / 32);
-  for (int64_t w = (int64_t)blockIdx.x * (kT / 32) + (threadIdx.x >> 5); w < ntasks;
-       w += nw) {
-    const int4 tk = tasks[t0 + interleave(w, ntasks)];
+__device__ __forceinline__ void run_task(const Ctx& c, const int4 tk, const int lane) {
     const xdg_mf_node nd = c.nodes[tk.x];
     if (tk.z == kMR) {  // kMR rows r, r + 1, ... of a G = 32 front
       const int r = tk.y;
@@ -331,7 +325,78 @@ mf_rows_kernel(int64_t t0, int64_t ntasks, const int4* __restrict__ tasks, Ctx c
       const double d = row_part<PH>(c, nd, r, j0, j1, gl, G, act && j1 > j0);
       if (act && gl == 0) row_done<PH>(c, nd, r, d);
     }
+}
+
+template <int PH>
+__global__ void __launch_bounds__(kT, MF_MINB)
+mf_rows_kernel(int64_t t0, int64_t ntasks, const int4* __restrict__ tasks, Ctx c) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (kT / 32);
+  for (int64_t w = (int64_t)blockIdx.x * (kT / 32) + (threadIdx.x >> 5); w < ntasks;
+       w += nw)
+    run_task<PH>(c, tasks[t0 + interleave(w, ntasks)], lane);
+}
+
+// Gather entry e: W[ent_w] = scale * b[src] + children's contributions (in
+// fixed order).  Plain loads: in the fused kernel C was written by the same
+// launch (children of an earlier stage).
+__device__ __forceinline__ void gather_entry(int64_t e, const xdg_mf& m, const double* b) {
+  const int64_t s = m.ent_src[e];
+  double v = s >= 0 ? __dmul_rn(m.ent_scale[e], b[s]) : 0.0;
+  for (int64_t k = m.ent_cptr[e]; k < m.ent_cptr[e + 1]; ++k) v = __dadd_rn(v, m.C[m.ent_cidx[k]]);
+  m.W[m.ent_w[e]] = v;
+}
+
+// Warps of the CTA stride over the warp tasks [t0, t1) of one stage.
+template <int PH>
+__device__ __forceinline__ void stage_tasks(const Ctx& c, const int4* tasks, int64_t t0,
+                                            int64_t t1) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t w = t0 + (threadIdx.x >> 5); w < t1; w += kT / 32) run_task<PH>(c, tasks[w], lane);
+}
+
+// Fused low levels: one CTA per group of fronts, the group's stages (sets
+// of fronts of one height whose children are in earlier stages of the same
+// group) in order, __syncthreads between phases.  Forward: gather, lower,
+// bound per stage; backward (reverse stage order): upb, upper.  Every row
+// runs the same run_task code as the per-level launches: bit-identical.
+template <bool FWD>
+__global__ void __launch_bounds__(kT, MF_MINB)
+mf_fused_kernel(int64_t g0, int64_t g1, const xdg_mf m, const double* b, Ctx c) {
+  const int64_t ns1 = m.nfstages + 1;
+  const int4* ft = reinterpret_cast<const int4*>(m.ftask);
+  for (int64_t g = g0 + blockIdx.x; g < g1; g += gridDim.x) {
+    const int64_t s0 = m.g_stage[g], s1 = m.g_stage[g + 1];
+    if (FWD) {
+      for (int64_t s = s0; s < s1; ++s) {
+        for (int64_t i = m.st_ent[s] + threadIdx.x; i < m.st_ent[s + 1]; i += kT)
+          gather_entry(m.fent[i], m, b);
+        __syncthreads();
+        stage_tasks<kLower>(c, ft, m.st_task[s], m.st_task[s + 1]);
+        __syncthreads();
+        stage_tasks<kBound>(c, ft, m.st_task[ns1 + s], m.st_task[ns1 + s + 1]);
+        __syncthreads();
+      }
+    } else {
+      for (int64_t s = s1 - 1; s >= s0; --s) {
+        stage_tasks<kUpb>(c, ft, m.st_task[2 * ns1 + s], m.st_task[2 * ns1 + s + 1]);
+        __syncthreads();
+        stage_tasks<kUpper>(c, ft, m.st_task[3 * ns1 + s], m.st_task[3 * ns1 + s + 1]);
+        __syncthreads();
+      }
+    }
   }
+}
+
+template <bool FWD>
+int launch_fused(const xdg_mf* mf, int k, const double* b, double* x, cudaStream_t s) {
+  const int64_t g0 = mf->fb_grp[k], ng = mf->fb_grp[k + 1] - g0;
+  if (ng <= 0) return XDG_OK;
+  Ctx c{mf->nodes, mf->F, mf->bidx, mf->pdst, mf->pscale, mf->W, mf->Y, mf->C, x};
+  const int g = resident_grid(mf_fused_kernel<FWD>, kT, 0, ng * kT);
+  mf_fused_kernel<FWD><<<g, kT, 0, s>>>(g0, g0 + ng, *mf, b, c);
+  XDG_CHECK_LAUNCH();
+  return XDG_OK;
 }
 
 template <int PH>
@@ -358,7 +423,9 @@ extern "C" int xdg_mf_solve(const xdg_mf* mf, const double* b, double* x,
   if (mf->total == 0 || mf->nlevels == 0) return XDG_OK;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int H = mf->nlevels;
-  for (int h = 0; h < H; ++h) {
+  const int HF = mf->fuse_levels;  // levels [0, HF) run as fused batches
+  for (int k = 0; k < mf->nfbatch; ++k) XDG_TRY(launch_fused<true>(mf, k, b, x, s));
+  for (int h = HF; h < H; ++h) {
     const int64_t e0 = mf->lev_ent[h], e1 = mf->lev_ent[h + 1];
     if (e1 > e0) {
       mf_gather_kernel<<<grid_for(e1 - e0, kT, 8), kT, 0, s>>>(
@@ -369,9 +436,10 @@ extern "C" int xdg_mf_solve(const xdg_mf* mf, const double* b, double* x,
     XDG_TRY(launch_rows<kLower>(mf, h, x, s));
     XDG_TRY(launch_rows<kBound>(mf, h, x, s));
   }
-  for (int h = H - 1; h >= 0; --h) {
+  for (int h = H - 1; h >= HF; --h) {
     XDG_TRY(launch_rows<kUpb>(mf, h, x, s));
     XDG_TRY(launch_rows<kUpper>(mf, h, x, s));
   }
+  for (int k = mf->nfbatch - 1; k >= 0; --k) XDG_TRY(launch_fused<false>(mf, k, b, x, s));
   return XDG_OK;
 }

@@ -65,6 +65,22 @@ def _row_sets() -> int:
     return v
 
 
+def _fuse_mode() -> tuple[str, int]:
+    """Low levels run as fused launches (xdg_mf.fuse_levels), XDG_MF_FUSE:
+    "tree:K" -- one launch per sweep, one CTA per subtree of fronts of
+    height < K; "level:K" -- one launch per height < K, one CTA per front
+    (gather + lower + bound, upb + upper); "0" -- per-phase launches."""
+    import os
+
+    v = os.environ.get("XDG_MF_FUSE", "0")
+    if v == "0":
+        return "off", 0
+    mode, _, k = v.partition(":")
+    if mode not in ("tree", "level") or not k.isdigit():
+        raise ValueError(f"XDG_MF_FUSE={v}: expected tree:K, level:K or 0")
+    return mode, int(k)
+
+
 def _rows_per_warp() -> int:
     """Rows a warp task of a whole-warp front covers: the kernel's kMR."""
     return int(nat.load().xdg_mf_rows_per_warp())
@@ -78,7 +94,9 @@ class XdgMf(C.Structure):
         [(f, _vp) for f in ("lev_ent", "lev_task", "ent_w", "ent_src", "ent_cptr",
                             "ent_cidx", "tasks", "nodes", "bidx",
                             "pdst", "ent_scale", "pscale", "F", "W", "Y", "C")] + \
-        [("apply_bytes", C.c_double)]
+        [("apply_bytes", C.c_double), ("fuse_levels", C.c_int32), ("nfbatch", C.c_int32),
+         ("nfstages", C.c_int64)] + \
+        [(f, _vp) for f in ("fb_grp", "g_stage", "st_ent", "st_task", "fent", "ftask")]
 
 
 def _ranges(starts: np.ndarray, ends: np.ndarray) -> np.ndarray:
@@ -637,6 +655,7 @@ class Multifrontal:
             base += int(np.sum(lv))
         task_arr = (np.concatenate(all_tasks) if all_tasks
                     else np.zeros((0, 4), np.int64))
+        self._fused_plan(task_arr, lev_task, ent_first, pn, bn, height, parent, order, H)
         bidx = np.zeros(int(bn.sum()), np.int64)
         pdst = np.zeros(int(pn.sum()), np.int64)
         pscale = np.ones(int(pn.sum()))
@@ -678,6 +697,91 @@ class Multifrontal:
                       "plan": time.perf_counter() - t2}
 
     # ------------------------------------------------------------------
+    def _fused_plan(self, task_arr, lev_task, ent_first, pn, bn, height, parent, order, H):
+        """Groups / stages of the fused low levels (XDG_MF_FUSE).  A stage is
+        a set of fronts of one height; its gather entries and its warp tasks
+        of each phase are copied out stage by stage (the same int4 tasks the
+        per-level launches run)."""
+        mode, K = _fuse_mode()
+        K = min(K, H)
+        nn = len(pn)
+        dev = self.F.device
+        if K == 0:
+            self.fuse_levels = self.nfbatch = self.nfstages = 0
+            self.fb_grp = np.zeros(1, np.int64)
+            self.g_stage = self.st_ent = self.st_task = self.fent = torch.zeros(
+                1, dtype=I64, device=dev)
+            self.ftask = torch.zeros(4, dtype=I32, device=dev)
+            return
+        # per-node warp-task range of each phase (tasks of a node contiguous)
+        trng = []
+        for ph in range(4):
+            a, e = int(lev_task[ph][0]), int(lev_task[ph][-1])
+            nodes_ = task_arr[a:e, 0]
+            st = np.full(nn, 0, np.int64)
+            ct = np.bincount(nodes_, minlength=nn).astype(np.int64)
+            if len(nodes_):
+                chg = np.flatnonzero(np.r_[True, nodes_[1:] != nodes_[:-1]])
+                assert len(chg) == int((ct > 0).sum()), "tasks of a node not contiguous"
+                st[nodes_[chg]] = a + chg
+            trng.append((st, ct))
+        groups = []  # per batch: list of groups; group = list of stages (node arrays)
+        if K > 0 and mode == "level":
+            for h in range(K):
+                ts = order[height[order] == h]
+                groups.append([[np.array([t])] for t in ts])
+        elif K > 0:
+            low = height < K
+            root = np.arange(nn)
+            top = low & ((parent < 0) | ~low[np.maximum(parent, 0)])
+            # root of every low node (post-order: ids increase toward the root)
+            for t in range(nn - 1, -1, -1):
+                if low[t] and not top[t]:
+                    root[t] = root[parent[t]]
+            batch = []
+            members = {}
+            for t in order:  # by height, then id
+                if low[t]:
+                    members.setdefault(int(root[t]), []).append(int(t))
+            for r in sorted(members, key=lambda r: (-height[r], r)):
+                ms = np.array(members[r], np.int64)
+                batch.append([ms[height[ms] == h] for h in range(int(height[r]) + 1)])
+            groups.append(batch)
+        fb_grp, g_stage, st_ent, fent = [0], [0], [0], []
+        st_task = [[0] for _ in range(4)]
+        ftask = [[] for _ in range(4)]
+        tcount = [0, 0, 0, 0]
+        for batch in groups:
+            for grp in batch:
+                for nodes_ in grp:
+                    e = [np.arange(ent_first[t], ent_first[t] + pn[t] + bn[t]) for t in nodes_]
+                    fent += e
+                    st_ent.append(st_ent[-1] + sum(len(x) for x in e))
+                    for ph in range(4):
+                        st, ct = trng[ph]
+                        for t in nodes_:
+                            if ct[t]:
+                                ftask[ph].append(task_arr[st[t]:st[t] + ct[t]])
+                                tcount[ph] += int(ct[t])
+                        st_task[ph].append(tcount[ph])
+                g_stage.append(len(st_ent) - 1)
+            fb_grp.append(len(g_stage) - 1)
+        ns = len(st_ent) - 1
+        base = np.cumsum([0] + tcount[:3])
+        st_task = np.concatenate([np.asarray(st_task[ph], np.int64) + base[ph]
+                                  for ph in range(4)])
+        ft = [np.concatenate(ftask[ph]) for ph in range(4) if ftask[ph]]
+        ft = np.concatenate(ft) if ft else np.zeros((1, 4), np.int64)
+        fe = np.concatenate(fent) if fent else np.zeros(1, np.int64)
+        self.fuse_levels = K if groups else 0
+        self.nfbatch, self.nfstages = len(groups), ns
+        self.fb_grp = np.asarray(fb_grp, np.int64)
+        self.g_stage = torch.tensor(g_stage, dtype=I64, device=dev)
+        self.st_ent = torch.tensor(st_ent, dtype=I64, device=dev)
+        self.st_task = torch.from_numpy(st_task).to(dev)
+        self.fent = torch.from_numpy(np.ascontiguousarray(fe, np.int64)).to(dev)
+        self.ftask = torch.from_numpy(np.ascontiguousarray(ft)).to(dev, I32)
+
     def struct(self) -> XdgMf:
         if self._s is None:
             s = XdgMf()
@@ -688,6 +792,10 @@ class Multifrontal:
                       "ent_scale", "pscale", "bidx", "pdst", "F", "W", "Y", "C"):
                 setattr(s, f, getattr(self, f).data_ptr())
             s.apply_bytes = float(self.apply_bytes)
+            s.fuse_levels, s.nfbatch, s.nfstages = self.fuse_levels, self.nfbatch, self.nfstages
+            s.fb_grp = self.fb_grp.ctypes.data
+            for f in ("g_stage", "st_ent", "st_task", "fent", "ftask"):
+                setattr(s, f, getattr(self, f).data_ptr())
             self._s = s
         return self._s
 

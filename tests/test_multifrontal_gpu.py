@@ -123,3 +123,22 @@ def test_two_set_tasks_bit_identical(case, monkeypatch):
             monkeypatch.setenv("XDG_MF_SETS", sets)
             out.append(SparseDirect(D, ctx).apply(b))
         assert torch.equal(out[0], out[1]), (case, lam)
+
+
+@pytest.mark.parametrize("case", ["bench4", "cfg1", "sphere8p3"])
+def test_fused_low_levels_bit_identical(case, monkeypatch):
+    """Fused low levels (one CTA per front or per subtree, the same warp
+    tasks between __syncthreads) give bit-identical solves to the
+    per-phase launches."""
+    z, meta, hier = load(case)
+    ctx = Context.get()
+    for lam in range(1, hier.num_levels + 1):
+        D = hier.level(lam).matrix.device(ctx)
+        g = torch.Generator(device=ctx.device).manual_seed(lam)
+        b = torch.randn(D.nbr * D.N, dtype=torch.float64, device=ctx.device, generator=g)
+        out = []
+        for mode in ("0", "level:3", "tree:2", "tree:5", "tree:99"):
+            monkeypatch.setenv("XDG_MF_FUSE", mode)
+            out.append(SparseDirect(D, ctx).apply(b))
+        for o in out[1:]:
+            assert torch.equal(out[0], o), (case, lam)

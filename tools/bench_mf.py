@@ -44,26 +44,36 @@ ctx = Context.get()
 D = M.device(ctx)
 if rp is None or path == "native":
     rp, col = D.row_ptr.cpu().numpy(), D.col.cpu().numpy()
-t0 = time.perf_counter()
 v = np.arange(nb, dtype=np.int64)
-mf = Multifrontal(ctx, rp, col, D.val_t, N, [v], m, v * N, v * m)
-torch.cuda.synchronize()
-setup = time.perf_counter() - t0
 b = torch.randn(nb * N, dtype=torch.float64, device=ctx.device)
-x = torch.zeros(nb * m, dtype=torch.float64, device=ctx.device)
-for _ in range(3):
-    mf.solve(b, x)
-ts = []
-for _ in range(20):
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.record()
-    mf.solve(b, x)
-    e.record()
-    e.synchronize()
-    ts.append(s.elapsed_time(e))
-ms = statistics.median(ts)
-print(json.dumps({"lib": os.environ.get("XDG_LIB", "default"), "m": m, "level": lam,
-                  "unknowns": nb * m, "nodes": mf.nnodes, "levels": mf.nlevels,
-                  "factor_GB": mf.factor_bytes / 1e9, "setup_s": round(setup, 3),
-                  "times": {k: round(v, 3) for k, v in mf.times.items()},
-                  "solve_ms": ms, "GBs": mf.apply_bytes / ms / 1e6}))
+ref = None
+# XDG_MF_FUSE_SWEEP="0,level:6,tree:4": one plan per fused-level mode, each
+# checked bit-identical against the first
+for mode in os.environ.get("XDG_MF_FUSE_SWEEP", os.environ.get("XDG_MF_FUSE", "0")).split(","):
+    os.environ["XDG_MF_FUSE"] = mode
+    t0 = time.perf_counter()
+    mf = Multifrontal(ctx, rp, col, D.val_t, N, [v], m, v * N, v * m)
+    torch.cuda.synchronize()
+    setup = time.perf_counter() - t0
+    x = torch.zeros(nb * m, dtype=torch.float64, device=ctx.device)
+    for _ in range(3):
+        mf.solve(b, x)
+    ts = []
+    for _ in range(20):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        mf.solve(b, x)
+        e.record()
+        e.synchronize()
+        ts.append(s.elapsed_time(e))
+    ms = statistics.median(ts)
+    if ref is None:
+        ref = x.clone()
+    print(json.dumps({"lib": os.environ.get("XDG_LIB", "default"), "fuse": mode, "m": m,
+                      "level": lam, "unknowns": nb * m, "nodes": mf.nnodes,
+                      "levels": mf.nlevels, "factor_GB": mf.factor_bytes / 1e9,
+                      "setup_s": round(setup, 3),
+                      "times": {k: round(v, 3) for k, v in mf.times.items()},
+                      "solve_ms": ms, "min_ms": min(ts), "GBs": mf.apply_bytes / ms / 1e6,
+                      "bit_identical": bool(torch.equal(x, ref))}), flush=True)
+    del mf
