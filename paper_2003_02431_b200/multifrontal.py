@@ -420,6 +420,15 @@ class Multifrontal:
             fst += nb * B_ * P_
             upb_off[ts] = fst + np.arange(nb) * P_ * B_
             fst += nb * P_ * B_
+        # the padded factors plus the largest height's front buffer must fit
+        front_max = max((sum(len(ts) * (P_ + B_) ** 2 for (hh, P_, B_), ts in buckets.items()
+                             if hh == h) for h in range(H)), default=0)
+        free, _ = torch.cuda.mem_get_info(dev)
+        if 8 * (fst + 2 * front_max) > free:
+            raise NotImplementedError(
+                f"multifrontal {what}: factors need {8 * fst / 1e9:.1f} GB + fronts "
+                f"{8 * front_max / 1e9:.1f} GB, {free / 1e9:.1f} GB of HBM free "
+                f"({self.total} unknowns)")
         self.F = torch.zeros(max(fst, 1), dtype=F64, device=dev)
         def offsets(sz):  # exclusive prefix sums in (height, id) order
             o = np.zeros(nn, np.int64)
