@@ -423,7 +423,8 @@ class Multifrontal:
         # the padded factors plus the largest height's front buffer must fit
         front_max = max((sum(len(ts) * (P_ + B_) ** 2 for (hh, P_, B_), ts in buckets.items()
                              if hh == h) for h in range(H)), default=0)
-        free, _ = torch.cuda.mem_get_info(dev)
+        free = (torch.cuda.mem_get_info(dev)[0] if torch.device(dev).type == "cuda"
+                else float("inf"))
         if 8 * (fst + 2 * front_max) > free:
             raise NotImplementedError(
                 f"multifrontal {what}: factors need {8 * fst / 1e9:.1f} GB + fronts "
