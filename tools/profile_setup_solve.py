@@ -28,7 +28,7 @@ if path == "cfg4-native":  # BASELINE config 4 at full size via the native setup
                      levelset="spheres",
                      levelset_params={"centers": [tuple(-0.4 + c), tuple(0.4 - c)],
                                       "radius": 0.3}, mu_b=100.0, num_levels=4,
-                     source="sin")
+                     source="sin", workers=os.cpu_count() or 1)
     t0 = time.perf_counter()
     hier = assemble_case(case).hierarchy
     print(f"native setup {time.perf_counter() - t0:.1f} s", flush=True)
