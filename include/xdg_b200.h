@@ -179,6 +179,15 @@ int xdg_pmg_build_low(int nwork, int N, int m, const int* wi_ptr,
                       const int* wi_blk, const int* wi_lcol, const int* wi_lrow,
                       const int* wi_sys, const int64_t* lu_off, const int* dims,
                       const double* val_t, double* A, xdg_stream_t stream);
+/* Setup: size-bucket staging of the batched dense factorization.
+ * unpack = 0: packed[q] (P x P) = the n x n row-major system sys[q]
+ * (n = dims[sys[q]], at flat + off[sys[q]]), identity in the padding;
+ * unpack = 1: the n x n top-left of packed[q] back to flat.  Replaces the
+ * per-system copies around the reference's per-block lu_factor
+ * (solvers.py:208-221). */
+int xdg_pack_square(int64_t nsys, const int64_t* sys, const int* dims,
+                    const int64_t* off, int P, double* packed, double* flat,
+                    int unpack, xdg_stream_t stream);
 /* Setup: H[c] = M[cells[c], cells[c]](m:, m:), row-major, diag_blk[c] the
  * block index of the diagonal block (solvers.py:232). */
 int xdg_pmg_gather_high(int ncells, int N, int m, const int* cells,

@@ -51,6 +51,7 @@ SIGNATURES = {
     "xdg_ipiv_to_perm": (_i32, [_i32, _vp, _vp, _vp, _vp, _vp]),
     "xdg_pmg_build_low": (_i32, [_i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp,
                                  _vp, _vp, _vp, _vp, _vp]),
+    "xdg_pack_square": (_i32, [_i64, _vp, _vp, _vp, _i32, _vp, _vp, _i32, _vp]),
     "xdg_pmg_gather_high": (_i32, [_i32, _i32, _i32, _vp, _vp, _vp, _vp,
                                    _vp]),
     "xdg_pmg_high": (_i32, [_i32, _i32, _i32] + [_vp] * 15),

@@ -249,6 +249,31 @@ combine_kernel(int nbr, int N, const int* __restrict__ cptr,
   }
 }
 
+// One CTA per system q of a size bucket: packed[q] (P x P) <-> the
+// system's n x n row-major matrix at flat + off[sys[q]].  Pack writes the
+// identity in the padding (rows / columns n..P-1).
+__global__ void __launch_bounds__(kT)
+pack_square_kernel(int64_t nsys, const int64_t* __restrict__ sys,
+                   const int* __restrict__ dims, const int64_t* __restrict__ off, int P,
+                   double* __restrict__ packed, double* __restrict__ flat, int unpack) {
+  for (int64_t q = blockIdx.x; q < nsys; q += gridDim.x) {
+    const int64_t sq = sys[q];
+    const int n = dims[sq];
+    double* src = flat + off[sq];
+    double* dst = packed + q * (int64_t)P * P;
+    const int64_t cnt = unpack ? (int64_t)n * n : (int64_t)P * P;
+    for (int64_t k = threadIdx.x; k < cnt; k += kT) {
+      if (unpack) {
+        const int i = (int)(k / n), j = (int)(k % n);
+        src[k] = dst[(int64_t)i * P + j];
+      } else {
+        const int i = (int)(k / P), j = (int)(k % P);
+        dst[k] = (i < n && j < n) ? src[(int64_t)i * n + j] : (i == j ? 1.0 : 0.0);
+      }
+    }
+  }
+}
+
 }  // namespace
 }  // namespace xdg
 
@@ -327,6 +352,18 @@ extern "C" int xdg_pmg_combine(int nbr, int N, const int* cptr,
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   combine_kernel<<<grid_for((int64_t)nbr * N, kT, 8), kT, 0, s>>>(
       nbr, N, cptr, cpos, out, damping, z);
+  XDG_CHECK_LAUNCH();
+  return XDG_OK;
+}
+
+extern "C" int xdg_pack_square(int64_t nsys, const int64_t* sys, const int* dims,
+                               const int64_t* off, int P, double* packed, double* flat,
+                               int unpack, xdg_stream_t stream) {
+  XDG_REQUIRE(P >= 1, XDG_ERR_ARG, "bad pad size P=%d", P);
+  if (nsys <= 0) return XDG_OK;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  pack_square_kernel<<<grid_for(nsys * kT, kT, 8), kT, 0, s>>>(nsys, sys, dims, off, P,
+                                                              packed, flat, unpack);
   XDG_CHECK_LAUNCH();
   return XDG_OK;
 }

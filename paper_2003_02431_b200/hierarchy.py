@@ -12,7 +12,7 @@ every level matrix and restriction, right-hand sides, aggregate graphs).
 from __future__ import annotations
 
 import json
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 from typing import Optional
 
 import numpy as np
@@ -26,6 +26,21 @@ class MeshGraph:
     num_cells: int
     edges: tuple
     adjacency: tuple
+    # (ptr int64[n+1], col int64[nnz]): the adjacency with every row sorted,
+    # when the builder has it as arrays (schwarz_partition reads it instead
+    # of flattening `adjacency`); None for graphs built elsewhere
+    csr: object = field(default=None, compare=False, repr=False)
+
+
+def graph_csr(rows: np.ndarray, cols: np.ndarray, n: int):
+    """(ptr, col) of the directed pairs (rows, cols), rows sorted, each row's
+    columns sorted (duplicates kept, like sorted(adjacency[i]))."""
+    rows = np.asarray(rows, np.int64)
+    cols = np.asarray(cols, np.int64)
+    o = np.lexsort((cols, rows))
+    ptr = np.zeros(n + 1, np.int64)
+    np.cumsum(np.bincount(rows, minlength=n), out=ptr[1:])
+    return ptr, np.ascontiguousarray(cols[o])
 
 
 @dataclass(frozen=True)
@@ -93,7 +108,9 @@ def _graph(ptr: np.ndarray, adj: np.ndarray) -> MeshGraph:
     n = len(ptr) - 1
     adjacency = tuple(tuple(int(v) for v in adj[ptr[i]:ptr[i + 1]]) for i in range(n))
     edges = tuple(sorted((a, b) for a in range(n) for b in adjacency[a] if a < b))
-    return MeshGraph(num_cells=n, edges=edges, adjacency=adjacency)
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(np.asarray(ptr, np.int64)))
+    return MeshGraph(num_cells=n, edges=edges, adjacency=adjacency,
+                     csr=graph_csr(rows, np.asarray(adj, np.int64)[:len(rows)], n))
 
 
 def fixture_array(z, key: str) -> np.ndarray:

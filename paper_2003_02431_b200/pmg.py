@@ -187,19 +187,28 @@ class PmgPlan:
                 continue
             for c0 in range(0, len(idx), max(1, (1 << 31) // (8 * P * P))):
                 chunk = idx[c0:c0 + max(1, (1 << 31) // (8 * P * P))]
-                batch = torch.eye(P, dtype=F64, device=dev).repeat(len(chunk), 1, 1)
-                for q, s_ in enumerate(chunk):
-                    n = int(dims[s_])
-                    batch[q, :n, :n] = A[lu_off[s_]:lu_off[s_] + n * n].view(n, n)
+                chunk_d = torch.from_numpy(np.ascontiguousarray(chunk, np.int64)).to(dev)
+                batch = torch.empty(len(chunk), P, P, dtype=F64, device=dev)
+                nat.check(ctx.lib.xdg_pack_square(
+                    len(chunk), chunk_d.data_ptr(), self.dims.data_ptr(),
+                    self.lu_off.data_ptr(), P, batch.data_ptr(), A.data_ptr(), 0,
+                    ctx.stream), "pack_square")
                 LU, pv, info = lu_factor_batched(batch)
                 dg = torch.diagonal(LU, dim1=-2, dim2=-1)
                 bad = (info != 0) | ~torch.isfinite(LU).flatten(1).all(1) | (dg == 0).any(1)
-                bad_flags.index_copy_(0, torch.from_numpy(chunk).to(dev), bad)
-                INV = triangular_inverses(LU)
-                for q, s_ in enumerate(chunk):
-                    n = int(dims[s_])
-                    A[lu_off[s_]:lu_off[s_] + n * n] = INV[q, :n, :n].reshape(-1)
-                    piv[vec_off[s_]:vec_off[s_] + n] = pv[q, :n].to(I32)
+                bad_flags.index_copy_(0, chunk_d, bad)
+                INV = triangular_inverses(LU).contiguous()
+                nat.check(ctx.lib.xdg_pack_square(
+                    len(chunk), chunk_d.data_ptr(), self.dims.data_ptr(),
+                    self.lu_off.data_ptr(), P, INV.data_ptr(), A.data_ptr(), 1,
+                    ctx.stream), "unpack_square")
+                # pivots of the leading n rows of every system
+                nq = dims[chunk]
+                q_of = np.repeat(np.arange(len(chunk)), nq)
+                i_of = _ranges(np.zeros(len(chunk), np.int64), nq)
+                dst = torch.from_numpy(vec_off[chunk][q_of] + i_of).to(dev)
+                srcp = torch.from_numpy(q_of * P + i_of).to(dev)
+                piv[dst] = pv.reshape(-1)[srcp].to(I32)
                 del batch, LU, INV
         if bool(bad_flags.any()):
             s_bad = int(torch.nonzero(bad_flags)[0])

@@ -58,9 +58,7 @@ class _Nodes:
             self.num_nodes = lvl.num_blocks
             size = lvl.block_size
             self.dim = lvl.basis.dim
-            self._blocks = [(g,) for g in range(self.num_nodes)]
-            self._slices = [slice(g * size, (g + 1) * size)
-                            for g in range(self.num_nodes)]
+            self._blocks = self._slices = None  # node g = block g (no lists)
             self.total = lvl.num_dofs
             self.block_size = size
             self.uniform_level = True
@@ -69,13 +67,19 @@ class _Nodes:
                 "index structure must be a species index map or a level")
 
     def blocks_of(self, j):
+        if self.uniform_level:
+            return (j,)
         return self._blocks[j]
 
     def dofs_of(self, j):
+        if self.uniform_level:
+            return self.block_size
         return sum(self._slices[b].stop - self._slices[b].start
                    for b in self._blocks[j])
 
     def dof_slices(self, j):
+        if self.uniform_level:
+            return [slice(j * self.block_size, (j + 1) * self.block_size)]
         return [self._slices[b] for b in self._blocks[j]]
 
 
@@ -85,7 +89,10 @@ def schwarz_partition(mesh_graph, indexmap, target_dofs: int) -> SchwarzPartitio
     if mesh_graph.num_cells != n:
         raise DimensionMismatchError(
             "graph and index structure disagree on the cell count")
-    dofs = np.array([nodes.dofs_of(j) for j in range(n)], np.int64)
+    if nodes.uniform_level:
+        dofs = np.full(n, nodes.block_size, np.int64)
+    else:
+        dofs = np.array([nodes.dofs_of(j) for j in range(n)], np.int64)
     largest = int(dofs.max()) if n else 0
     if target_dofs < largest:
         raise InvalidConfigError(
@@ -140,6 +147,13 @@ def schwarz_partition(mesh_graph, indexmap, target_dofs: int) -> SchwarzPartitio
                             dim=nodes.dim)
 
 
+def _pieces(flat: np.ndarray, ptr: np.ndarray) -> list:
+    """[flat[ptr[q]:ptr[q+1]] as a list of Python ints for each q]."""
+    vals = flat[:int(ptr[-1])].tolist()
+    p = ptr.tolist()
+    return [vals[p[q]:p[q + 1]] for q in range(len(p) - 1)]
+
+
 def _schwarz_partition_native(mesh_graph, nodes, dofs, target: int) -> SchwarzPartition:
     """schwarz_partition on an aggregation level (node g = block g of
     block_size DOFs) through the native xdg_schwarz_partition: the same
@@ -148,11 +162,17 @@ def _schwarz_partition_native(mesh_graph, nodes, dofs, target: int) -> SchwarzPa
     from . import _native as nat
 
     n = nodes.num_nodes
-    adj = [sorted(a) for a in mesh_graph.adjacency]
-    ptr = np.zeros(n + 1, np.int64)
-    np.cumsum([len(a) for a in adj], out=ptr[1:])
-    flat = np.ascontiguousarray(np.fromiter((v for a in adj for v in a), np.int64,
-                                            count=int(ptr[-1])))
+    csr = getattr(mesh_graph, "csr", None)
+    if csr is not None:  # sorted rows built from the builder's arrays
+        ptr, flat = csr
+        ptr = np.ascontiguousarray(ptr, np.int64)
+        flat = np.ascontiguousarray(flat, np.int64)
+    else:
+        adj = [sorted(a) for a in mesh_graph.adjacency]
+        ptr = np.zeros(n + 1, np.int64)
+        np.cumsum([len(a) for a in adj], out=ptr[1:])
+        flat = np.ascontiguousarray(np.fromiter((v for a in adj for v in a), np.int64,
+                                                count=int(ptr[-1])))
     dofs = np.ascontiguousarray(dofs, np.int64)
     lib = nat.load()
     ncore = int(lib.xdg_schwarz_partition(n, ptr.ctypes.data, flat.ctypes.data,
@@ -163,9 +183,8 @@ def _schwarz_partition_native(mesh_graph, nodes, dofs, target: int) -> SchwarzPa
     eptr, enodes = np.zeros(ncore + 1, np.int64), np.zeros(max(int(sz[1]), 1), np.int64)
     lib.xdg_schwarz_copy(cptr.ctypes.data, cnodes.ctypes.data, eptr.ctypes.data,
                          enodes.ctypes.data)
-    cores = tuple(tuple(int(v) for v in cnodes[cptr[q]:cptr[q + 1]]) for q in range(ncore))
-    extended = tuple(tuple(int(v) for v in enodes[eptr[q]:eptr[q + 1]])
-                     for q in range(ncore))
+    cores = tuple(map(tuple, _pieces(cnodes, cptr)))
+    extended = tuple(map(tuple, _pieces(enodes, eptr)))
     N = nodes.block_size
     cover = np.bincount(enodes[:int(eptr[-1])], minlength=n).astype(float)
     damping = np.repeat(cover, N)

@@ -18,6 +18,7 @@ from . import _native as nat
 from .blockmatrix import BlockSparseMatrix, as_block_sparse
 from .errors import LayoutMismatchError
 from .hierarchy import HierarchyLevel, LevelInfo, MeshGraph, MultigridHierarchy  # noqa: F401
+from .hierarchy import graph_csr
 
 I32 = torch.int32
 
@@ -416,7 +417,9 @@ def aggregate_graph(level: LevelData, mesh) -> MeshGraph:
         nbrs[a].append(b)
         nbrs[b].append(a)
     return MeshGraph(num_cells=n, edges=tuple(map(tuple, P.tolist())),
-                     adjacency=tuple(tuple(sorted(x)) for x in nbrs))
+                     adjacency=tuple(tuple(sorted(x)) for x in nbrs),
+                     csr=graph_csr(np.concatenate([P[:, 0], P[:, 1]]),
+                                   np.concatenate([P[:, 1], P[:, 0]]), n))
 
 
 def assemble_device(terms, ctx=None):

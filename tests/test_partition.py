@@ -35,3 +35,23 @@ def test_partition_rejects_target_below_cell():
     lv = hier.level(1)
     with pytest.raises(InvalidConfigError):
         schwarz_partition(lv.graph, lv.data, lv.data.block_size - 1)
+
+
+@pytest.mark.parametrize("case", ["bench4", "cfg1", "sphere8p3"])
+def test_partition_graph_csr_same_as_adjacency(case):
+    """The graph's array copy (MeshGraph.csr) is the sorted adjacency, and
+    the partition read through it equals the one read from the tuples."""
+    from dataclasses import replace
+
+    hier = load_hierarchy(np.load(golden_path(case)))
+    for lam in range(1, hier.num_levels + 1):
+        lv = hier.level(lam)
+        ptr, flat = lv.graph.csr
+        srt = [v for a in lv.graph.adjacency for v in sorted(a)]
+        assert flat.tolist() == srt
+        assert np.diff(ptr).tolist() == [len(a) for a in lv.graph.adjacency]
+        tgt = max(2000, lv.data.block_size)
+        a = schwarz_partition(lv.graph, lv.data, tgt)
+        b = schwarz_partition(replace(lv.graph, csr=None), lv.data, tgt)
+        assert a.cores == b.cores and a.block_rows == b.block_rows
+        assert np.array_equal(a.damping, b.damping)

@@ -56,6 +56,10 @@ def test_assemble_case_levels(name):
         assert np.abs(lv.rhs - rr).max() <= 1e3 * TOL[name] * np.abs(rr).max()
         adj = np.array([v for a in lv.graph.adjacency for v in a], np.int64)
         assert np.array_equal(adj, z[p + "adj"])
+        ptr, flat = lv.graph.csr  # the array copy schwarz_partition reads
+        srt = np.array([v for a in lv.graph.adjacency for v in sorted(a)], np.int64)
+        assert np.array_equal(flat, srt)
+        assert np.array_equal(np.diff(ptr), [len(a) for a in lv.graph.adjacency])
 
 
 def _slack(env):
