@@ -65,7 +65,12 @@ class _quiet_stdout:
         os.close(self._null)
 
 
-LU_BLOCK = 128  # panel width of the blocked batched LU (XDG_LU_BLOCK, 0 = off)
+# Blocked batched LU for systems larger than LU_BLOCKED_MIN (XDG_LU_BLOCK =
+# panel width, 0 = off).  tools/bench_lu_blocked.py on B200: 340 x 1920
+# 0.293 s unblocked MAGMA vs 0.205 s blocked (nb 256); 1100 x 896 0.094 vs
+# 0.096 s; 4400 x 448 0.059 vs 0.070 s.
+LU_BLOCK = 256
+LU_BLOCKED_MIN = 1280
 
 
 def lu_factor_batched(A: torch.Tensor):
@@ -78,7 +83,7 @@ def lu_factor_batched(A: torch.Tensor):
     import os
 
     nb = int(os.environ.get("XDG_LU_BLOCK", LU_BLOCK))
-    if A.dim() == 3 and A.shape[0] >= 4 and nb > 0 and A.shape[-1] > 2 * nb:
+    if A.dim() == 3 and A.shape[0] >= 4 and nb > 0 and A.shape[-1] > max(LU_BLOCKED_MIN, nb):
         return lu_factor_blocked(A, nb)
     return _lu_factor_unblocked(A)
 

@@ -179,7 +179,9 @@ class PmgPlan:
         # for batches >= 4), and the top-left n x n blocks copied back.  One
         # deferred singularity check for all systems.
         bad_flags = torch.zeros(self.nsys, dtype=torch.bool, device=dev)
-        pad_to = np.where(dims <= 64, dims, ((dims + 127) // 128) * 128)
+        # small systems padded to multiples of 16 (few buckets: every bucket
+        # is one batched-getrf call with a fixed cost), larger ones to 128
+        pad_to = np.where(dims <= 64, ((dims + 15) // 16) * 16, ((dims + 127) // 128) * 128)
         for P in np.unique(pad_to):
             idx = np.flatnonzero(pad_to == P)
             P = int(P)

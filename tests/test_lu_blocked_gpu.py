@@ -17,7 +17,7 @@ def test_blocked_lu_matches_unblocked(b, n, nb):
     LU, piv, info = lu_factor_blocked(A, nb)
     LU0, piv0, info0 = _lu_factor_unblocked(A)
     assert int(info.abs().sum()) == 0 and int(info0.abs().sum()) == 0
-    P, L, U = torch.linalg.lu_unpack(LU, piv)
+    P, L, U = torch.lu_unpack(LU, piv)
     rec = (P @ L @ U - A).flatten(1).norm(dim=1) / A.flatten(1).norm(dim=1)
     assert float(rec.max()) <= 1e-13
     # partial pivoting picks the same rows (no near-ties in random data)
