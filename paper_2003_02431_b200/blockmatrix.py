@@ -258,6 +258,15 @@ class BlockSparseMatrix:
         return y[self._pad_index(self.row_layout, N)]
 
     def transpose(self) -> "BlockSparseMatrix":
+        if self._blocks is None:  # array form: one stable sort, no dict
+            rp, col, val = self._bsr
+            rows = np.repeat(np.arange(len(rp) - 1, dtype=np.int64), np.diff(rp))
+            o = np.lexsort((rows, col))
+            trp = np.zeros(self.col_layout.num_blocks + 1, np.int64)
+            np.cumsum(np.bincount(col, minlength=self.col_layout.num_blocks), out=trp[1:])
+            return BlockSparseMatrix.from_bsr(
+                trp, rows[o], np.ascontiguousarray(val[o].transpose(0, 2, 1)),
+                self.col_layout, self.row_layout)
         out = BlockSparseMatrix(self.col_layout, self.row_layout)
         for (bi, bj), block in self.blocks.items():
             out.blocks[(bj, bi)] = block.T

@@ -55,3 +55,31 @@ def test_partition_graph_csr_same_as_adjacency(case):
         b = schwarz_partition(replace(lv.graph, csr=None), lv.data, tgt)
         assert a.cores == b.cores and a.block_rows == b.block_rows
         assert np.array_equal(a.damping, b.damping)
+
+
+@pytest.mark.parametrize("case", ["cfg1", "sphere8p3"])
+def test_array_form_transpose_matches_dict_transpose(case):
+    """BlockSparseMatrix.transpose on array-form operators (one stable sort)
+    gives the same blocks as the reference's dict loop (blockmatrix.py:
+    127-131) -- the restrictions R of every level and the level matrices."""
+    from paper_2003_02431_b200.blockmatrix import BlockSparseMatrix
+
+    hier = load_hierarchy(np.load(golden_path(case)))
+    for lam in range(1, hier.num_levels + 1):
+        lv = hier.level(lam)
+        for M in (lv.matrix, lv.restriction):
+            if M is None:
+                continue
+            rp, col, val = M.bsr_arrays()
+            A = BlockSparseMatrix.from_bsr(rp, col, val, M.row_layout, M.col_layout)
+            T = A.transpose()
+            assert T._blocks is None  # array form kept
+            Bd = BlockSparseMatrix(M.row_layout, M.col_layout)
+            for k in range(len(rp) - 1):
+                for j in range(rp[k], rp[k + 1]):
+                    Bd.add_block(k, int(col[j]), val[j])
+            ref = Bd.transpose()
+            t_rp, t_col, t_val = T.bsr_arrays()
+            r_rp, r_col, r_val = ref.bsr_arrays()
+            assert np.array_equal(t_rp, r_rp) and np.array_equal(t_col, r_col)
+            assert np.array_equal(t_val, r_val)
