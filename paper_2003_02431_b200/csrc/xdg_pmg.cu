@@ -21,6 +21,8 @@
 //  xdg_pmg_combine     (apply)  z = (sum of overlapping contributions in
 //                               Schwarz-block order) ./ damping, no atomics
 //                               (solvers.py:473-478)
+#include <algorithm>
+
 #include "xdg_common.cuh"
 
 namespace xdg {
@@ -249,9 +251,10 @@ combine_kernel(int nbr, int N, const int* __restrict__ cptr,
   }
 }
 
-// One CTA per system q of a size bucket: packed[q] (P x P) <-> the
-// system's n x n row-major matrix at flat + off[sys[q]].  Pack writes the
-// identity in the padding (rows / columns n..P-1).
+// Systems q of a size bucket on grid x, element ranges on grid y:
+// packed[q] (P x P) <-> the system's n x n row-major matrix at
+// flat + off[sys[q]].  Pack writes the identity in the padding (rows /
+// columns n..P-1).  32-bit index math (P * P < 2^31).
 __global__ void __launch_bounds__(kT)
 pack_square_kernel(int64_t nsys, const int64_t* __restrict__ sys,
                    const int* __restrict__ dims, const int64_t* __restrict__ off, int P,
@@ -261,15 +264,14 @@ pack_square_kernel(int64_t nsys, const int64_t* __restrict__ sys,
     const int n = dims[sq];
     double* src = flat + off[sq];
     double* dst = packed + q * (int64_t)P * P;
-    const int64_t cnt = unpack ? (int64_t)n * n : (int64_t)P * P;
-    for (int64_t k = threadIdx.x; k < cnt; k += kT) {
-      if (unpack) {
-        const int i = (int)(k / n), j = (int)(k % n);
-        src[k] = dst[(int64_t)i * P + j];
-      } else {
-        const int i = (int)(k / P), j = (int)(k % P);
-        dst[k] = (i < n && j < n) ? src[(int64_t)i * n + j] : (i == j ? 1.0 : 0.0);
-      }
+    const int cnt = unpack ? n * n : P * P;
+    const int w = unpack ? n : P;
+    for (int k = blockIdx.y * kT + threadIdx.x; k < cnt; k += kT * gridDim.y) {
+      const int i = k / w, j = k - i * w;
+      if (unpack)
+        src[k] = dst[i * P + j];
+      else
+        dst[k] = (i < n && j < n) ? src[i * n + j] : (i == j ? 1.0 : 0.0);
     }
   }
 }
@@ -362,8 +364,12 @@ extern "C" int xdg_pack_square(int64_t nsys, const int64_t* sys, const int* dims
   XDG_REQUIRE(P >= 1, XDG_ERR_ARG, "bad pad size P=%d", P);
   if (nsys <= 0) return XDG_OK;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  pack_square_kernel<<<grid_for(nsys * kT, kT, 8), kT, 0, s>>>(nsys, sys, dims, off, P,
-                                                              packed, flat, unpack);
+  XDG_REQUIRE((int64_t)P * P < (1LL << 31), XDG_ERR_ARG, "pad size P=%d too large", P);
+  // about 8 elements per thread, at most 65535 parts per system
+  const int64_t parts = std::min<int64_t>(65535, ((int64_t)P * P + 8 * kT - 1) / (8 * kT));
+  const int64_t gx = std::min<int64_t>(nsys, std::max<int64_t>(1, 8 * sm_count() / parts));
+  pack_square_kernel<<<dim3((unsigned)gx, (unsigned)parts), kT, 0, s>>>(nsys, sys, dims, off,
+                                                                      P, packed, flat, unpack);
   XDG_CHECK_LAUNCH();
   return XDG_OK;
 }
