@@ -279,6 +279,13 @@ typedef struct xdg_mf {
   const int32_t* ftask;        /* int4 warp tasks, stage by stage            */
 } xdg_mf;
 
+/* Setup: extend-add of one round of children's Schur complements into
+ * their parents' fronts (pair = 7 int64 per (parent, child): parent base,
+ * parent stride, child base, child stride, child pivot pad, n, U offset).
+ * Replaces the per-child assembly of the factorization SuperLU does inside
+ * splu (cutdg blockmatrix.py:203-227). */
+int xdg_mf_extend_add(int64_t npairs, const int64_t* pair, const int64_t* U,
+                      const double* child, double* parent, xdg_stream_t stream);
 /* Rows per warp task of a front whose rows take a whole warp. */
 int xdg_mf_rows_per_warp(void);
 /* Host-side symbolic analysis (csrc/xdg_ordering.cu).  Nested dissection

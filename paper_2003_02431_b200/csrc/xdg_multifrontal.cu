@@ -443,3 +443,43 @@ extern "C" int xdg_mf_solve(const xdg_mf* mf, const double* b, double* x,
   for (int k = mf->nfbatch - 1; k >= 0; --k) XDG_TRY(launch_fused<false>(mf, k, b, x, s));
   return XDG_OK;
 }
+
+// Setup: extend-add of the children's Schur complements into their parents'
+// fronts, one CTA per (parent, child) pair of one round (the r-th child of
+// every parent: targets are distinct, no atomics; rounds run in child order,
+// so each entry receives its children's terms in the same order as the
+// reference-ordered host loop -- bit-identical).  pair[7q ..] = (parent
+// base, parent stride, child base, child stride, child pivot pad, boundary
+// unknowns n, offset of the pair's n front rows in U).
+namespace xdg {
+namespace {
+__global__ void __launch_bounds__(kT)
+mf_extend_add_kernel(int64_t npairs, const int64_t* __restrict__ pair,
+                     const int64_t* __restrict__ U, const double* __restrict__ child,
+                     double* __restrict__ parent) {
+  for (int64_t q = blockIdx.x; q < npairs; q += gridDim.x) {
+    const int64_t* pq = pair + 7 * q;
+    const int64_t tb = pq[0], ts = pq[1], cb = pq[2], cs = pq[3], cp = pq[4];
+    const int64_t n = pq[5];
+    const int64_t* u = U + pq[6];
+    for (int64_t k = threadIdx.x; k < n * n; k += kT) {
+      const int64_t i = k / n, j = k - i * n;
+      double* d = parent + tb + u[i] * ts + u[j];
+      *d = __dadd_rn(*d, child[cb + (cp + i) * cs + cp + j]);
+    }
+  }
+}
+}  // namespace
+}  // namespace xdg
+
+extern "C" int xdg_mf_extend_add(int64_t npairs, const int64_t* pair, const int64_t* U,
+                                 const double* child, double* parent,
+                                 xdg_stream_t stream) {
+  using namespace xdg;
+  if (npairs <= 0) return XDG_OK;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  mf_extend_add_kernel<<<grid_for(npairs * kT, kT, 8), kT, 0, s>>>(npairs, pair, U, child,
+                                                                   parent);
+  XDG_CHECK_LAUNCH();
+  return XDG_OK;
+}

@@ -33,6 +33,7 @@ SingularSystemError like SuperLU's "exactly singular" (blockmatrix.py:211-215).
 from __future__ import annotations
 
 import ctypes as C
+import os
 import sys
 
 import numpy as np
@@ -469,6 +470,10 @@ class Multifrontal:
             if parent[t] >= 0:
                 last_use[height[t]] = max(last_use[height[t]], height[parent[t]])
         perms = [None] * nn
+        # extend-add on the device (xdg_mf_extend_add) or, XDG_MF_EXTEND=torch
+        # / host plans, by per-child indexed adds (bit-identical)
+        ext_kernel = (ctx is not None and torch.device(dev).type == "cuda"
+                      and os.environ.get("XDG_MF_EXTEND", "kernel") == "kernel")
         bad_nodes, dev_perms = [], []
         for h in range(H):
             hb = [(k, ts) for k, ts in buckets.items() if k[0] == h]
@@ -504,7 +509,10 @@ class Multifrontal:
                 blocks = blocks * sr[:, :, None] * scl[:, None, :]
                 flat[torch.from_numpy(tgt.reshape(-1)).to(dev)] = blocks.reshape(-1)
             # children's Schur complements (extend-add), child by child
-            for t in (t for (_, _, _), ts in hb for t in ts):
+            if ext_kernel:
+                self._extend_add(ctx, hb, kids, bn, pp, fbase, fstride, height, fronts, flat,
+                                 B_list, front_pos, m)
+            for t in (t for (_, _, _), ts in hb for t in ts if not ext_kernel):
                 if not kids[t]:
                     continue
                 Ft = flat[fbase[t]:fbase[t] + fstride[t] ** 2].view(fstride[t], fstride[t])
@@ -707,6 +715,39 @@ class Multifrontal:
                       "plan": time.perf_counter() - t2}
 
     # ------------------------------------------------------------------
+    @staticmethod
+    def _extend_add(ctx, hb, kids, bn, pp, fbase, fstride, height, fronts, flat, B_list,
+                    front_pos, m):
+        """Device extend-add of one height (xdg_mf_extend_add): round r adds
+        the r-th child (kids order, bn > 0) of every parent, one launch per
+        (round, child height)."""
+        groups = {}
+        for t in (t for (_, _, _), ts in hb for t in ts):
+            r = 0
+            for c in kids[t]:
+                if bn[c] == 0:
+                    continue
+                groups.setdefault((r, int(height[c])), []).append((t, c))
+                r += 1
+        dev = flat.device
+        for key in sorted(groups):
+            prs = groups[key]
+            tt = np.array([t for t, _ in prs], np.int64)
+            cc = np.array([c for _, c in prs], np.int64)
+            nodes_ = np.repeat(tt, [len(B_list[c]) for c in cc])
+            verts = np.concatenate([B_list[c] for c in cc])
+            U = (front_pos(nodes_, verts)[:, None] + np.arange(m)[None, :]).reshape(-1)
+            n = bn[cc].astype(np.int64)
+            uoff = np.concatenate([[0], np.cumsum(n)[:-1]])
+            pair = np.stack([fbase[tt], fstride[tt], fbase[cc], fstride[cc], pp[cc], n, uoff],
+                            1).astype(np.int64)
+            pair_d = torch.from_numpy(np.ascontiguousarray(pair)).to(dev)
+            U_d = torch.from_numpy(np.ascontiguousarray(U, np.int64)).to(dev)
+            child = fronts[key[1]]
+            nat.check(ctx.lib.xdg_mf_extend_add(len(prs), pair_d.data_ptr(), U_d.data_ptr(),
+                                                child.data_ptr(), flat.data_ptr(),
+                                                ctx.stream), "mf_extend_add")
+
     def _fused_plan(self, task_arr, lev_task, ent_first, pn, bn, height, parent, order, H):
         """Groups / stages of the fused low levels (XDG_MF_FUSE).  A stage is
         a set of fronts of one height; its gather entries and its warp tasks

@@ -142,3 +142,21 @@ def test_fused_low_levels_bit_identical(case, monkeypatch):
             out.append(SparseDirect(D, ctx).apply(b))
         for o in out[1:]:
             assert torch.equal(out[0], o), (case, lam)
+
+
+@pytest.mark.parametrize("case", ["bench4", "cfg1", "sphere8p3"])
+def test_device_extend_add_bit_identical(case, monkeypatch):
+    """Extend-add by xdg_mf_extend_add (rounds of one child per parent)
+    gives the same factors as the per-child indexed adds: bit-identical
+    solves."""
+    z, meta, hier = load(case)
+    ctx = Context.get()
+    for lam in range(1, hier.num_levels + 1):
+        D = hier.level(lam).matrix.device(ctx)
+        g = torch.Generator(device=ctx.device).manual_seed(lam)
+        b = torch.randn(D.nbr * D.N, dtype=torch.float64, device=ctx.device, generator=g)
+        out = []
+        for mode in ("torch", "kernel"):
+            monkeypatch.setenv("XDG_MF_EXTEND", mode)
+            out.append(SparseDirect(D, ctx).apply(b))
+        assert torch.equal(out[0], out[1]), (case, lam)
