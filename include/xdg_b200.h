@@ -285,7 +285,8 @@ typedef struct xdg_mf {
  * Replaces the per-child assembly of the factorization SuperLU does inside
  * splu (cutdg blockmatrix.py:203-227). */
 int xdg_mf_extend_add(int64_t npairs, const int64_t* pair, const int64_t* U,
-                      const double* child, double* parent, xdg_stream_t stream);
+                      const double* child, double* parent, int64_t max_n,
+                      xdg_stream_t stream);
 /* Rows per warp task of a front whose rows take a whole warp. */
 int xdg_mf_rows_per_warp(void);
 /* Host-side symbolic analysis (csrc/xdg_ordering.cu).  Nested dissection

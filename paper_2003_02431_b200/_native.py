@@ -80,7 +80,7 @@ SIGNATURES = {
     "xdg_schwarz_sizes": (_i32, [_vp]),
     "xdg_schwarz_copy": (_i32, [_vp, _vp, _vp, _vp]),
     "xdg_mf_rows_per_warp": (_i32, []),
-    "xdg_mf_extend_add": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp]),
+    "xdg_mf_extend_add": (_i32, [_i64, _vp, _vp, _vp, _vp, _i64, _vp]),
 }
 
 _lib = None

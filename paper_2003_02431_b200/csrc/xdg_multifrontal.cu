@@ -22,6 +22,8 @@
 // with the symmetric equilibration S folded in (b scaled in F1, x in B2).
 // Bound: HBM -- each apply streams every stored factor once
 // (8 (p^2 + 2 p b) bytes per front); no sequential substitution chains.
+#include <algorithm>
+
 #include "xdg_common.cuh"
 
 namespace xdg {
@@ -460,10 +462,10 @@ mf_extend_add_kernel(int64_t npairs, const int64_t* __restrict__ pair,
   for (int64_t q = blockIdx.x; q < npairs; q += gridDim.x) {
     const int64_t* pq = pair + 7 * q;
     const int64_t tb = pq[0], ts = pq[1], cb = pq[2], cs = pq[3], cp = pq[4];
-    const int64_t n = pq[5];
+    const int n = (int)pq[5];
     const int64_t* u = U + pq[6];
-    for (int64_t k = threadIdx.x; k < n * n; k += kT) {
-      const int64_t i = k / n, j = k - i * n;
+    for (int k = blockIdx.y * kT + threadIdx.x; k < n * n; k += kT * gridDim.y) {
+      const int i = k / n, j = k - i * n;
       double* d = parent + tb + u[i] * ts + u[j];
       *d = __dadd_rn(*d, child[cb + (cp + i) * cs + cp + j]);
     }
@@ -473,13 +475,19 @@ mf_extend_add_kernel(int64_t npairs, const int64_t* __restrict__ pair,
 }  // namespace xdg
 
 extern "C" int xdg_mf_extend_add(int64_t npairs, const int64_t* pair, const int64_t* U,
-                                 const double* child, double* parent,
+                                 const double* child, double* parent, int64_t max_n,
                                  xdg_stream_t stream) {
   using namespace xdg;
   if (npairs <= 0) return XDG_OK;
+  XDG_REQUIRE(max_n * max_n < (1LL << 31), XDG_ERR_ARG, "boundary too large (%lld)",
+              (long long)max_n);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  mf_extend_add_kernel<<<grid_for(npairs * kT, kT, 8), kT, 0, s>>>(npairs, pair, U, child,
-                                                                   parent);
+  // pairs on grid x, element ranges of a pair on grid y (~8 per thread)
+  const int64_t parts = std::min<int64_t>(65535, std::max<int64_t>(
+                                                     1, (max_n * max_n + 8 * kT - 1) / (8 * kT)));
+  const int64_t gx = std::min<int64_t>(npairs, std::max<int64_t>(1, 8 * sm_count() / parts));
+  mf_extend_add_kernel<<<dim3((unsigned)gx, (unsigned)parts), kT, 0, s>>>(npairs, pair, U,
+                                                                        child, parent);
   XDG_CHECK_LAUNCH();
   return XDG_OK;
 }

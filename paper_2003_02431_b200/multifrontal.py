@@ -746,7 +746,7 @@ class Multifrontal:
             child = fronts[key[1]]
             nat.check(ctx.lib.xdg_mf_extend_add(len(prs), pair_d.data_ptr(), U_d.data_ptr(),
                                                 child.data_ptr(), flat.data_ptr(),
-                                                ctx.stream), "mf_extend_add")
+                                                int(n.max()), ctx.stream), "mf_extend_add")
 
     def _fused_plan(self, task_arr, lev_task, ent_first, pn, bn, height, parent, order, H):
         """Groups / stages of the fused low levels (XDG_MF_FUSE).  A stage is
