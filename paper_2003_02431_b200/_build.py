@@ -19,7 +19,10 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = [
     "-O3", "-lineinfo", "-std=c++17", "--shared", "-Xcompiler", "-fPIC",
-    "-Xcompiler", "-O3", "--threads", "0", "-I", os.path.join(ROOT, "include"),
+    "-Xcompiler", "-O3", "--threads", "0",
+    # DT_SONAME: a bare ctypes.CDLL("libxdg_b200.so") (INTEGRATION.md's stub)
+    # resolves to the already loaded in-tree library
+    "-Xlinker", "-soname=libxdg_b200.so", "-I", os.path.join(ROOT, "include"),
 ]
 
 

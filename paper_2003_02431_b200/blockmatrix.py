@@ -70,6 +70,7 @@ class BlockSparseMatrix:
         self._host_fn = None
         self._bsr = None  # (row_ptr, col, val) host arrays, sorted
         self._dev = None
+        self._host_stream = None  # (HostStreamSpMV, pinned x, pinned y)
 
     @property
     def _bsr(self):
@@ -131,6 +132,7 @@ class BlockSparseMatrix:
         else:
             blocks[key] = np.array(block, dtype=float)
         self._dev = None
+        self._host_stream = None
 
     def get_block(self, bi: int, bj: int):
         if self._blocks is None:
@@ -236,26 +238,83 @@ class BlockSparseMatrix:
         return np.concatenate([s + np.arange(n) for s, n in zip(starts, sizes)]) \
             if len(sizes) else np.zeros(0, np.int64)
 
-    def matvec(self, x: np.ndarray) -> np.ndarray:
-        """y = M x on the GPU (blockmatrix.py:119-125); bit-identical to
-        the reference's csr_matvec on tocsr()."""
+    # host vectors above this many rows stream in z-slab chunks (transfers
+    # overlapped with the SpMV); below, one chunk (fewest launches)
+    STREAM_CHUNK_ROWS = 1 << 18
+
+    def _host_streamer(self, D):
+        """Cached HostStreamSpMV + pinned staging buffers of this matrix."""
         import torch
 
-        x = np.asarray(x, dtype=float)
-        if x.shape != (self.shape[1],):
-            raise DimensionMismatchError(
-                f"vector of length {x.shape} against matrix {self.shape}")
+        from .device import HostStreamSpMV
+
+        if self._host_stream is None or self._host_stream[0].D is not D:
+            n = D.nbr * D.N
+            chunks = 8 if n >= self.STREAM_CHUNK_ROWS else 1
+            self._host_stream = (HostStreamSpMV(D, chunks=chunks),
+                                 torch.empty(n, dtype=torch.float64).pin_memory(),
+                                 torch.empty(n, dtype=torch.float64).pin_memory())
+        return self._host_stream
+
+    def matvec(self, x, out=None):
+        """y = M x on the GPU (blockmatrix.py:119-125); bit-identical to
+        the reference's csr_matvec on tocsr().
+
+        numpy in -> numpy out (the reference's contract): x is staged into
+        pinned memory and the product streams host -> device -> host in
+        row chunks, the transfers overlapped with the SpMV
+        (device.HostStreamSpMV).  A pinned CPU torch tensor (optionally
+        with a pinned `out`) skips the staging copies; a CUDA tensor stays
+        on the device (CUDA in -> CUDA out)."""
+        import torch
+
+        if isinstance(x, torch.Tensor):
+            xt = x.reshape(-1)
+            if xt.numel() != self.shape[1] or xt.dtype != torch.float64:
+                raise DimensionMismatchError(
+                    f"vector of length {xt.numel()} ({xt.dtype}) against matrix {self.shape}")
+        else:
+            x = np.asarray(x, dtype=float)
+            if x.shape != (self.shape[1],):
+                raise DimensionMismatchError(
+                    f"vector of length {x.shape} against matrix {self.shape}")
+            xt = None
         if self.row_layout.num_blocks == 0:
-            return np.zeros(0)
+            return np.zeros(0) if xt is None else torch.zeros(0, dtype=torch.float64,
+                                                               device=xt.device)
         D = self.device()
-        if self._dev_pad is None:
-            xd = torch.from_numpy(x).to(D.ctx.device)
-            return D.spmv(xd).cpu().numpy()
-        N = self._dev_pad
-        xp = np.zeros(self.col_layout.num_blocks * N)
-        xp[self._pad_index(self.col_layout, N)] = x
-        y = D.spmv(torch.from_numpy(xp).to(D.ctx.device)).cpu().numpy()
-        return y[self._pad_index(self.row_layout, N)]
+        if self._dev_pad is not None:  # variable layouts: padded vectors
+            N = self._dev_pad
+            xv = xt.cpu().numpy() if xt is not None else x
+            xp = np.zeros(self.col_layout.num_blocks * N)
+            xp[self._pad_index(self.col_layout, N)] = xv
+            y = D.spmv(torch.from_numpy(xp).to(D.ctx.device)).cpu().numpy()
+            y = y[self._pad_index(self.row_layout, N)]
+            return y if xt is None else torch.from_numpy(y).to(xt.device)
+        if xt is not None and xt.is_cuda:
+            return D.spmv(xt, out)
+        if D.nbr != D.nbc:  # rectangular transfer operators: one staged product
+            xd = (xt if xt is not None else torch.from_numpy(x)).to(D.ctx.device)
+            y = D.spmv(xd).cpu()
+            if out is not None:
+                out.copy_(y)
+                return out
+            return y if xt is not None else y.numpy()
+        hs, xh, yh = self._host_streamer(D)
+        if xt is not None and xt.is_pinned():
+            src = xt
+        else:
+            xh.copy_(xt if xt is not None else torch.from_numpy(x))
+            src = xh
+        dst = out if (out is not None and out.is_pinned()) else yh
+        hs(src, dst, sync=True)  # blocks until dst holds the product
+        if xt is None:
+            return dst.numpy().copy() if out is None else out.copy_(dst)
+        if out is not None:
+            if dst is not out:
+                out.copy_(dst)
+            return out
+        return dst.clone()
 
     def transpose(self) -> "BlockSparseMatrix":
         if self._blocks is None:  # array form: one stable sort, no dict

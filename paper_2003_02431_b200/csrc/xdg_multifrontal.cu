@@ -464,8 +464,11 @@ mf_extend_add_kernel(int64_t npairs, const int64_t* __restrict__ pair,
     const int64_t tb = pq[0], ts = pq[1], cb = pq[2], cs = pq[3], cp = pq[4];
     const int n = (int)pq[5];
     const int64_t* u = U + pq[6];
-    for (int k = blockIdx.y * kT + threadIdx.x; k < n * n; k += kT * gridDim.y) {
-      const int i = k / n, j = k - i * n;
+    const int64_t nn = (int64_t)n * n;
+    for (int64_t k = (int64_t)blockIdx.y * kT + threadIdx.x; k < nn;
+         k += (int64_t)kT * gridDim.y) {  // 64-bit counter: no overflow past n^2
+      const int kk = (int)k;
+      const int i = kk / n, j = kk - i * n;
       double* d = parent + tb + u[i] * ts + u[j];
       *d = __dadd_rn(*d, child[cb + (cp + i) * cs + cp + j]);
     }

@@ -264,14 +264,18 @@ pack_square_kernel(int64_t nsys, const int64_t* __restrict__ sys,
     const int n = dims[sq];
     double* src = flat + off[sq];
     double* dst = packed + q * (int64_t)P * P;
-    const int cnt = unpack ? n * n : P * P;
+    const int64_t cnt = unpack ? (int64_t)n * n : (int64_t)P * P;
     const int w = unpack ? n : P;
-    for (int k = blockIdx.y * kT + threadIdx.x; k < cnt; k += kT * gridDim.y) {
-      const int i = k / w, j = k - i * w;
+    // 64-bit loop counter (the stride may step past INT_MAX near the end);
+    // i, j stay 32-bit (k < P * P < 2^31 inside the loop)
+    for (int64_t k = (int64_t)blockIdx.y * kT + threadIdx.x; k < cnt;
+         k += (int64_t)kT * gridDim.y) {
+      const int kk = (int)k;
+      const int i = kk / w, j = kk - i * w;
       if (unpack)
-        src[k] = dst[i * P + j];
+        src[kk] = dst[i * P + j];
       else
-        dst[k] = (i < n && j < n) ? src[i * n + j] : (i == j ? 1.0 : 0.0);
+        dst[kk] = (i < n && j < n) ? src[i * n + j] : (i == j ? 1.0 : 0.0);
     }
   }
 }

@@ -240,9 +240,11 @@ class HostStreamSpMV:
         return len(self.bounds) - 1
 
     def __call__(self, xh: torch.Tensor, yh: torch.Tensor, sync: bool = True) -> torch.Tensor:
-        """Enqueue one product; with sync=False the current stream does not
-        wait for the copies back (call wait() before reading yh) so
-        consecutive products overlap."""
+        """Enqueue one product.  sync=True (default) blocks the host until
+        yh holds the product (the reference's matvec returns a finished
+        array).  sync=False only enqueues: consecutive products overlap,
+        and the caller must call wait() (stream-ordered) and synchronize
+        before reading yh on the host."""
         D, N = self.D, self.D.N
         s_h, s_c, s_d = self.s
         buf = self.step & 1
@@ -271,8 +273,10 @@ class HostStreamSpMV:
                 self.ev_d[buf][k].record(s_d)
         if sync:
             self.wait()
+            s_d.synchronize()  # host-visible: every D2H chunk has landed
         return yh
 
     def wait(self) -> None:
-        """Make the current stream wait for every enqueued copy back."""
+        """Make the current stream wait for every enqueued copy back.
+        Stream-ordered only: it does not block the host."""
         torch.cuda.current_stream(self.D.ctx.device).wait_stream(self.s[2])

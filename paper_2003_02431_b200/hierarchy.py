@@ -108,9 +108,10 @@ def _graph(ptr: np.ndarray, adj: np.ndarray) -> MeshGraph:
     n = len(ptr) - 1
     adjacency = tuple(tuple(int(v) for v in adj[ptr[i]:ptr[i + 1]]) for i in range(n))
     edges = tuple(sorted((a, b) for a in range(n) for b in adjacency[a] if a < b))
-    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(np.asarray(ptr, np.int64)))
+    ptr = np.asarray(ptr, np.int64)
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(ptr))
     return MeshGraph(num_cells=n, edges=edges, adjacency=adjacency,
-                     csr=graph_csr(rows, np.asarray(adj, np.int64)[:len(rows)], n))
+                     csr=graph_csr(rows, np.asarray(adj, np.int64)[ptr[0]:ptr[-1]], n))
 
 
 def fixture_array(z, key: str) -> np.ndarray:

@@ -163,6 +163,9 @@ def _schwarz_partition_native(mesh_graph, nodes, dofs, target: int) -> SchwarzPa
 
     n = nodes.num_nodes
     csr = getattr(mesh_graph, "csr", None)
+    if csr is not None and (len(csr[0]) != n + 1 or int(csr[0][-1]) != sum(
+            len(a) for a in mesh_graph.adjacency)):
+        csr = None  # stale copy (graph rebuilt with another adjacency): flatten
     if csr is not None:  # sorted rows built from the builder's arrays
         ptr, flat = csr
         ptr = np.ascontiguousarray(ptr, np.int64)

@@ -419,9 +419,13 @@ class _OmgContext:
         return fact
 
     def native_levels(self, hierarchy, entry: int):
-        """XdgOmgLevel array for levels entry..last visited (built once)."""
-        if self._native is not None:
-            return self._native
+        """XdgOmgLevel array for levels entry..last visited (built once per
+        hierarchy; a context reused at a lower entry level than the one the
+        cached array was built for gets a rebuilt array -- the reference's
+        context is valid for any level)."""
+        got = self._native
+        if got is not None and got[2] is hierarchy and got[3] <= entry:
+            return got[0], got[1]
         ctx = self._dev
         cfg = self.config
         nl = hierarchy.num_levels
@@ -459,8 +463,8 @@ class _OmgContext:
             L.R, L.Rt = bsr_struct(Rd), bsr_struct(Rtd)
             keep += [Rd, Rtd]
             L.has_restriction = 1
-        self._native = (arr, keep)
-        return self._native
+        self._native = (arr, keep, hierarchy, entry)
+        return arr, keep
 
 
 def ortho_mg_solve(hierarchy, b, x0=None, config: Optional[SolverConfig] = None,

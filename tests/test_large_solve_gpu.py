@@ -95,3 +95,74 @@ def test_converged_solution_true_residual(name):
     print(f"{name}: tracked {rep.final_residual:.3e}  true {res:.3e}")
     assert rep.final_residual <= cfg.tolerance
     assert res <= 1e-8 * np.linalg.norm(b), res
+
+
+@pytest.mark.parametrize("name", ["s16p3", "cfg2"])
+def test_gmres_pmg_full_size_true_residual_and_omg_agreement(name):
+    """Full-size GMRES(50)-PMG (k_lo = 2; the cfg2 global low-order system
+    is the 336,610-unknown multifrontal factor): converged, its true
+    residual recomputed with the oracle SpMV (bit-identical to the
+    reference matvec) at the tolerance's roundoff floor, and the solution
+    equal to the converged OMG solution to 1e-8 (both solve the same
+    system to an absolute residual of 1e-10)."""
+    from oracle import spmv
+    from paper_2003_02431_b200.hierarchy import fixture_array, load_hierarchy
+    from paper_2003_02431_b200.solvers import SolverConfig, gmres_pmg_solve, ortho_mg_solve
+
+    z = fixture(name)
+    meta = json.loads(bytes(z["meta"]).decode())
+    hier = load_hierarchy(z)
+    lv = hier.level(1)
+    b = np.asarray(lv.rhs)
+    gcfg = dict(meta["gmres"], max_iterations=20000)
+    xg, rg = gmres_pmg_solve(lv.matrix, b, SolverConfig(**gcfg), dim=meta["dim"])
+    assert rg.converged and rg.final_residual <= gcfg["tolerance"]
+    assert rg.residual_history[-1] == rg.final_residual
+    r = b - spmv.bsr_spmv(z["L1_row_ptr"], z["L1_col"], fixture_array(z, "L1_val"), xg,
+                          spmv.max_threads())
+    assert np.linalg.norm(r) <= 1e-8 * np.linalg.norm(b)
+    xo, ro = ortho_mg_solve(hier, b, None, SolverConfig(**meta["omg"]), 1)
+    assert ro.converged
+    d = np.linalg.norm(xg - xo) / np.linalg.norm(xo)
+    print(f"{name}: gmres {rg.iterations} it, omg {ro.iterations} it, |xg - xo|/|xo| = {d:.3e}")
+    assert d <= 1e-8
+
+
+def test_cfg2_low_order_multifrontal_backward_error():
+    """The cfg2 GMRES-PMG global low-order system (33,661 blocks x 10 modes
+    = 336,610 unknowns, k_lo = 2) factored by the device multifrontal LU:
+    b = A x_true with the oracle SpMV, x = xdg_mf_solve(b); normwise
+    backward error <= 1e-14 and forward error bounded like a
+    partial-pivoting LU's (eps cond(A))."""
+    import torch
+
+    from oracle import spmv
+    from paper_2003_02431_b200.device import Context, DeviceBSR
+    from paper_2003_02431_b200.direct import SparseDirect
+    from paper_2003_02431_b200.hierarchy import fixture_array
+
+    z = fixture("cfg2")
+    rp, col = z["L1_row_ptr"], z["L1_col"]
+    m = 10  # modes_low(k_lo=2, dim=3)
+    val = np.ascontiguousarray(fixture_array(z, "L1_val")[:, :m, :m])
+    nb = len(rp) - 1
+    assert nb * m == 336_610
+    ctx = Context.get()
+    D = DeviceBSR.from_arrays(rp, col, val, m, nb, ctx)
+    sd = SparseDirect(D, ctx)
+    rng = np.random.default_rng(7)
+    x_true = rng.standard_normal(nb * m)
+    b = spmv.bsr_spmv(rp, col, val, x_true, spmv.max_threads())
+    got = sd.apply(torch.from_numpy(b).to(ctx.device)).cpu().numpy()
+    r = b - spmv.bsr_spmv(rp, col, val, got, spmv.max_threads())
+    a_inf = np.abs(val).sum(axis=2)  # row sums of |A| per block row
+    rows = np.repeat(np.arange(nb), np.diff(rp))
+    rowsum = np.zeros((nb, m))
+    np.add.at(rowsum, rows, a_inf)
+    norm_a = rowsum.max()
+    berr = np.abs(r).max() / (norm_a * np.abs(got).max() + np.abs(b).max())
+    ferr = np.linalg.norm(got - x_true) / np.linalg.norm(x_true)
+    print(f"cfg2 low-order: n = {nb * m}, factor {sd.mf.factor_bytes / 1e9:.2f} GB, "
+          f"backward {berr:.3e}, forward {ferr:.3e}")
+    assert berr <= 1e-14, berr
+    assert ferr <= 1e-6, ferr
