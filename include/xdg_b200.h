@@ -164,6 +164,28 @@ int xdg_lu_inv_apply_tasks(int64_t ntasks, const int* task_sys,
                            const int64_t* vec_off, const double* INV,
                            const int* src, const double* b, double* x,
                            double* scratch, xdg_stream_t stream);
+/* ---- batched dense factorization (setup, xdg_factor.cu) --------------- */
+/* Partial-pivoting LU of a batch of row-major matrices of any sizes, in
+ * place: matrix b at A + off[b] (elements), leading dimension ld[b],
+ * n[b] x n[b], its first p[b] <= n[b] columns eliminated with pivots chosen
+ * among its first p[b] rows (p = n: a full LU; p < n: a multifrontal front,
+ * leaving L_BP = F_BP U^-1, U_PB = L^-1 P F_PB and the Schur complement
+ * F_BB - L_BP U_PB in place).  max_n / max_p bound n[b] / p[b] (grid
+ * sizing).  perm[perm_off[b] + i] (i < p[b]) = original row at position i
+ * ((P b)[i] = b[perm[i]]); info[b] = 1 + first column with a zero or
+ * non-finite pivot, 0 if none (the caller raises SingularSystemError).
+ * invert != 0: the top-left p x p LU is replaced by the triangular
+ * inverses xdg_lu_inv_apply reads (L^-1 strictly below the diagonal, U^-1
+ * on and above), using ws (xdg_batched_factor_ws_bytes(nmat, max_p)).
+ * nmat < 65536 per call.
+ * Replaces scipy lu_factor (cutdg solvers.py:233), SuperLU splu
+ * (blockmatrix.py:213) and the dense factor of direct_factor
+ * (blockmatrix.py:203-216) -- SURVEY 8(b)'s xdg_batched_factor. */
+int xdg_batched_factor(int64_t nmat, const int64_t* off, const int* n,
+                       const int* p, const int* ld, int max_n, int max_p,
+                       double* A, int* perm, const int64_t* perm_off, int* info,
+                       int invert, double* ws, xdg_stream_t stream);
+int64_t xdg_batched_factor_ws_bytes(int64_t nmat, int max_p);
 /* LAPACK ipiv (1-based sequential swaps) -> permutation perm with
  * (P^T b)[i] = b[perm[i]], per system (setup). */
 int xdg_ipiv_to_perm(int nsys, const int* dims, const int64_t* vec_off,

@@ -29,9 +29,6 @@ class Context:
     def __init__(self, device: torch.device):
         self.device = device
         self.lib = nat.load()
-        # setup factorizations through cuSOLVER (MAGMA's batched getrf prints
-        # advisory banners to stdout and is slower at these sizes)
-        torch.backends.cuda.preferred_linalg_library("cusolver")
         with torch.cuda.device(device):
             nb = int(self.lib.xdg_reduce_workspace_bytes())
             self._ws = torch.zeros((nb + 7) // 8, dtype=F64, device=device)

@@ -37,10 +37,10 @@ from .direct import (
     DeviceDirect,
     SparseDirect,
     dense_from_device_bsr,
-    ipiv_to_perm,
 )
 from .distributed import DistributedSpMV, HaloPlan
 from .errors import SingularSystemError
+from .factor import batched_factor
 from .solvers import SolverConfig, SolverReport, space_dimension
 
 F64 = torch.float64
@@ -156,18 +156,17 @@ class DistPmg:
             nat.check(ctx.lib.xdg_pmg_gather_high(
                 nloc, N, m, up(np.arange(nloc), I32).data_ptr(), up(diag_k, I32).data_ptr(),
                 op.D.val_t.data_ptr(), H.data_ptr(), ctx.stream), "pmg_gather_high")
-            LUh, pvh, _ = torch.linalg.lu_factor_ex(H.view(nloc, nh, nh))
-            dg = torch.diagonal(LUh, dim1=-2, dim2=-1)
-            bad = (~torch.isfinite(LUh).flatten(1).all(1)) | (dg == 0).any(1)
-            if bool(bad.any()):
-                c = op.r0 + int(torch.nonzero(bad)[0])
+            hoff = np.arange(nloc, dtype=np.int64) * nh
+            hperm, _, info = batched_factor(ctx, H, hoff * nh, np.full(nloc, nh, np.int32),
+                                            invert=False, perm_off=hoff)
+            bad = torch.nonzero(info[:nloc])
+            if bad.numel():
+                c = op.r0 + int(bad[0])
                 raise SingularSystemError(f"high-order block of cell {c} is singular")
             self.HLU = torch.empty_like(H)
-            nat.check(ctx.lib.xdg_blocks_transpose(nloc, nh, LUh.contiguous().data_ptr(),
+            nat.check(ctx.lib.xdg_blocks_transpose(nloc, nh, H.data_ptr(),
                                                    self.HLU.data_ptr(), ctx.stream), "transpose")
-            self.hperm = ipiv_to_perm(ctx, pvh.to(I32).contiguous(),
-                                      torch.full((nloc,), nh, dtype=I32, device=dev),
-                                      torch.arange(nloc, dtype=torch.int64, device=dev) * nh)
+            self.hperm = hperm
             self.wi_ptr = op.D.row_ptr
             self.wi_blk = torch.arange(op.D.nnzb, dtype=I32, device=dev)
             self.wi_lcol = up(op.gcol, I32)                  # global cell -> xlo

@@ -40,7 +40,7 @@ import numpy as np
 import torch
 
 from . import _native as nat
-from .direct import lu_factor_batched, triangular_inverses
+from .factor import batched_factor
 from .errors import SingularSystemError
 
 F64 = torch.float64
@@ -345,7 +345,7 @@ class Multifrontal:
 
     def __init__(self, ctx, rp, col, val_t, N, sets, m, vsrc, vdst,
                  leaf_unknowns: int = 100, what: str = "system",
-                 equilibrate: bool = True):
+                 equilibrate: bool = True, front_factor=None):
         import time
 
         t0 = time.perf_counter()
@@ -532,34 +532,33 @@ class Multifrontal:
                 nb = len(ts)
                 n_ = P_ + B_
                 Fb = flat[fbase[ts[0]]:fbase[ts[0]] + nb * n_ * n_].view(nb, n_, n_)
-                A = Fb[:, :P_, :P_].contiguous()
                 if P_ == 0:
                     continue
-                LU, piv, info = (lu_factor_batched(A) if A.is_cuda
-                                 else torch.linalg.lu_factor_ex(A))
-                dg = torch.diagonal(LU, dim1=-2, dim2=-1)
-                bad = (info != 0) | ~torch.isfinite(LU).flatten(1).all(1) | (dg == 0).any(1)
-                perm = _ipiv_to_perm(ctx, piv.to(I32).contiguous(), P_)
+                # partial LU of every front of the bucket in place
+                # (xdg_batched_factor, p = P_ of n = P_ + B_ columns): L_BP,
+                # U_PB, the Schur complement for the parent and the
+                # triangular inverses of the pivot block, no library calls
+                if front_factor is not None:  # CPU planning tests (tests/mf_emulation.py)
+                    perm, bad = front_factor(Fb, P_)
+                else:
+                    foff = fbase[ts[0]] + np.arange(nb, dtype=np.int64) * n_ * n_
+                    perm, _, info = batched_factor(
+                        ctx, flat, foff, np.full(nb, n_, np.int32),
+                        np.full(nb, P_, np.int32), invert=True,
+                        perm_off=np.arange(nb, dtype=np.int64) * P_)
+                    perm = perm[:nb * P_].view(nb, P_)
+                    bad = info[:nb] != 0
                 if B_:
-                    FPB = Fb[:, :P_, P_:]
-                    PF = torch.gather(FPB, 1, perm.long()[:, :, None].expand(nb, P_, B_))
-                    UPB = torch.linalg.solve_triangular(LU, PF, upper=False,
-                                                        unitriangular=True)
-                    LBP = torch.linalg.solve_triangular(LU, Fb[:, P_:, :P_].contiguous(),
-                                                        upper=True, left=False)
-                    Fb[:, P_:, P_:] -= torch.bmm(LBP, UPB)
+                    LBP = Fb[:, P_:, :P_]
                     bad |= ~torch.isfinite(LBP).flatten(1).all(1)
                     o = int(lbp_off[ts[0]])
-                    self.F[o:o + nb * B_ * P_] = LBP.reshape(-1)
+                    self.F[o:o + nb * B_ * P_].view(nb, B_, P_).copy_(LBP)
                     o = int(upb_off[ts[0]])
-                    self.F[o:o + nb * P_ * B_] = UPB.reshape(-1)
-                    del FPB, PF, UPB, LBP
-                INV = triangular_inverses(LU)
+                    self.F[o:o + nb * P_ * B_].view(nb, P_, B_).copy_(Fb[:, :P_, P_:])
                 o = int(inv_off[ts[0]])
-                self.F[o:o + nb * P_ * P_] = INV.reshape(-1)
+                self.F[o:o + nb * P_ * P_].view(nb, P_, P_).copy_(Fb[:, :P_, :P_])
                 bad_nodes.append((ts, bad))
                 dev_perms.append((ts, perm))  # read back once, after all heights
-                del LU, INV, A
             for hh in range(h + 1):
                 if hh in fronts and last_use[hh] <= h:
                     del fronts[hh]

@@ -21,7 +21,7 @@ import numpy as np
 import torch
 
 from . import _native as nat
-from .direct import ipiv_to_perm, lu_factor_batched, triangular_inverses
+from .factor import batched_factor, buckets_by_size
 from .errors import SingularSystemError
 
 F64 = torch.float64
@@ -159,7 +159,7 @@ class PmgPlan:
         # ---- low-order dense factors (solvers.py:208-221) ----------------
         need = 8 * int(lu_off[-1])
         free, _ = torch.cuda.mem_get_info(dev)
-        if need + (8 << 30) > free:  # factors + chunk temporaries (<= 2 GB each)
+        if need + (3 << 30) > free:  # factors (in place) + the <= 2 GB sweep workspace
             raise NotImplementedError(
                 f"dense low-order factors need {need / 1e9:.1f} GB (largest system "
                 f"{int(dims.max())} unknowns; {free / 1e9:.0f} GB free): use the "
@@ -171,53 +171,26 @@ class PmgPlan:
             self.wi_lrow.data_ptr(), self.wi_sys.data_ptr(),
             self.lu_off.data_ptr(), self.dims.data_ptr(), D.val_t.data_ptr(),
             A.data_ptr(), ctx.stream), "pmg_build_low")
-        piv = torch.zeros(int(vec_off[-1]), dtype=I32, device=dev)
-        # factor the systems in size buckets: each bucket is padded with
-        # identity to a common size P (the LU / triangular inverses of
-        # diag(A, I) are diag(LU_A, I) -- padding rows hold zeros in A's
-        # columns so partial pivoting never selects them), batched (MAGMA
-        # for batches >= 4), and the top-left n x n blocks copied back.  One
-        # deferred singularity check for all systems.
-        bad_flags = torch.zeros(self.nsys, dtype=torch.bool, device=dev)
-        # small systems padded to multiples of 16 (few buckets: every bucket
-        # is one batched-getrf call with a fixed cost), larger ones to 128
-        pad_to = np.where(dims <= 64, ((dims + 15) // 16) * 16, ((dims + 127) // 128) * 128)
-        for P in np.unique(pad_to):
-            idx = np.flatnonzero(pad_to == P)
-            P = int(P)
-            if P == 0:
+        # factor every system in place (xdg_batched_factor: partial-pivoting
+        # LU, then the triangular inverses the solve kernels read), one call
+        # per size bucket; permutations land at the systems' vector offsets.
+        # One deferred singularity check for all systems.
+        perm = torch.zeros(max(int(vec_off[-1]), 1), dtype=I32, device=dev)
+        infos = []
+        for idx in buckets_by_size(dims):
+            idx = idx[dims[idx] > 0]
+            if not len(idx):
                 continue
-            for c0 in range(0, len(idx), max(1, (1 << 31) // (8 * P * P))):
-                chunk = idx[c0:c0 + max(1, (1 << 31) // (8 * P * P))]
-                chunk_d = torch.from_numpy(np.ascontiguousarray(chunk, np.int64)).to(dev)
-                batch = torch.empty(len(chunk), P, P, dtype=F64, device=dev)
-                nat.check(ctx.lib.xdg_pack_square(
-                    len(chunk), chunk_d.data_ptr(), self.dims.data_ptr(),
-                    self.lu_off.data_ptr(), P, batch.data_ptr(), A.data_ptr(), 0,
-                    ctx.stream), "pack_square")
-                LU, pv, info = lu_factor_batched(batch)
-                dg = torch.diagonal(LU, dim1=-2, dim2=-1)
-                bad = (info != 0) | ~torch.isfinite(LU).flatten(1).all(1) | (dg == 0).any(1)
-                bad_flags.index_copy_(0, chunk_d, bad)
-                INV = triangular_inverses(LU).contiguous()
-                nat.check(ctx.lib.xdg_pack_square(
-                    len(chunk), chunk_d.data_ptr(), self.dims.data_ptr(),
-                    self.lu_off.data_ptr(), P, INV.data_ptr(), A.data_ptr(), 1,
-                    ctx.stream), "unpack_square")
-                # pivots of the leading n rows of every system
-                nq = dims[chunk]
-                q_of = np.repeat(np.arange(len(chunk)), nq)
-                i_of = _ranges(np.zeros(len(chunk), np.int64), nq)
-                dst = torch.from_numpy(vec_off[chunk][q_of] + i_of).to(dev)
-                srcp = torch.from_numpy(q_of * P + i_of).to(dev)
-                piv[dst] = pv.reshape(-1)[srcp].to(I32)
-                del batch, LU, INV
-        if bool(bad_flags.any()):
-            s_bad = int(torch.nonzero(bad_flags)[0])
-            cells = tuple(int(c) for c in sets[s_bad][:8])
-            raise SingularSystemError(f"low-order system on cells {cells}... is singular")
+            _, _, info = batched_factor(ctx, A, lu_off[idx], dims[idx], invert=True,
+                                        perm=perm, perm_off=vec_off[idx])
+            infos.append((idx, info[:len(idx)]))
+        for idx, info in infos:
+            bad = torch.nonzero(info)
+            if bad.numel():
+                cells = tuple(int(c) for c in sets[int(idx[int(bad[0])])][:8])
+                raise SingularSystemError(f"low-order system on cells {cells}... is singular")
         self.LU = A
-        perm = ipiv_to_perm(ctx, piv, self.dims, self.vec_off).long()
+        perm = perm[:int(vec_off[-1])].long()
         # src = global DOF of local low unknown perm[i]:  cell*N + mode
         gidx = torch.from_numpy(
             np.concatenate([np.repeat(S * N, self.m) + np.tile(np.arange(self.m), len(S))
@@ -257,19 +230,21 @@ class PmgPlan:
                 len(ucells), N, self.m, up(ucells, I32).data_ptr(),
                 up(diag_k[ucells], I32).data_ptr(), D.val_t.data_ptr(),
                 H.data_ptr(), ctx.stream), "pmg_gather_high")
-            LUh, pvh, info = torch.linalg.lu_factor_ex(H.view(len(ucells), nh, nh))
-            dg = torch.diagonal(LUh, dim1=-2, dim2=-1)
-            bad = (~torch.isfinite(LUh).flatten(1).all(1)) | (dg == 0).any(1)
-            if bool(bad.any()):
-                c = int(ucells[int(torch.nonzero(bad)[0])])
+            # per-cell partial-pivoting LU in place (xdg_batched_factor; the
+            # reference's scipy lu_factor, solvers.py:233), column-major copy
+            # for the warp-per-cell solve
+            nu = len(ucells)
+            hoff = np.arange(nu, dtype=np.int64) * nh
+            hperm, _, info = batched_factor(ctx, H, hoff * nh, np.full(nu, nh, np.int32),
+                                            invert=False, perm_off=hoff)
+            bad = torch.nonzero(info[:nu])
+            if bad.numel():
+                c = int(ucells[int(bad[0])])
                 raise SingularSystemError(f"high-order block of cell {c} is singular")
             self.HLU = torch.empty_like(H)
             nat.check(ctx.lib.xdg_blocks_transpose(
-                len(ucells), nh, LUh.contiguous().data_ptr(), self.HLU.data_ptr(),
-                ctx.stream), "blocks_transpose(H)")
-            hdims = torch.full((len(ucells),), nh, dtype=I32, device=dev)
-            hoff = torch.arange(len(ucells), dtype=I64, device=dev) * nh
-            self.hperm = ipiv_to_perm(ctx, pvh.to(I32).contiguous(), hdims, hoff)
+                nu, nh, H.data_ptr(), self.HLU.data_ptr(), ctx.stream), "blocks_transpose(H)")
+            self.hperm = hperm
             hidx = np.full(nbr, -1, np.int64)
             hidx[ucells] = np.arange(len(ucells))
             self.wi_hidx = up(hidx[wcell], I32)

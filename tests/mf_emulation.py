@@ -2,6 +2,45 @@
 INFRASTRUCTURE ONLY: lets the CPU suite check the multifrontal symbolic and
 numeric factorization (multifrontal.py) without a GPU."""
 import numpy as np
+import scipy.linalg as sla
+import torch
+
+
+def front_factor_cpu(Fb, P):
+    """The xdg_batched_factor front contract on CPU tensors (test checker):
+    partial-pivoting LU of the first P columns of each (P+B)^2 front in
+    place, the triangular inverses of the pivot block, L_BP, U_PB and the
+    Schur complement; returns (perm (nb, P), bad flags)."""
+    nb = Fb.shape[0]
+    perms = np.zeros((nb, P), np.int64)
+    bad = np.zeros(nb, bool)
+    for q in range(nb):
+        F = Fb[q].numpy()  # a view: in place
+        import warnings
+
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            lu, piv = sla.lu_factor(F[:P, :P].copy(), check_finite=False)
+        pr = np.arange(P)
+        for i, k in enumerate(piv):
+            pr[[i, k]] = pr[[k, i]]
+        perms[q] = pr
+        d = np.diag(lu)
+        bad[q] = (not np.all(np.isfinite(lu))) or np.any(d == 0)
+        if bad[q]:
+            continue
+        L = np.tril(lu, -1) + np.eye(P)
+        U = np.triu(lu)
+        if F.shape[0] > P:
+            UPB = sla.solve_triangular(L, F[:P, P:][pr], lower=True, unit_diagonal=True)
+            LBP = sla.solve_triangular(U, F[P:, :P].T, trans="T").T
+            F[P:, P:] -= LBP @ UPB
+            F[:P, P:] = UPB
+            F[P:, :P] = LBP
+        Li = sla.solve_triangular(L, np.eye(P), lower=True, unit_diagonal=True)
+        Ui = sla.solve_triangular(U, np.eye(P))
+        F[:P, :P] = np.tril(Li, -1) + np.triu(Ui)
+    return torch.from_numpy(perms), torch.from_numpy(bad)
 
 
 def emulate_solve(mf, b, xlen):

@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 import torch
 
-from mf_emulation import emulate_solve
+from mf_emulation import emulate_solve, front_factor_cpu
 from paper_2003_02431_b200.errors import SingularSystemError
 from paper_2003_02431_b200.multifrontal import Multifrontal, SystemGraph, nested_dissection
 
@@ -53,7 +53,7 @@ def build(rp, col, vals, N, sets, m, leaf=9):
         off += len(S) * m
     val_t = torch.from_numpy(np.ascontiguousarray(vals.transpose(0, 2, 1)))
     mf = Multifrontal(None, rp, col, val_t, N, sets, m, np.concatenate(vsrc),
-                      np.concatenate(vdst), leaf_unknowns=leaf)
+                      np.concatenate(vdst), leaf_unknowns=leaf, front_factor=front_factor_cpu)
     return mf, off
 
 

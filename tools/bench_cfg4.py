@@ -18,7 +18,8 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2003_02431_b200 import solvers as S  # noqa: E402
 from paper_2003_02431_b200.case import BenchCase, assemble_case  # noqa: E402
-from paper_2003_02431_b200.direct import lu_factor_dense  # noqa: E402
+from paper_2003_02431_b200.device import Context  # noqa: E402
+from paper_2003_02431_b200.factor import warmup  # noqa: E402
 from paper_2003_02431_b200.solvers import (  # noqa: E402
     SolverConfig, gmres_pmg_solve, ortho_mg_solve)
 
@@ -40,8 +41,7 @@ print(json.dumps({"case": f"cfg4 {cells}^3 p=2 (native setup)", "setup_s": round
                   "level_blocks": [hier.level(i).data.num_blocks
                                    for i in range(1, hier.num_levels + 1)],
                   "nnzb_level1": int(lv.matrix.device().nnzb)}), flush=True)
-eye = torch.eye(64, dtype=torch.float64, device="cuda")
-lu_factor_dense(eye)
+warmup(Context.get())
 torch.cuda.synchronize()
 meta = {"omg": {"tolerance": 1e-10, "max_iterations": 3000, "k_lo": 1, "num_levels": 4},
         "gmres": {"tolerance": 1e-10, "max_iterations": 6000, "k_lo": 1, "gmres_restart": 50}}

@@ -16,7 +16,8 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2003_02431_b200.blockmatrix import BlockSparseMatrix, uniform_layout  # noqa: E402
 from paper_2003_02431_b200.device import Context  # noqa: E402
-from paper_2003_02431_b200.direct import lu_factor_dense  # noqa: E402
+from paper_2003_02431_b200.device import Context  # noqa: E402
+from paper_2003_02431_b200.factor import warmup  # noqa: E402
 from paper_2003_02431_b200.hierarchy import fixture_array  # noqa: E402
 from paper_2003_02431_b200.multifrontal import Multifrontal  # noqa: E402
 
@@ -30,7 +31,7 @@ N, nb = val.shape[1], len(rp) - 1
 M = BlockSparseMatrix.from_bsr(rp, col, val, uniform_layout(nb, N), uniform_layout(nb, N))
 ctx = Context.get()
 D = M.device(ctx)
-lu_factor_dense(torch.eye(64, dtype=torch.float64, device="cuda"))
+warmup(Context.get())
 v = np.arange(nb, dtype=np.int64)
 Multifrontal(ctx, rp, col, D.val_t, N, [v], m, v * N, v * m)  # warm (MAGMA, kernels)
 torch.cuda.synchronize()

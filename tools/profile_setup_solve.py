@@ -43,8 +43,9 @@ cfgd = dict(meta[solver])
 cfgd["max_iterations"] = 1
 cfg = SolverConfig(**cfgd)
 # warm-up (module loads, cuSOLVER/MAGMA handles) on a tiny system
-from paper_2003_02431_b200.direct import lu_factor_dense  # noqa: E402
-lu_factor_dense(torch.eye(64, dtype=torch.float64, device="cuda"))
+from paper_2003_02431_b200.device import Context  # noqa: E402
+from paper_2003_02431_b200.factor import warmup  # noqa: E402
+warmup(Context.get())
 torch.cuda.synchronize()
 pr = cProfile.Profile()
 t0 = time.perf_counter()
