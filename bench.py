@@ -160,18 +160,38 @@ def cpu_spmv_sample(n_sample: int, seconds: float, threads: int):
                 seconds=t, reps=len(times))
 
 
+def _ref_size(args) -> tuple:
+    """Full workload size for the reference arm when the host can hold the
+    BSR operator (12.4 GB at 128^3, ~3x that while the recipe builds it),
+    else the bounded sample; returns (n, why)."""
+    try:
+        import psutil
+
+        avail = psutil.virtual_memory().available
+    except Exception:  # noqa: BLE001
+        avail = 0
+    need = 3.2 * 12.4e9 * (args.n / 128) ** 3
+    if avail >= need:
+        return args.n, f"full {args.n}^3 operator ({avail / 1e9:.0f} GB host RAM available)"
+    return args.ref_sample, (f"bounded {args.ref_sample}^3 sample: the {args.n}^3 operator "
+                             f"needs ~{need / 1e9:.0f} GB host RAM to build, "
+                             f"{avail / 1e9:.0f} GB available")
+
+
 def run_reference(args):
     """The reference's CPU path (oracle C restatement of scipy csr_matvec over
-    tocsr(), all host threads) on a bounded sample of the workload: each of
-    the K timed steps is a batch of SpMVs on the seeded n^3 sample sized to
-    ~0.5 s; W untimed warm-up steps."""
+    tocsr(), all host threads) on the same workload: the full 128^3
+    operator when host RAM allows (same_config), else a bounded sample;
+    each of the K timed steps is a batch of SpMVs of >= 0.5 s; W untimed
+    warm-up steps."""
     world, rank, _ = dist_env()
     if world > 1 and rank != 0:
         return
     from oracle import cfg3, spmv
 
     threads = spmv.max_threads()
-    rp, col, val, x = cfg3.build(args.ref_sample)
+    n_ref, why = _ref_size(args)
+    rp, col, val, x = cfg3.build(n_ref)
     nbr, N, nnzb = len(rp) - 1, val.shape[1], len(col)
     B = 8 * N * N * nnzb + 4 * nnzb + 4 * (nbr + 1) + 16 * nbr * N
     t0 = time.perf_counter()
@@ -188,8 +208,9 @@ def run_reference(args):
     wall = time.perf_counter() - t0
     ms_per_step = 1e3 * wall / args.steps
     value = B * reps * args.steps / wall / 1e9
-    sample = (f"cfg3 recipe at {args.ref_sample}^3 ({nbr} block rows, {nnzb} blocks, "
-              f"{B / 1e9:.3f} GB/SpMV); one step = {reps} SpMVs; oracle/bsr_spmv.c "
+    same = n_ref == args.n
+    sample = (f"cfg3 recipe at {n_ref}^3 ({nbr} block rows, {nnzb} blocks, "
+              f"{B / 1e9:.3f} GB/SpMV; {why}); one step = {reps} SpMV(s); oracle/bsr_spmv.c "
               f"(scipy csr_matvec order) on {threads} host threads")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
@@ -197,8 +218,11 @@ def run_reference(args):
         "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (SURVEY 8(d) cfg3 recipe, seed 0)",
-        "config": {"workload": f"cfg3 block-MSR SpMV, bounded sample {args.ref_sample}^3 "
-                               f"of the {args.n}^3 operator", "N": 10, "cut_fraction": 0.05},
+        "config": {"workload": (f"BASELINE cfg3: block-MSR SpMV {args.n}^3 cells, p=2 (N=10), "
+                                f"5% cut, {nbr} block rows, {nnzb} blocks") if same else
+                               (f"cfg3 block-MSR SpMV, bounded sample {n_ref}^3 of the "
+                                f"{args.n}^3 operator"),
+                   "N": 10, "cut_fraction": 0.05, "same_config": same},
         "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0,
@@ -214,6 +238,29 @@ CFG2_META = {  # BASELINE config 2: 32^3, p=3, sphere r=0.6, mu 1/
     "omg": {"tolerance": 1e-10, "max_iterations": 2000, "k_lo": 2, "rm_max_columns": 800,
             "num_levels": 3},
     "gmres": {"tolerance": 1e-10, "max_iterations": 10000, "k_lo": 2, "gmres_restart": 50}}
+
+
+def oracle_cfg2_box_estimate(solver: str, iterations: int, dofs_raw: int):
+    """cpu_baseline of a cfg2 solve row: the CPU oracle (reference-exact
+    numpy/scipy restatement) timed on the GPU box's host by
+    tools/time_oracle_cfg2.py (1 and 3 iterations, first one with the lazy
+    factorizations), extrapolated to the GPU's iteration count."""
+    path = os.path.join(ROOT, "tests", "golden", "oracle_cfg2_timing_box.json")
+    if not os.path.exists(path):
+        return None
+    t = json.load(open(path))
+    k = "omg" if solver == "omg" else "gmres"
+    if f"{k}_1it_s" not in t or f"{k}_3it_s" not in t:
+        return None
+    first, per = t[f"{k}_1it_s"], (t[f"{k}_3it_s"] - t[f"{k}_1it_s"]) / 2
+    est = first + max(iterations - 1, 0) * per
+    return {"value": dofs_raw / est, "unit": "DOF/s", "cores": t.get("cores"), "kind": "port",
+            "sample": (f"oracle/solvers_np.py on the GPU box host ({t.get('cpu')}), "
+                       f"1 and 3 iterations timed ({first:.1f} s incl. lazy factorizations, "
+                       f"{per:.2f} s/iteration), extrapolated to {iterations} iterations = "
+                       f"{est:.0f} s; tests/golden/oracle_cfg2_timing_box.json "
+                       f"(tools/time_oracle_cfg2.py)"),
+            "seconds_extrapolated": est}
 
 
 def reference_cfg2_estimate(solver: str, iterations: int):
@@ -263,6 +310,23 @@ def native_cfg2(world: int = 1):
            "reference_setup_source": "tests/golden/make_large.py cfg2 (cutdg assemble_case, "
                                      "1 host thread)"}
     return asm.hierarchy, meta, row
+
+
+def ref_envelope(case, z, solver, meta):
+    """[min, max] iterations of the reference under +-1-ulp perturbations of
+    b: the K = 20-40 run envelope of {case}_env.npz at
+    the solve's tolerance when present, else the fixture's K = 5 one."""
+    tol = meta[solver].get("tolerance", 1e-10)
+    p = os.path.join(ROOT, "tests", "golden", f"{case}_env.npz")
+    key = f"{solver}_tol{tol:.0e}"
+    if os.path.exists(p):
+        e = np.load(p)
+        if key in e.files:
+            return {"min": int(e[key].min()), "max": int(e[key].max()), "runs": int(len(e[key]))}
+    if f"{solver}_envelope" in z:
+        e = z[f"{solver}_envelope"]
+        return {"min": int(e.min()), "max": int(e.max()), "runs": int(len(e))}
+    return None
 
 
 def time_solves(torch, budget_s: float):
@@ -329,18 +393,22 @@ def time_solves(torch, budget_s: float):
             ref_extrap = None
             if case.endswith("cfg2") or case.startswith("cfg2"):
                 ref_extrap = reference_cfg2_estimate(solver, rep.iterations)
-            cpu_here = None
+            cpu_here, cpu_base = None, None
             if case == "cfg1":  # bounded: ~10 s of CPU per solver
                 from oracle import solvers_np
 
                 _, cpu_it, cpu_here = solvers_np.timed_solve(z, meta, solver)
+                cpu_base = {"value": meta["dofs_raw"] / cpu_here, "unit": "DOF/s",
+                            "cores": os.cpu_count(), "kind": "port",
+                            "sample": (f"full cfg1 solve ({cpu_it} iterations) by "
+                                       f"oracle/solvers_np.py on this host, timed live")}
+            elif "cfg2" in case:
+                cpu_base = oracle_cfg2_box_estimate(solver, rep.iterations, meta["dofs_raw"])
             out.append({
                 "case": case, "solver": "omg" if solver == "omg" else "gmres-pmg",
                 "config": meta[solver], "dofs_raw": meta["dofs_raw"],
                 "dofs_agglomerated": lv.num_dofs, "iterations": rep.iterations,
-                "ref_iterations_envelope": ([int(z[f"{solver}_envelope"].min()),
-                                             int(z[f"{solver}_envelope"].max())]
-                                            if f"{solver}_envelope" in z else None),
+                "ref_iterations_envelope": ref_envelope(case, z, solver, meta),
                 "converged": rep.converged, "final_residual": rep.final_residual,
                 "relative_residual": rep.final_residual / float(np.linalg.norm(lv.rhs)),
                 "solve_s": rep.time_iterations,
@@ -362,6 +430,7 @@ def time_solves(torch, budget_s: float):
                 "reference_cpu_dof_per_s_build_container":
                     (meta["dofs_raw"] / ref_s) if ref_s else None,
                 "reference_cpu_extrapolated": ref_extrap,
+                "cpu_baseline": cpu_base,
             })
     return out
 

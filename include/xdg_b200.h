@@ -96,6 +96,13 @@ int xdg_dot(int64_t n, const double* x, const double* y, double* out,
  *                 s = a * (*a_dev) otherwise (device scalar)   */
 int xdg_axpy(int64_t n, double a, const double* a_dev, const double* x,
              double* y, xdg_stream_t stream);
+/* One modified Gram-Schmidt step in one pass (distributed GMRES,
+ * solvers.py:802-805): y += c * x with c = a * (*a_dev) (a_dev != NULL) or
+ * c = a, then *out = sum_i v_i y_i over the updated y (v == NULL: sum y_i^2);
+ * deterministic reduction (ws as for xdg_dot). */
+int xdg_axpy_dot(int64_t n, double a, const double* a_dev, const double* x,
+                 double* y, const double* v, double* out, void* ws,
+                 xdg_stream_t stream);
 /* y = s * x with s = a                   if a_dev == NULL and !invert
  *                s = a * (*a_dev)        if a_dev != NULL and !invert
  * y = a * (x / (*a_dev))                 if a_dev != NULL and invert

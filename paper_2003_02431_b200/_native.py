@@ -84,6 +84,7 @@ SIGNATURES = {
     "xdg_batched_factor": (_i32, [_i64, _vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp,
                                   _vp, _i32, _vp, _vp]),
     "xdg_batched_factor_ws_bytes": (_i64, [_i64, _i32]),
+    "xdg_axpy_dot": (_i32, [_i64, _f64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
 }
 
 _lib = None

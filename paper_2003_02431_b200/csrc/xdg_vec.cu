@@ -58,6 +58,26 @@ axpy_kernel(int64_t n, double a, const double* __restrict__ a_dev,
     y[i] = __dadd_rn(y[i], __dmul_rn(s, x[i]));
 }
 
+// One MGS step of the distributed GMRES (solvers.py:802-805) in one pass:
+// y += c x with c = a * (*a_dev), then *out = sum_i v_i y_i (v == NULL:
+// sum y_i^2) -- the axpy of step i fused with the dot of step i + 1, with
+// the rounding of the single-GPU cooperative mgs_kernel.
+__global__ void __launch_bounds__(kT)
+axpy_dot_kernel(int64_t n, double a, const double* __restrict__ a_dev,
+                const double* __restrict__ x, double* y, const double* v, double* out,
+                double* ws) {
+  const double c = a_dev ? __dmul_rn(a, *a_dev) : a;
+  double t = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * kT;
+  for (int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x; i < n; i += stride) {
+    const double yi = __dadd_rn(y[i], __dmul_rn(c, x[i]));
+    y[i] = yi;
+    t = v ? fma(v[i], yi, t) : fma(yi, yi, t);
+  }
+  __shared__ double red[kT / 32];
+  grid_finalize(block_sum(t, red), ws, out);
+}
+
 __global__ void __launch_bounds__(kT)
 scale_kernel(int64_t n, double a, const double* __restrict__ a_dev, int invert,
              const double* __restrict__ x, double* __restrict__ y) {
@@ -276,6 +296,17 @@ extern "C" int xdg_axpy(int64_t n, double a, const double* a_dev,
   if (n <= 0) return XDG_OK;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   axpy_kernel<<<grid_for(n, kT, kPerSm), kT, 0, s>>>(n, a, a_dev, x, y);
+  XDG_CHECK_LAUNCH();
+  return XDG_OK;
+}
+
+extern "C" int xdg_axpy_dot(int64_t n, double a, const double* a_dev, const double* x,
+                            double* y, const double* v, double* out, void* ws,
+                            xdg_stream_t stream) {
+  XDG_REQUIRE(n >= 0 && ws != nullptr, XDG_ERR_ARG, "axpy_dot: bad length or workspace");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  axpy_dot_kernel<<<grid_for(n, kT, kPerSm), kT, 0, s>>>(n, a, a_dev, x, y, v, out,
+                                                          static_cast<double*>(ws));
   XDG_CHECK_LAUNCH();
   return XDG_OK;
 }

@@ -252,10 +252,15 @@ def dist_gmres_pmg_solve(rp, col, val, b, config: SolverConfig, *, dim: int,
             total += 1
             pmg.apply(V[j], Z[j, :L])
             spmv(Z[j], w)
-            for i in range(j + 1):                       # modified Gram-Schmidt
-                gdot(V[i], w, sc[i:i + 1])
-                ctx.axpy(-1.0, V[i], w, a_dev=sc[i:i + 1])
-            gdot(w, w, sc[j + 1:j + 2])
+            # modified Gram-Schmidt (solvers.py:802-805): step i's axpy fused
+            # with step i+1's dot (xdg_axpy_dot), one all-reduce per step
+            gdot(V[0], w, sc[0:1])
+            for i in range(j + 1):
+                nat.check(ctx.lib.xdg_axpy_dot(
+                    L, -1.0, sc[i:i + 1].data_ptr(), V[i].data_ptr(), w.data_ptr(),
+                    V[i + 1].data_ptr() if i < j else None, sc[i + 1:i + 2].data_ptr(),
+                    ctx.ws, ctx.stream), "axpy_dot")
+                comm.allreduce_(sc[i + 1:i + 2])
             col_h = sc[: j + 2].cpu().numpy()
             H[: j + 1, j] = col_h[: j + 1]
             H[j + 1, j] = math.sqrt(col_h[j + 1])

@@ -38,11 +38,14 @@ def batched_factor(ctx, A: torch.Tensor, off, n, p=None, ld=None, *, invert: boo
     nmat = len(off)
     dev = ctx.device
     if perm_off is None:
-        perm_off = np.zeros(nmat + 1, np.int64)
-        np.cumsum(p, out=perm_off[1:])
-    perm_off = np.ascontiguousarray(perm_off, np.int64)
+        perm_off = np.zeros(nmat, np.int64)
+        np.cumsum(p[:-1], out=perm_off[1:])
+    perm_off = np.ascontiguousarray(perm_off[:nmat], np.int64)
+    need = int((perm_off + p).max()) if nmat else 0
     if perm is None:
-        perm = torch.zeros(max(int(perm_off[-1]) if nmat else 0, 1), dtype=I32, device=dev)
+        perm = torch.zeros(max(need, 1), dtype=I32, device=dev)
+    elif perm.numel() < need:
+        raise ValueError(f"perm buffer holds {perm.numel()} entries, {need} needed")
     info = torch.zeros(max(nmat, 1), dtype=I32, device=dev)
     if nmat == 0:
         return perm, perm_off, info

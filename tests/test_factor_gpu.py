@@ -85,16 +85,18 @@ def test_partial_front_schur_complement():
         for a, f, po, (P, B) in zip(mats, out, poff, shapes):
             pr = pm[po:po + P]
             FPP, FPB, FBP, FBB = a[:P, :P], a[:P, P:], a[P:, :P], a[P:, P:]
-            S = FBB - FBP @ np.linalg.solve(FPP, FPB)
-            assert np.abs(f[P:, P:] - S).max() <= 1e-10 * max(1, np.abs(S).max()), (P, B)
+            if B:
+                S = FBB - FBP @ np.linalg.solve(FPP, FPB)
+                assert np.abs(f[P:, P:] - S).max() <= 1e-10 * max(1, np.abs(S).max()), (P, B)
             if invert:
                 L = np.linalg.inv(np.tril(f[:P, :P], -1) + np.eye(P))
                 U = np.linalg.inv(np.triu(f[:P, :P]))
             else:
                 L, U = np.tril(f[:P, :P], -1) + np.eye(P), np.triu(f[:P, :P])
             assert np.abs(FPP[pr] - L @ U).max() <= 1e-11 * np.abs(FPP).max()
-            assert np.abs(f[P:, :P] @ U - FBP).max() <= 1e-10 * max(1, np.abs(FBP).max())
-            assert np.abs(L @ f[:P, P:] - FPB[pr]).max() <= 1e-10 * max(1, np.abs(FPB).max())
+            if B:
+                assert np.abs(f[P:, :P] @ U - FBP).max() <= 1e-10 * max(1, np.abs(FBP).max())
+                assert np.abs(L @ f[:P, P:] - FPB[pr]).max() <= 1e-10 * max(1, np.abs(FPB).max())
 
 
 @pytest.mark.parametrize("n", [700, 3000, 9000])
