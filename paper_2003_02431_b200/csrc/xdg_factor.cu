@@ -29,14 +29,15 @@
 // With `invert`, the top-left p x p LU is then overwritten by its
 // triangular inverses in the layout the solve kernels read
 // (xdg_lu_inv_apply: L^-1 strictly below the diagonal, unit diagonal
-// implicit; U^-1 on and above it), blocked the same way:
-//   diag    every NB x NB diagonal block of L and U inverted in shared memory;
-//   sweep   block column j of U^-1: T = triu(X11) U12, X12 = -T X_jj;
-//           block row i of L^-1:    T = L21 tril1(X11), X21 = -X_ii T.
+// implicit; U^-1 on and above it): blocked TRSMs with the identity, block
+// row by block row (GEMM with the rows already inverted, then substitution
+// with the diagonal block), see trtri_gemm_kernel / trtri_solve_kernel.
 // The permutation is returned directly (perm[i] = original row now at
 // position i, the form xdg_lu_inv_apply / pmg_high consume), and info[b] =
 // first column whose pivot is zero or not finite (+1), 0 if none.
 #include <cooperative_groups.h>
+
+#include <stdlib.h>
 
 #include <algorithm>
 
@@ -339,193 +340,155 @@ lu_update_kernel(double* __restrict__ A, const int64_t* __restrict__ off,
 }
 
 // ---------------------------------------------------------------------------
-// triangular inverses of the p x p LU (in place)
+// Triangular inverses of the p x p LU, in place, as blocked TRSMs with the
+// identity (U X = I bottom-up, L X = I top-down: the right-residual method
+// LAPACK's dtrtrs / scipy solve_triangular(U, I) use; multiplying by
+// explicit inverses of the diagonal blocks instead loses up to two digits
+// on the 1:1000 jump-coefficient systems, measured).  Step s handles block
+// row i = nblk-1-s of U^-1 (z = 0) and block row i = s of L^-1 (z = 1):
+//   gemm   R = E_i - U[i, i+1:] X[i+1:, :]   (z = 0, columns [i0, p))
+//          R = E_i - L[i, :i] X[:i, :]       (z = 1, columns [0, i0 + kb))
+//          into the workspace, with a copy of the diagonal block
+//   solve  U_ii X_i = R by back substitution / L_ii X_i = R by forward
+//          substitution, thread per column, written into the upper / strictly
+//          lower part of block row i only.
+// The U sweep reads and writes only on/above the diagonal, the L sweep only
+// below it: both run in the same launches.  Workspace per (matrix, sweep):
+// NB x p for R, then NB x NB for the diagonal block.
 
-// Invert every NB x NB diagonal block: U_dd (upper, with diagonal) and the
-// unit-lower L_dd; grid (diag blocks, matrices), 256 threads.
+__device__ __forceinline__ double* trtri_ws(double* W, int64_t wstride, int b, int z) {
+  return W + (2 * (int64_t)b + z) * wstride;
+}
+
+// grid (64-column tiles, matrices, 2)
 __global__ void __launch_bounds__(256)
-trtri_diag_kernel(double* __restrict__ A, const int64_t* __restrict__ off,
+trtri_gemm_kernel(double* __restrict__ A, const int64_t* __restrict__ off,
                   const int* __restrict__ dn, const int* __restrict__ dp,
-                  const int* __restrict__ dld, int NB) {
-  extern __shared__ double sm[];
+                  const int* __restrict__ dld, double* __restrict__ W, int64_t wstride,
+                  int step, int NB) {
+  __shared__ double As[kKc][kTile + 1];
+  __shared__ double Bs[kKc][kTile + 1];
   const Mat M = mat_of(A, off, dn, dp, dld, blockIdx.y);
-  const int d0 = blockIdx.x * NB;
-  if (d0 >= M.p) return;
-  const int kb = min(NB, M.p - d0);
-  double* T = sm;             // the block, kb x kb
-  double* X = sm + kb * kb;   // its inverse parts
-  for (int e = threadIdx.x; e < kb * kb; e += blockDim.x)
-    T[e] = M.a[(int64_t)(d0 + e / kb) * M.ld + d0 + e % kb];
+  const int nblk = (M.p + NB - 1) / NB;
+  if (step >= nblk) return;
+  const int z = blockIdx.z;
+  const int i = z == 0 ? nblk - 1 - step : step;
+  const int i0 = i * NB, kb = min(NB, M.p - i0);
+  const int cbeg = z == 0 ? i0 : 0;
+  const int cend = z == 0 ? M.p : i0 + kb;
+  const int j0 = cbeg + blockIdx.x * kTile;
+  if (j0 >= cend) return;
+  const double* a = M.a;
+  const int ld = M.ld, P = M.p;
+  double* R = trtri_ws(W, wstride, blockIdx.y, z);
+  double* Dg = R + (int64_t)NB * P;
+  if (blockIdx.x == 0)  // original diagonal block for the solve step
+    for (int e = threadIdx.x; e < kb * kb; e += 256)
+      Dg[e] = a[(int64_t)(i0 + e / kb) * ld + i0 + e % kb];
+  TileAcc acc;
+  if (z == 0) {
+    // K over k in [i0 + kb, min(P, j0 + 64)): X[k][j] upper (k <= j)
+    const int kbeg = i0 + kb, kend = min(P, j0 + kTile);
+    tile_mma(
+        acc, max(0, kend - kbeg),
+        [&](int r, int k) {
+          const int gk = kbeg + k;
+          return (r < kb && gk < kend) ? a[(int64_t)(i0 + r) * ld + gk] : 0.0;
+        },
+        [&](int k, int c) {
+          const int gk = kbeg + k, gj = j0 + c;
+          return (gk < kend && gj < cend && gk <= gj) ? a[(int64_t)gk * ld + gj] : 0.0;
+        },
+        As, Bs);
+  } else {
+    // K over k in [j0, i0): X[k][j] unit lower (k > j stored, k == j -> 1)
+    const int kbeg = j0, kend = i0;
+    tile_mma(
+        acc, max(0, kend - kbeg),
+        [&](int r, int k) {
+          const int gk = kbeg + k;
+          return (r < kb && gk < kend) ? a[(int64_t)(i0 + r) * ld + gk] : 0.0;
+        },
+        [&](int k, int c) {
+          const int gk = kbeg + k, gj = j0 + c;
+          if (gk >= kend || gj >= cend || gk < gj) return 0.0;
+          return gk == gj ? 1.0 : a[(int64_t)gk * ld + gj];
+        },
+        As, Bs);
+  }
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int r = ty * 4 + q;
+    if (r >= kb) continue;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int gj = j0 + tx * 4 + c;
+      if (gj < cend) R[(int64_t)r * P + gj] = (gj == i0 + r ? 1.0 : 0.0) - acc.c[q][c];
+    }
+  }
+}
+
+// grid (256-column chunks, matrices, 2)
+__global__ void __launch_bounds__(256)
+trtri_solve_kernel(double* __restrict__ A, const int64_t* __restrict__ off,
+                   const int* __restrict__ dn, const int* __restrict__ dp,
+                   const int* __restrict__ dld, const double* __restrict__ W,
+                   int64_t wstride, int step, int NB) {
+  __shared__ double D[64 * 65];
+  const Mat M = mat_of(A, off, dn, dp, dld, blockIdx.y);
+  const int nblk = (M.p + NB - 1) / NB;
+  if (step >= nblk) return;
+  const int z = blockIdx.z;
+  const int i = z == 0 ? nblk - 1 - step : step;
+  const int i0 = i * NB, kb = min(NB, M.p - i0);
+  const int cbeg = z == 0 ? i0 : 0;
+  const int cend = z == 0 ? M.p : i0 + kb;
+  const int P = M.p;
+  const double* R = trtri_ws(const_cast<double*>(W), wstride, blockIdx.y, z);
+  const double* Dg = R + (int64_t)NB * P;
+  if (cbeg + (int)blockIdx.x * 256 >= cend) return;
+  for (int e = threadIdx.x; e < kb * kb; e += 256) D[(e / kb) * 65 + e % kb] = Dg[e];
   __syncthreads();
-  // U^-1 column by column: x_jj = 1/u_jj, x_ij = -(sum_{k=i}^{j-1} x_ik u_kj) x_jj
-  // L^-1 row by row:       x_ij = -(l_ij + sum_{k=j+1}^{i-1} l_ik x_kj), i > j
-  for (int t = 0; t < kb; ++t) {
-    // U column t (threads i < t), diag by thread t
-    for (int i = threadIdx.x; i <= t; i += blockDim.x) {
-      const double xjj = 1.0 / T[t * kb + t];
-      if (i == t) {
-        X[t * kb + t] = xjj;
-      } else {
-        double s = 0.0;
-        for (int k = i; k < t; ++k) s = __fma_rn(X[i * kb + k], T[k * kb + t], s);
-        X[i * kb + t] = -s * xjj;
+  const int j = cbeg + blockIdx.x * 256 + threadIdx.x;
+  if (j >= cend) return;
+  double x[64];
+  if (z == 0) {  // back substitution, rows kb-1 .. 0
+    const int rmax = j < i0 + kb ? j - i0 : kb - 1;  // X_ii upper: rows <= j - i0
+    for (int r = kb - 1; r >= 0; --r) {
+      if (r > rmax) {
+        x[r] = 0.0;
+        continue;
       }
+      double v = R[(int64_t)r * P + j];
+      for (int c = r + 1; c <= rmax; ++c) v = __fma_rn(-D[r * 65 + c], x[c], v);
+      x[r] = v / D[r * 65 + r];
     }
-    // L row t (threads j < t)
-    for (int jx = threadIdx.x; jx < t; jx += blockDim.x) {
-      double s = T[t * kb + jx];
-      for (int k = jx + 1; k < t; ++k) s = __fma_rn(T[t * kb + k], X[k * kb + jx], s);
-      X[t * kb + jx] = -s;
-    }
-    __syncthreads();
-  }
-  for (int e = threadIdx.x; e < kb * kb; e += blockDim.x)
-    M.a[(int64_t)(d0 + e / kb) * M.ld + d0 + e % kb] = X[e];
-}
-
-// Block column j0 of U^-1 (z = 0) or block row j0 of L^-1 (z = 1), first
-// half: T = triu(X[0:j0,0:j0]) U[0:j0, j0:j0+kb]   (z = 0, T: j0 x kb)
-//       T = L[j0:j0+kb, 0:j0] tril1(X[0:j0,0:j0])   (z = 1, T: kb x j0)
-// into the workspace (matrix b, sweep z at W + (2b + z) * wstride, row-major,
-// kb-wide / j0-wide).
-// grid (64-row (z=0) / 64-column (z=1) tiles, matrices, 2).
-__global__ void __launch_bounds__(256)
-trtri_sweep_t_kernel(double* __restrict__ A, const int64_t* __restrict__ off,
-                     const int* __restrict__ dn, const int* __restrict__ dp,
-                     const int* __restrict__ dld, double* __restrict__ W,
-                     int64_t wstride, int j0, int NB) {
-  __shared__ double As[kKc][kTile + 1];
-  __shared__ double Bs[kKc][kTile + 1];
-  const Mat M = mat_of(A, off, dn, dp, dld, blockIdx.y);
-  if (j0 >= M.p) return;
-  const int kb = min(NB, M.p - j0);
-  const double* a = M.a;
-  const int ld = M.ld;
-  double* T = W + (2 * (int64_t)blockIdx.y + blockIdx.z) * wstride;
-  const int t0 = blockIdx.x * kTile;
-  if (t0 >= j0) return;
-  TileAcc acc;
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  if (blockIdx.z == 0) {
-    // rows t0.., K runs over k in [t0, j0) with k >= i (upper triangle)
-    const int K = j0 - t0;
-    tile_mma(
-        acc, K,
-        [&](int i, int k) {
-          const int gi = t0 + i, gk = t0 + k;
-          return (gi < j0 && gk < j0 && gk >= gi) ? a[(int64_t)gi * ld + gk] : 0.0;
-        },
-        [&](int k, int jx) {
-          const int gk = t0 + k;
-          return (gk < j0 && jx < kb) ? a[(int64_t)gk * ld + j0 + jx] : 0.0;
-        },
-        As, Bs);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int gi = t0 + ty * 4 + i;
-      if (gi >= j0) continue;
-#pragma unroll
-      for (int jx = 0; jx < 4; ++jx) {
-        const int c = tx * 4 + jx;
-        if (c < kb) T[(int64_t)gi * kb + c] = acc.c[i][jx];
+    for (int r = 0; r <= rmax; ++r) M.a[(int64_t)(i0 + r) * M.ld + j] = x[r];
+  } else {  // forward substitution with the unit-lower L_ii
+    const int rmin = j >= i0 ? j - i0 + 1 : 0;  // strictly lower part only
+    for (int r = 0; r < kb; ++r) {
+      if (r < rmin) {
+        x[r] = 0.0;
+        continue;
       }
+      double v = R[(int64_t)r * P + j];
+      for (int c = rmin; c < r; ++c) v = __fma_rn(-D[r * 65 + c], x[c], v);
+      x[r] = v;
     }
-  } else {
-    // columns t0.., K over k in [t0, j0) with k >= column (unit lower X)
-    const int K = j0 - t0;
-    tile_mma(
-        acc, K,
-        [&](int i, int k) {
-          const int gk = t0 + k;
-          return (i < kb && gk < j0) ? a[(int64_t)(j0 + i) * ld + gk] : 0.0;
-        },
-        [&](int k, int jx) {
-          const int gk = t0 + k, gc = t0 + jx;
-          if (gk >= j0 || gc >= j0 || gk < gc) return 0.0;
-          return gk == gc ? 1.0 : a[(int64_t)gk * ld + gc];
-        },
-        As, Bs);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int r = ty * 4 + i;
-      if (r >= kb) continue;
-#pragma unroll
-      for (int jx = 0; jx < 4; ++jx) {
-        const int gc = t0 + tx * 4 + jx;
-        if (gc < j0) T[(int64_t)r * j0 + gc] = acc.c[i][jx];
-      }
-    }
-  }
-}
-
-// Second half: X[0:j0, j0:j0+kb] = -T X_jj   (z = 0)
-//              X[j0:j0+kb, 0:j0] = -X_jj T   (z = 1)
-// grid (64-row / 64-column tiles, matrices, 2).
-__global__ void __launch_bounds__(256)
-trtri_sweep_x_kernel(double* __restrict__ A, const int64_t* __restrict__ off,
-                     const int* __restrict__ dn, const int* __restrict__ dp,
-                     const int* __restrict__ dld, const double* __restrict__ W,
-                     int64_t wstride, int j0, int NB) {
-  __shared__ double As[kKc][kTile + 1];
-  __shared__ double Bs[kKc][kTile + 1];
-  const Mat M = mat_of(A, off, dn, dp, dld, blockIdx.y);
-  if (j0 >= M.p) return;
-  const int kb = min(NB, M.p - j0);
-  const int t0 = blockIdx.x * kTile;
-  if (t0 >= j0) return;
-  const double* a = M.a;
-  const int ld = M.ld;
-  const double* T = W + (2 * (int64_t)blockIdx.y + blockIdx.z) * wstride;
-  TileAcc acc;
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  if (blockIdx.z == 0) {
-    tile_mma(
-        acc, kb,
-        [&](int i, int k) {
-          const int gi = t0 + i;
-          return (gi < j0 && k < kb) ? T[(int64_t)gi * kb + k] : 0.0;
-        },
-        [&](int k, int jx) {  // X_jj upper (with diagonal)
-          return (k < kb && jx < kb && k <= jx) ? a[(int64_t)(j0 + k) * ld + j0 + jx] : 0.0;
-        },
-        As, Bs);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int gi = t0 + ty * 4 + i;
-      if (gi >= j0) continue;
-#pragma unroll
-      for (int jx = 0; jx < 4; ++jx) {
-        const int c = tx * 4 + jx;
-        if (c < kb) M.a[(int64_t)gi * ld + j0 + c] = -acc.c[i][jx];
-      }
-    }
-  } else {
-    tile_mma(
-        acc, kb,
-        [&](int i, int k) {  // X_jj unit lower
-          if (i >= kb || k >= kb || k > i) return 0.0;
-          return k == i ? 1.0 : a[(int64_t)(j0 + i) * ld + j0 + k];
-        },
-        [&](int k, int jx) {
-          const int gc = t0 + jx;
-          return (k < kb && gc < j0) ? T[(int64_t)k * j0 + gc] : 0.0;
-        },
-        As, Bs);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int r = ty * 4 + i;
-      if (r >= kb) continue;
-#pragma unroll
-      for (int jx = 0; jx < 4; ++jx) {
-        const int gc = t0 + tx * 4 + jx;
-        if (gc < j0) M.a[(int64_t)(j0 + r) * ld + gc] = -acc.c[i][jx];
-      }
-    }
+    for (int r = rmin; r < kb; ++r) M.a[(int64_t)(i0 + r) * M.ld + j] = x[r];
   }
 }
 
 int panel_nb(int max_n) {
+  // XDG_FACTOR_NB (8/16/32/64) overrides the panel width (experiments)
+  static const int forced = [] {
+    const char* e = getenv("XDG_FACTOR_NB");
+    const int v = e ? atoi(e) : 0;
+    return (v == 8 || v == 16 || v == 32 || v == 64) ? v : 0;
+  }();
   // NB x (max_n / 16 rows) must fit one CTA's shared memory
+  if (forced && (size_t)(max_n + 15) / 16 * (forced + 1) * 8 <= 200 * 1024) return forced;
   if (max_n <= 6144) return 64;
   if (max_n <= 12288) return 32;
   if (max_n <= 24576) return 16;
@@ -540,10 +503,10 @@ constexpr size_t kSmemCap = 200 * 1024;
 using namespace xdg;
 
 extern "C" int64_t xdg_batched_factor_ws_bytes(int64_t nmat, int max_p) {
-  // per matrix: the U sweep's j0 x NB and the L sweep's NB x j0 temporaries
-  // (j0 < max_p; NB as chosen for max_n >= max_p, at most panel_nb(max_p))
+  // per matrix and sweep: NB x max_p (R) + NB x NB (diagonal block); NB as
+  // chosen for max_n >= max_p is at most panel_nb(max_p)
   const int NB = panel_nb(max_p);
-  return 2 * nmat * (int64_t)std::max(max_p, 1) * NB * 8;
+  return 2 * nmat * ((int64_t)NB * std::max(max_p, 1) + (int64_t)NB * NB) * 8;
 }
 
 extern "C" int xdg_batched_factor(int64_t nmat, const int64_t* off, const int* n,
@@ -564,9 +527,6 @@ extern "C" int xdg_batched_factor(int64_t nmat, const int64_t* off, const int* n
     XDG_TRY_CUDA(cudaFuncSetAttribute(lu_panel_kernel,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)kSmemCap + 4096));
-    XDG_TRY_CUDA(cudaFuncSetAttribute(trtri_diag_kernel,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      2 * 64 * 64 * 8));
     attr_done = true;
   }
   XDG_TRY_CUDA(cudaMemsetAsync(info, 0, sizeof(int) * nmat, s));
@@ -607,16 +567,15 @@ extern "C" int xdg_batched_factor(int64_t nmat, const int64_t* off, const int* n
     }
   }
   if (!invert) return XDG_OK;
-  const int nd = (max_p + NB - 1) / NB;
-  trtri_diag_kernel<<<dim3((unsigned)nd, (unsigned)nmat), 256, 2 * NB * NB * 8, s>>>(
-      A, off, n, p, ld, NB);
-  XDG_CHECK_LAUNCH();
-  const int64_t wstride = (int64_t)max_p * NB;
-  for (int j0 = NB; j0 < max_p; j0 += NB) {
-    dim3 g((unsigned)((j0 + kTile - 1) / kTile), (unsigned)nmat, 2);
-    trtri_sweep_t_kernel<<<g, 256, 0, s>>>(A, off, n, p, ld, ws, wstride, j0, NB);
+  // workspace per (matrix, sweep): NB x max_p for R + NB x NB diagonal block
+  const int64_t wstride = (int64_t)NB * max_p + (int64_t)NB * NB;
+  const int nblk = (max_p + NB - 1) / NB;
+  for (int st = 0; st < nblk; ++st) {
+    dim3 g1((unsigned)((max_p + kTile - 1) / kTile), (unsigned)nmat, 2);
+    trtri_gemm_kernel<<<g1, 256, 0, s>>>(A, off, n, p, ld, ws, wstride, st, NB);
     XDG_CHECK_LAUNCH();
-    trtri_sweep_x_kernel<<<g, 256, 0, s>>>(A, off, n, p, ld, ws, wstride, j0, NB);
+    dim3 g2((unsigned)((max_p + 255) / 256), (unsigned)nmat, 2);
+    trtri_solve_kernel<<<g2, 256, 0, s>>>(A, off, n, p, ld, ws, wstride, st, NB);
     XDG_CHECK_LAUNCH();
   }
   return XDG_OK;

@@ -55,10 +55,13 @@ def main():
         off = np.cumsum([0] + [a.size for a in mats[:-1]])
         ns = [a.shape[0] for a in mats]
         A = torch.from_numpy(flat).cuda()
+        A2 = A.clone()
         perm, poff, info = batched_factor(ctx, A, off, ns, invert=True)
         F = A.cpu().numpy()
         pm = perm.cpu().numpy()
-        e_mine, e_lapack, e_linv = [], [], []
+        batched_factor(ctx, A2, off, ns, invert=False)
+        F2 = A2.cpu().numpy()
+        e_mine, e_lapack, e_linv, e_myLU_subst, e_myLU_inv, e_lu_diff = [], [], [], [], [], []
         for a, o, po, n in zip(mats, off, poff, ns):
             b = rng.standard_normal(n)
             xr = refined(a, b)
@@ -76,13 +79,30 @@ def main():
             for i, q in enumerate(piv):
                 sp[[i, q]] = sp[[q, i]]
             x3 = Ui @ (Li @ b[sp])
+            # my LU (no inverse) with LAPACK substitution / LAPACK inverses
+            LU2 = F2[o:o + n * n].reshape(n, n)
+            L2 = np.tril(LU2, -1) + np.eye(n)
+            U2 = np.triu(LU2)
+            x4 = sla.solve_triangular(U2, sla.solve_triangular(L2, b[pr], lower=True,
+                                                                unit_diagonal=True))
+            L2i = sla.solve_triangular(L2, np.eye(n), lower=True, unit_diagonal=True)
+            U2i = sla.solve_triangular(U2, np.eye(n))
+            x5 = U2i @ (L2i @ b[pr])
+            e_lu_diff.append(float(np.abs(LU2 - lu).max() / np.abs(lu).max())
+                             if np.array_equal(pr, sp) else -1.0)
             nr = np.linalg.norm(xr)
+            e_myLU_subst.append(np.linalg.norm(x4 - xr) / nr)
+            e_myLU_inv.append(np.linalg.norm(x5 - xr) / nr)
             e_mine.append(np.linalg.norm(x1 - xr) / nr)
             e_lapack.append(np.linalg.norm(x2 - xr) / nr)
             e_linv.append(np.linalg.norm(x3 - xr) / nr)
         r = {"case": case, "target": tgt, "m": m, "systems": len(mats), "max_n": max(ns),
              "fwd_err_mine_max": max(e_mine), "fwd_err_lapack_subst_max": max(e_lapack),
              "fwd_err_lapack_inverses_max": max(e_linv),
+             "fwd_err_myLU_subst_max": max(e_myLU_subst),
+             "fwd_err_myLU_lapack_inverses_max": max(e_myLU_inv),
+             "lu_diff_vs_lapack_max (-1: other pivots)": max(e_lu_diff),
+             "pivots_equal_lapack": int(sum(d >= 0 for d in e_lu_diff)),
              "fwd_err_mine_med": float(np.median(e_mine)),
              "fwd_err_lapack_inverses_med": float(np.median(e_linv))}
         print(json.dumps(r), flush=True)
