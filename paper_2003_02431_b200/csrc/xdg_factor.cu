@@ -466,17 +466,19 @@ trtri_solve_kernel(double* __restrict__ A, const int64_t* __restrict__ off,
     }
     for (int r = 0; r <= rmax; ++r) M.a[(int64_t)(i0 + r) * M.ld + j] = x[r];
   } else {  // forward substitution with the unit-lower L_ii
-    const int rmin = j >= i0 ? j - i0 + 1 : 0;  // strictly lower part only
+    // X_ii unit lower: column j - i0 of it starts at its unit diagonal
+    // (R = 1 there), which takes part in the substitution but is not stored
+    const int rlo = j >= i0 ? j - i0 : 0;
     for (int r = 0; r < kb; ++r) {
-      if (r < rmin) {
+      if (r < rlo) {
         x[r] = 0.0;
         continue;
       }
       double v = R[(int64_t)r * P + j];
-      for (int c = rmin; c < r; ++c) v = __fma_rn(-D[r * 65 + c], x[c], v);
+      for (int c = rlo; c < r; ++c) v = __fma_rn(-D[r * 65 + c], x[c], v);
       x[r] = v;
     }
-    for (int r = rmin; r < kb; ++r) M.a[(int64_t)(i0 + r) * M.ld + j] = x[r];
+    for (int r = j >= i0 ? rlo + 1 : 0; r < kb; ++r) M.a[(int64_t)(i0 + r) * M.ld + j] = x[r];
   }
 }
 
