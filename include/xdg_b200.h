@@ -62,6 +62,10 @@ int xdg_gather_blocks(int64_t nidx, int N, const int* idx, const double* x,
 
 /* y[idx[i]*N + q] += src[i*N + q] (idx without duplicates): adds the
  * partial Schwarz sums other ranks computed for this rank's cells. */
+/* y[idx[i]*N + q] = src[i*N + q] (idx without duplicates): unpacks
+ * values received from other ranks (multi-GPU multifrontal exchange). */
+int xdg_scatter_blocks(int64_t nidx, int N, const int* idx, const double* src, double* y,
+                       xdg_stream_t stream);
 int xdg_scatter_add_blocks(int64_t nidx, int N, const int* idx,
                            const double* src, double* y, xdg_stream_t stream);
 /* out[k*m + q] = x[k*N + q], q < m: the low-order modes of nblk blocks (the
@@ -347,6 +351,13 @@ int xdg_schwarz_copy(int64_t* core_ptr, int64_t* core_nodes, int64_t* ext_ptr,
  * 3 launches per forward level, 2 per backward level. */
 int xdg_mf_solve(const xdg_mf* mf, const double* b, double* x,
                  xdg_stream_t stream);
+/* One sweep of xdg_mf_solve: phase 1 = forward (gather, L^-1, bound
+ * contributions), 2 = backward (U_PB, U^-1, output), 3 = both.  The
+ * multi-GPU factor (dist_multifrontal) runs the owned subtrees' forward
+ * sweep, exchanges the subtree roots' contributions, runs the replicated
+ * top fronts, then the owned backward sweep. */
+int xdg_mf_solve_phase(const xdg_mf* mf, const double* b, double* x, int phase,
+                       xdg_stream_t stream);
 
 /* ======================================================================
  * Native solver driver (the reference's control loops, solvers.py:559-846,

@@ -85,6 +85,8 @@ SIGNATURES = {
                                   _vp, _i32, _vp, _vp]),
     "xdg_batched_factor_ws_bytes": (_i64, [_i64, _i32]),
     "xdg_axpy_dot": (_i32, [_i64, _f64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "xdg_mf_solve_phase": (_i32, [_vp, _vp, _vp, _i32, _vp]),
+    "xdg_scatter_blocks": (_i32, [_i64, _i32, _vp, _vp, _vp, _vp]),
 }
 
 _lib = None

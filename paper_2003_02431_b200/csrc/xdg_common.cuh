@@ -11,8 +11,18 @@
 #include <stdio.h>
 
 #include "../../include/xdg_b200.h"
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3 (no library to link)
 
 namespace xdg {
+
+// NVTX range for the lifetime of a scope: the solver phases show up as named
+// ranges in nsys / ncu --nvtx timelines (no cost when no tool is attached).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 void set_error(const char* fmt, ...);
 
@@ -41,6 +51,16 @@ void set_error(const char* fmt, ...);
       return (code);                                                       \
     }                                                                      \
   } while (0)
+
+// Device-resident column-count variants of the RM kernels (xdg_vec.cu):
+// launched for max_cols columns, the kernels use min(max_cols, *ncols_dev).
+int gemv_t_dev(int64_t L, int max_cols, const int* ncols_dev, const double* W, int64_t ldw,
+               const double* w, double* coeff, void* ws, cudaStream_t s);
+int gemv_update2_dev(int64_t L, int max_cols, const int* ncols_dev, const double* W,
+                     const double* Z, int64_t ld, const double* cw, const double* cz,
+                     double* w, double* z, cudaStream_t s);
+int add_small_dev(int max_n, const int* n_dev, const double* a, const double* b, double* out,
+                  cudaStream_t s);
 
 // Number of SMs on the current device (cached per process; one device per
 // process is the deployment model).

@@ -18,6 +18,7 @@
 //   rm_current        x = x0 + y ; r = r0 - My
 #include <cooperative_groups.h>
 #include <math.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <vector>
@@ -267,6 +268,7 @@ static int pmg_apply_op(const xdg_pmg* P, const xdg_bsr* M, const double* b,
 extern "C" int xdg_pmg_apply_op(const xdg_pmg* P, const xdg_bsr* M,
                                 const double* b, double* z,
                                 xdg_stream_t stream) {
+  NvtxRange nv("xdg_pmg_apply");
   return pmg_apply_op(P, M, b, z, reinterpret_cast<cudaStream_t>(stream));
 }
 
@@ -313,6 +315,7 @@ static int rm_restart(xdg_rm* rm, cudaStream_t s) {
 
 extern "C" int xdg_rm_step(xdg_rm* rm, const xdg_bsr* M, const double* zc,
                            xdg_stream_t stream) {
+  NvtxRange nv("xdg_rm_step");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int64_t n = rm->n;
   if (rm->ncols >= rm->max_columns) XDG_TRY(rm_restart(rm, s));
@@ -466,7 +469,515 @@ int omg_level(OmgRun& R, int lam, const double* b, double* x, int has_x0,
   return XDG_OK;
 }
 
+
 }  // namespace
+
+namespace xdg {
+namespace omg_graph {
+
+// ===========================================================================
+// Graph-captured ortho_mg_solve: the whole Alg. 4 recursion as ONE CUDA graph
+// with device-side control flow -- no host round trip per rm_step or
+// iteration (the host-decision driver above reads 4 scalars back after every
+// rm_step and one per level visit: ~11 blocking D2H reads per level-1
+// iteration at cfg1).
+//   * RmState scalars (column count, best norm, counters) live on the
+//     device (RmDev); rm_step's three outcomes (solvers.py:594-615:
+//     dependent -> current(), reject -> restart(), accept -> commit) are the
+//     bodies of a SWITCH node whose value a 1-thread decision kernel sets;
+//     the restart at a full space (solvers.py:574-575) is an IF node.
+//   * Each level's iteration loop (solvers.py:719-738: `while ||r|| > tol
+//     and it < budget`) is a WHILE node; the loop-end kernel appends the
+//     history entry and re-evaluates the condition.  Coarse levels nest
+//     their WHILE node inside the finer level's body.
+//   * The candidate w of a step is built in a per-level scratch vector and
+//     copied into its column on accept (the host driver builds it in the
+//     column itself); My takes My_new's values on accept (the host driver
+//     swaps the pointers).  Same kernels, same grids, same arithmetic: the
+//     results are bit-identical to the host-decision driver
+//     (tests/test_omg_graph_gpu.py).
+//   * Algorithmic bytes: the decision kernels add each rm_step's bytes for
+//     the path actually taken, the loop-end kernels each body's fixed bytes.
+
+struct RmDev {
+  double best_norm, last, bytes, pad0;
+  int ncols, last_dependent, dependent_count, rejected_count, restart_count;
+  int col, path, it, budget, pad1;
+};
+
+__global__ void rm_dev_pre_kernel(RmDev* st, int max_columns, cudaGraphConditionalHandle h,
+                                  double restart_bytes, double* gbytes) {
+  const int full = st->ncols >= max_columns;
+  if (full) *gbytes += restart_bytes;
+  cudaGraphSetConditional(h, full);
+}
+
+__global__ void __launch_bounds__(kT)
+rm_dev_restart_kernel(int64_t n, RmDev* st, double* __restrict__ x0, double* __restrict__ r0,
+                      double* __restrict__ y, double* __restrict__ My, double* __restrict__ x,
+                      double* __restrict__ r) {
+  const int64_t stride = (int64_t)gridDim.x * kT;
+  for (int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x; i < n; i += stride) {
+    const double xn = __dadd_rn(x0[i], y[i]);
+    const double rn = __dadd_rn(r0[i], -My[i]);
+    x0[i] = xn;
+    r0[i] = rn;
+    y[i] = 0.0;
+    My[i] = 0.0;
+    x[i] = xn;
+    r[i] = rn;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->ncols = 0;
+    st->restart_count += 1;
+  }
+}
+
+// rm_step decision (solvers.py:594-615) on the device
+__global__ void rm_dev_decide_kernel(RmDev* st, const double* sc, cudaGraphConditionalHandle h,
+                                     double* gbytes, double n, double spmv2, double cgs_per_col,
+                                     double cgs_fixed) {
+  const int col = st->ncols;
+  double bytes = spmv2 + 96.0 * n + (col > 0 ? cgs_per_col * col + cgs_fixed : 0.0);
+  const double scale = sqrt(sc[0]), norm_w = sqrt(sc[1]);
+  int path;
+  if (scale == 0.0 || norm_w <= 1e-13 * scale) {
+    st->last_dependent = 1;
+    st->dependent_count += 1;
+    path = 1;
+    bytes += 48.0 * n;
+  } else {
+    const double rho = sqrt(sc[3]);
+    st->last_dependent = 0;
+    if (rho > st->best_norm) {
+      st->rejected_count += 1;  // the restart body zeroes ncols, counts the restart
+      path = 2;
+      bytes += 80.0 * n;
+    } else {
+      st->col = col;
+      st->ncols = col + 1;
+      st->best_norm = rho;
+      path = 0;
+      bytes += 64.0 * n;
+    }
+  }
+  st->path = path;
+  *gbytes += bytes;
+  cudaGraphSetConditional(h, (unsigned)path);
+}
+
+// accept: y += alpha z; x = x0 + y; r = r0 - My_new; My = My_new; the
+// candidate (z, w) becomes column `col` of (Z, W)
+__global__ void __launch_bounds__(kT)
+rm_dev_commit_kernel(int64_t n, const RmDev* st, const double* __restrict__ alpha,
+                     const double* __restrict__ z, const double* __restrict__ w,
+                     double* __restrict__ y, const double* __restrict__ x0,
+                     const double* __restrict__ r0, const double* __restrict__ My_new,
+                     double* __restrict__ My, double* __restrict__ x, double* __restrict__ r,
+                     double* __restrict__ Z, double* __restrict__ W) {
+  const double a = *alpha;
+  const int64_t col = st->col;
+  double* Zc = Z + col * n;
+  double* Wc = W + col * n;
+  const int64_t stride = (int64_t)gridDim.x * kT;
+  for (int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x; i < n; i += stride) {
+    const double zi = z[i];
+    const double yi = __dadd_rn(y[i], __dmul_rn(a, zi));
+    const double mn = My_new[i];
+    y[i] = yi;
+    x[i] = __dadd_rn(x0[i], yi);
+    r[i] = __dadd_rn(r0[i], -mn);
+    My[i] = mn;
+    Zc[i] = zi;
+    Wc[i] = w[i];
+  }
+}
+
+__global__ void __launch_bounds__(kT)
+copy_kernel(int64_t n, const double* __restrict__ a, double* __restrict__ b) {
+  const int64_t stride = (int64_t)gridDim.x * kT;
+  for (int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x; i < n; i += stride) b[i] = a[i];
+}
+
+__global__ void __launch_bounds__(kT)
+zero2_kernel(int64_t n, double* __restrict__ a, double* __restrict__ b) {
+  const int64_t stride = (int64_t)gridDim.x * kT;
+  for (int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x; i < n; i += stride) {
+    a[i] = 0.0;
+    if (b) b[i] = 0.0;
+  }
+}
+
+// RmState(x, r) scalars + the level loop's first condition
+__global__ void rm_dev_init_kernel(RmDev* st, const double* nr2, int budget, double tol,
+                                   double* hist, cudaGraphConditionalHandle h) {
+  const double bn = sqrt(*nr2);
+  st->best_norm = bn;
+  st->last = bn;
+  st->ncols = st->last_dependent = st->dependent_count = 0;
+  st->rejected_count = st->restart_count = 0;
+  st->it = 0;
+  st->budget = budget;
+  if (hist) hist[0] = bn;
+  cudaGraphSetConditional(h, (bn > tol && budget > 0) ? 1u : 0u);
+}
+
+__global__ void level_loop_end_kernel(RmDev* st, double tol, double* hist,
+                                      cudaGraphConditionalHandle h, double* gbytes,
+                                      double body_bytes) {
+  const int it = st->it + 1;
+  st->it = it;
+  const double last = st->best_norm;
+  st->last = last;
+  if (hist) hist[it] = last;
+  *gbytes += body_bytes;
+  cudaGraphSetConditional(h, (last > tol && it < st->budget) ? 1u : 0u);
+}
+
+// x = rm.x when the loop ran at least once
+__global__ void __launch_bounds__(kT)
+copy_if_ran_kernel(int64_t n, const RmDev* st, const double* __restrict__ a,
+                   double* __restrict__ b) {
+  if (st->it <= 0) return;
+  const int64_t stride = (int64_t)gridDim.x * kT;
+  for (int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x; i < n; i += stride) b[i] = a[i];
+}
+
+struct GraphOmg {
+  xdg_omg_level* L;
+  int nlevels, entry;
+  double tol;
+  int max_it, coarse_it;
+  std::vector<cudaStream_t> streams;  // one capture stream per nesting depth
+  RmDev* dev = nullptr;               // per level
+  double* wc = nullptr;               // per level candidate-w scratch (offsets)
+  std::vector<int64_t> wc_off;
+  double* hist = nullptr;
+  double* gbytes = nullptr;
+  cudaGraph_t top = nullptr;
+};
+
+cudaStream_t cap_stream(GraphOmg& G, int depth) {
+  while ((int)G.streams.size() <= depth) {
+    cudaStream_t t;
+    if (cudaStreamCreateWithFlags(&t, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+    G.streams.push_back(t);
+  }
+  return G.streams[depth];
+}
+
+// A conditional handle on the graph stream s is capturing into.
+int make_handle(cudaStream_t s, cudaGraphConditionalHandle* h) {
+  cudaStreamCaptureStatus cs;
+  cudaGraph_t g;
+  XDG_TRY_CUDA(cudaStreamGetCaptureInfo(s, &cs, nullptr, &g, nullptr, nullptr));
+  XDG_REQUIRE(cs == cudaStreamCaptureStatusActive, XDG_ERR_CUDA, "stream not capturing");
+  XDG_TRY_CUDA(cudaGraphConditionalHandleCreate(h, g, 0, 0));
+  return XDG_OK;
+}
+
+// Add a conditional node (handle h) at the capture frontier of stream s;
+// returns its body graphs.
+int add_cond_node(cudaStream_t s, cudaGraphConditionalHandle h,
+                  cudaGraphConditionalNodeType type, int size, cudaGraph_t* bodies) {
+  cudaStreamCaptureStatus cs;
+  cudaGraph_t g;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  XDG_TRY_CUDA(cudaStreamGetCaptureInfo(s, &cs, nullptr, &g, &deps, &nd));
+  XDG_REQUIRE(cs == cudaStreamCaptureStatusActive, XDG_ERR_CUDA, "stream not capturing");
+  cudaGraphNodeParams p = {};
+  p.type = cudaGraphNodeTypeConditional;
+  p.conditional.handle = h;
+  p.conditional.type = type;
+  p.conditional.size = size;
+  cudaGraphNode_t node;
+  XDG_TRY_CUDA(cudaGraphAddNode(&node, g, deps, nd, &p));
+  for (int i = 0; i < size; ++i) bodies[i] = p.conditional.phGraph_out[i];
+  XDG_TRY_CUDA(cudaStreamUpdateCaptureDependencies(s, &node, 1,
+                                                   cudaStreamSetCaptureDependencies));
+  return XDG_OK;
+}
+
+int begin_body(GraphOmg& G, int depth, cudaGraph_t body, cudaStream_t* out) {
+  cudaStream_t t = cap_stream(G, depth);
+  XDG_REQUIRE(t != nullptr, XDG_ERR_CUDA, "no capture stream");
+  XDG_TRY_CUDA(cudaStreamBeginCaptureToGraph(t, body, nullptr, nullptr, 0,
+                                             cudaStreamCaptureModeRelaxed));
+  *out = t;
+  return XDG_OK;
+}
+
+int end_body(cudaStream_t t) {
+  cudaGraph_t g;
+  XDG_TRY_CUDA(cudaStreamEndCapture(t, &g));
+  return XDG_OK;
+}
+
+// One rm_step (solvers.py:559-625) of level lam on the candidate z (updated
+// in place), captured on stream s at nesting depth `depth`.
+int cap_rm_step(GraphOmg& G, int lam, double* z, cudaStream_t s, int depth) {
+  xdg_omg_level& lv = G.L[lam];
+  xdg_rm& rm = lv.rm;
+  RmDev* st = G.dev + lam;
+  const int64_t n = rm.n;
+  const double saved = g_bytes;  // rm_step bytes are counted on the device
+  double* w = G.wc + G.wc_off[lam];
+  double* sc = rm.sc;
+  const int mc = rm.max_columns;
+  const xdg_stream_t xs = reinterpret_cast<xdg_stream_t>(s);
+  const int* ncols = &st->ncols;
+  // restart when the space is full (solvers.py:574-575)
+  {
+    cudaGraphConditionalHandle h;
+    XDG_TRY(make_handle(s, &h));
+    rm_dev_pre_kernel<<<1, 1, 0, s>>>(st, mc, h, 80.0 * n, G.gbytes);
+    XDG_CHECK_LAUNCH();
+    cudaGraph_t body;
+    XDG_TRY(add_cond_node(s, h, cudaGraphCondTypeIf, 1, &body));
+    cudaStream_t t;
+    XDG_TRY(begin_body(G, depth + 1, body, &t));
+    rm_dev_restart_kernel<<<grid_for(n, kT, kPerSm), kT, 0, t>>>(n, st, rm.x0, rm.r0, rm.y,
+                                                                  rm.My, rm.x, rm.r);
+    XDG_CHECK_LAUNCH();
+    XDG_TRY(end_body(t));
+  }
+  XDG_TRY(spmv(&lv.M, z, w, nullptr, sc + 0, rm.ws, s));           // w = M z
+  // two classical Gram-Schmidt passes (solvers.py:589-592), columns on the
+  // device (no-ops while the space is empty)
+  double* c1 = rm.coeff;
+  double* c2 = rm.coeff + mc;
+  double* cs = rm.coeff + 2 * (int64_t)mc;
+  XDG_TRY(gemv_t_dev(n, mc, ncols, rm.W, n, w, c1, rm.gemv_ws, s));
+  XDG_TRY(gemv_update2_dev(n, mc, ncols, rm.W, nullptr, n, c1, nullptr, w, nullptr, s));
+  XDG_TRY(gemv_t_dev(n, mc, ncols, rm.W, n, w, c2, rm.gemv_ws, s));
+  XDG_TRY(add_small_dev(mc, ncols, c1, c2, cs, s));
+  XDG_TRY(gemv_update2_dev(n, mc, ncols, rm.W, rm.Z, n, c2, cs, w, z, s));
+  XDG_TRY(xdg_dot(n, w, w, sc + 1, rm.ws, xs));                     // ||w||^2
+  rm_normalize_kernel<<<grid_for(n, kT, kPerSm), kT, 0, s>>>(n, sc + 1, w, z);
+  XDG_CHECK_LAUNCH();
+  XDG_TRY(xdg_dot(n, w, rm.r0, sc + 2, rm.ws, xs));                 // alpha
+  XDG_TRY(spmv(&lv.M, z, rm.Mz, nullptr, nullptr, nullptr, s));    // exact image
+  XDG_TRY(xdg_rm_update(n, rm.r0, rm.My, rm.Mz, sc + 2, rm.My_new, sc + 3, rm.ws, xs));
+  g_bytes = saved;
+  {
+    cudaGraphConditionalHandle h;
+    XDG_TRY(make_handle(s, &h));
+    const double sb = spmv_bytes(&lv.M, false);
+    rm_dev_decide_kernel<<<1, 1, 0, s>>>(st, sc, h, G.gbytes, (double)n, 2.0 * sb,
+                                         8.0 * n * 5, 8.0 * n * 10);
+    XDG_CHECK_LAUNCH();
+    cudaGraph_t bodies[3];
+    XDG_TRY(add_cond_node(s, h, cudaGraphCondTypeSwitch, 3, bodies));
+    cudaStream_t t;
+    XDG_TRY(begin_body(G, depth + 1, bodies[0], &t));             // accept
+    rm_dev_commit_kernel<<<grid_for(n, kT, kPerSm), kT, 0, t>>>(
+        n, st, sc + 2, z, w, rm.y, rm.x0, rm.r0, rm.My_new, rm.My, rm.x, rm.r, rm.Z, rm.W);
+    XDG_CHECK_LAUNCH();
+    XDG_TRY(end_body(t));
+    XDG_TRY(begin_body(G, depth + 1, bodies[1], &t));             // dependent
+    rm_current_kernel<<<grid_for(n, kT, kPerSm), kT, 0, t>>>(n, rm.x0, rm.y, rm.r0, rm.My,
+                                                              rm.x, rm.r);
+    XDG_CHECK_LAUNCH();
+    XDG_TRY(end_body(t));
+    XDG_TRY(begin_body(G, depth + 1, bodies[2], &t));             // rejected
+    rm_dev_restart_kernel<<<grid_for(n, kT, kPerSm), kT, 0, t>>>(n, st, rm.x0, rm.r0, rm.y,
+                                                                  rm.My, rm.x, rm.r);
+    XDG_CHECK_LAUNCH();
+    XDG_TRY(end_body(t));
+  }
+  return XDG_OK;
+}
+
+int cap_direct(xdg_omg_level& lv, const double* b, double* x, cudaStream_t s) {
+  const xdg_direct& D = lv.direct;
+  const xdg_stream_t st = reinterpret_cast<xdg_stream_t>(s);
+  if (D.mf) {
+    count(D.mf->apply_bytes);
+    return xdg_mf_solve(D.mf, b, x, st);
+  }
+  count(8.0 * D.n * (double)D.n + 32.0 * D.n);
+  if (D.task_sys)
+    return xdg_lu_inv_apply_tasks(D.ntasks, D.task_sys, D.task_row0, D.rows_per_task,
+                                  D.max_dim, D.n, D.zero_off, D.dims, D.zero_off, D.LU,
+                                  D.perm, b, x, D.scratch, st);
+  return xdg_lu_inv_apply(1, D.n, D.row_sys, D.zero_off, D.dims, D.zero_off, D.LU, D.perm, b,
+                          x, D.scratch, st);
+}
+
+// Level lam (not the coarsest) solving for b into x (solvers.py:696-738),
+// captured on s at depth `depth`.
+int cap_level(GraphOmg& G, int lam, const double* b, double* x, int has_x0, cudaStream_t s,
+              int depth) {
+  xdg_omg_level& lv = G.L[lam];
+  xdg_rm& rm = lv.rm;
+  RmDev* st = G.dev + lam;
+  const int64_t n = (int64_t)lv.M.nbr * lv.M.N;
+  const bool entry = lam == G.entry;
+  double* hist = entry ? G.hist : nullptr;
+  if (!has_x0) {
+    zero2_kernel<<<grid_for(n, kT, kPerSm), kT, 0, s>>>(n, x, nullptr);
+    XDG_CHECK_LAUNCH();
+  }
+  XDG_TRY(spmv(&lv.M, x, rm.r, b, nullptr, nullptr, s));          // r = b - M x
+  // RmState(x, r)
+  count(48.0 * n);
+  copy_kernel<<<grid_for(n, kT, kPerSm), kT, 0, s>>>(n, x, rm.x0);
+  XDG_CHECK_LAUNCH();
+  copy_kernel<<<grid_for(n, kT, kPerSm), kT, 0, s>>>(n, rm.r, rm.r0);
+  XDG_CHECK_LAUNCH();
+  zero2_kernel<<<grid_for(n, kT, kPerSm), kT, 0, s>>>(n, rm.y, rm.My);
+  XDG_CHECK_LAUNCH();
+  XDG_TRY(xdg_dot(n, rm.r0, rm.r0, rm.sc + 7, rm.ws, reinterpret_cast<xdg_stream_t>(s)));
+  cudaGraphConditionalHandle h;
+  XDG_TRY(make_handle(s, &h));
+  rm_dev_init_kernel<<<1, 1, 0, s>>>(st, rm.sc + 7, entry ? G.max_it : G.coarse_it, G.tol,
+                                     hist, h);
+  XDG_CHECK_LAUNCH();
+  cudaGraph_t body;
+  XDG_TRY(add_cond_node(s, h, cudaGraphCondTypeWhile, 1, &body));
+  cudaStream_t t;
+  XDG_TRY(begin_body(G, depth + 1, body, &t));
+  const double b0 = g_bytes;
+  xdg_omg_level& nx = G.L[lam + 1];
+  const bool coarsest_next = lam + 1 == G.nlevels - 1 || !nx.has_restriction;
+  XDG_TRY(pmg_apply_op(&lv.schwarz, &lv.M, rm.r, lv.z, t));
+  XDG_TRY(cap_rm_step(G, lam, lv.z, t, depth + 1));
+  XDG_TRY(spmv(&lv.Rt, rm.r, nx.b, nullptr, nullptr, nullptr, t));  // r_c = R^T r
+  if (coarsest_next)
+    XDG_TRY(cap_direct(nx, nx.b, nx.rm.x, t));
+  else
+    XDG_TRY(cap_level(G, lam + 1, nx.b, nx.rm.x, 0, t, depth + 1));
+  XDG_TRY(spmv(&lv.R, nx.rm.x, lv.xf, nullptr, nullptr, nullptr, t));
+  XDG_TRY(cap_rm_step(G, lam, lv.xf, t, depth + 1));
+  XDG_TRY(pmg_apply_op(&lv.schwarz, &lv.M, rm.r, lv.z, t));
+  XDG_TRY(cap_rm_step(G, lam, lv.z, t, depth + 1));
+  const double body_bytes = g_bytes - b0;
+  g_bytes = b0;
+  level_loop_end_kernel<<<1, 1, 0, t>>>(st, G.tol, hist, h, G.gbytes, body_bytes);
+  XDG_CHECK_LAUNCH();
+  XDG_TRY(end_body(t));
+  if (x != rm.x) {
+    copy_if_ran_kernel<<<grid_for(n, kT, kPerSm), kT, 0, s>>>(n, st, rm.x, x);
+    XDG_CHECK_LAUNCH();
+  }
+  return XDG_OK;
+}
+
+bool omg_graph_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("XDG_OMG_GRAPH");
+    return e == nullptr || atoi(e) != 0;
+  }();
+  return on;
+}
+
+// Whole solve as one graph launch.  Returns XDG_OK with the outputs filled.
+int omg_solve_graph(xdg_omg_level* levels, int nlevels, int entry, double tolerance,
+                    int max_iterations, int coarse_cycle_iterations, const double* b,
+                    double* x, int has_x0, int* iterations, double* history, int* hist_len,
+                    double* final_residual, cudaStream_t s) {
+  GraphOmg G;
+  G.L = levels;
+  G.nlevels = nlevels;
+  G.entry = entry;
+  G.tol = tolerance;
+  G.max_it = max_iterations;
+  G.coarse_it = coarse_cycle_iterations;
+  // device state: RmDev per level, candidate-w scratch per level, history,
+  // byte counter
+  int64_t tot = 0;
+  G.wc_off.assign(nlevels, 0);
+  for (int l = 0; l < nlevels; ++l) {
+    G.wc_off[l] = tot;
+    tot += (int64_t)levels[l].M.nbr * levels[l].M.N;
+  }
+  const size_t bytes_state = sizeof(RmDev) * nlevels;
+  const size_t bytes_all = bytes_state + sizeof(double) * (tot + max_iterations + 2 + 1);
+  char* buf = nullptr;
+  XDG_TRY_CUDA(cudaMallocAsync(&buf, bytes_all, s));
+  XDG_TRY_CUDA(cudaMemsetAsync(buf, 0, bytes_all, s));
+  G.dev = reinterpret_cast<RmDev*>(buf);
+  G.wc = reinterpret_cast<double*>(buf + bytes_state);
+  G.hist = G.wc + tot;
+  G.gbytes = G.hist + max_iterations + 2;
+  cudaStream_t s0 = cap_stream(G, 0);
+  int st = XDG_OK;
+  cudaGraphExec_t exec = nullptr;
+  cudaGraph_t graph = nullptr;
+  if (s0 == nullptr) {
+    st = XDG_ERR_CUDA;
+  } else {
+    // the capture stream waits for the caller's stream (allocation, memset)
+    cudaEvent_t ev;
+    cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    cudaEventRecord(ev, s);
+    cudaStreamWaitEvent(s0, ev, 0);
+    cudaEventDestroy(ev);
+    XDG_TRY_CUDA(cudaStreamBeginCapture(s0, cudaStreamCaptureModeRelaxed));
+    st = cap_level(G, entry, b, x, has_x0, s0, 0);
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(s0, &g);
+    if (st == XDG_OK && e != cudaSuccess) {
+      set_error("graph capture: %s", cudaGetErrorString(e));
+      st = XDG_ERR_CUDA;
+    }
+    graph = g;
+    if (st == XDG_OK) {
+      e = cudaGraphInstantiate(&exec, graph, 0);
+      if (e != cudaSuccess) {
+        set_error("graph instantiate: %s", cudaGetErrorString(e));
+        st = XDG_ERR_CUDA;
+      }
+    }
+    if (st == XDG_OK) {
+      e = cudaGraphLaunch(exec, s);
+      if (e != cudaSuccess) {
+        set_error("graph launch: %s", cudaGetErrorString(e));
+        st = XDG_ERR_CUDA;
+      }
+    }
+  }
+  RmDev top;
+  double dbytes = 0.0;
+  if (st == XDG_OK) {
+    cudaError_t e = cudaMemcpyAsync(&top, G.dev + entry, sizeof(RmDev), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&dbytes, G.gbytes, sizeof(double),
+                                              cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e == cudaSuccess) {
+      *iterations = top.it;
+      *hist_len = top.it + 1;
+      e = cudaMemcpy(history, G.hist, sizeof(double) * (top.it + 1), cudaMemcpyDeviceToHost);
+    }
+    if (e != cudaSuccess) {
+      set_error("graph readback: %s", cudaGetErrorString(e));
+      st = XDG_ERR_CUDA;
+    }
+    *final_residual = top.last;
+    // level state back into the host structs (counters the Python side reads)
+    xdg_rm& rm = levels[entry].rm;
+    rm.ncols = top.ncols;
+    rm.best_norm = top.best_norm;
+    rm.last_dependent = top.last_dependent;
+    rm.dependent_count = top.dependent_count;
+    rm.rejected_count = top.rejected_count;
+    rm.restart_count = top.restart_count;
+    g_bytes += dbytes;
+  }
+  if (exec) cudaGraphExecDestroy(exec);
+  if (graph) cudaGraphDestroy(graph);
+  cudaFreeAsync(buf, s);
+  for (cudaStream_t t : G.streams) cudaStreamDestroy(t);
+  return st;
+}
+
+}  // namespace omg_graph
+}  // namespace xdg
+
+using xdg::omg_graph::omg_graph_enabled;
+using xdg::omg_graph::omg_solve_graph;
+
 
 extern "C" int xdg_omg_solve(xdg_omg_level* levels, int nlevels, int entry,
                              double tolerance, int max_iterations,
@@ -475,13 +986,21 @@ extern "C" int xdg_omg_solve(xdg_omg_level* levels, int nlevels, int entry,
                              double* history, int* hist_len,
                              double* final_residual, double* bytes_out,
                              xdg_stream_t stream) {
+  NvtxRange nv("xdg_omg_solve");
   g_bytes = 0.0;
   XDG_REQUIRE(nlevels >= 1 && entry >= 0 && entry < nlevels, XDG_ERR_ARG,
               "bad level range");
   OmgRun R{levels, nlevels, entry, tolerance, max_iterations,
            coarse_cycle_iterations, reinterpret_cast<cudaStream_t>(stream)};
-  int st = omg_level(R, entry, b, x, has_x0, iterations, history, hist_len,
-                     final_residual);
+  const bool coarsest = entry == nlevels - 1 || !levels[entry].has_restriction;
+  // one CUDA graph with device-side control flow (XDG_OMG_GRAPH=0: the
+  // host-decision driver, same arithmetic)
+  int st = (omg_graph_enabled() && !coarsest)
+               ? omg_solve_graph(levels, nlevels, entry, tolerance, max_iterations,
+                                 coarse_cycle_iterations, b, x, has_x0, iterations, history,
+                                 hist_len, final_residual, R.s)
+               : omg_level(R, entry, b, x, has_x0, iterations, history, hist_len,
+                           final_residual);
   if (st != XDG_OK) return st;
   XDG_TRY_CUDA(cudaStreamSynchronize(R.s));
   if (bytes_out) *bytes_out = g_bytes;
@@ -534,6 +1053,7 @@ extern "C" int xdg_gmres_solve(const xdg_bsr* M, const xdg_pmg* pmg,
                                void* gemv_ws, int* iterations, double* history,
                                int* hist_len, double* final_residual,
                                double* bytes_out, xdg_stream_t stream) {
+  NvtxRange nv("xdg_gmres_solve");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   g_bytes = 0.0;
   const int m = restart;
@@ -564,7 +1084,8 @@ extern "C" int xdg_gmres_solve(const xdg_bsr* M, const xdg_pmg* pmg,
       double* Zj = Zb + (int64_t)j * n;
       XDG_TRY(pmg_apply_op(pmg, M, Vj, Zj, s));
       XDG_TRY(spmv(M, Zj, w, nullptr, nullptr, nullptr, s));
-      count(8.0 * n * (3.0 * (j + 1) + 3.0));
+      // MGS of iteration j moves 8 n (2 (j + 1) + 3) bytes
+      count(8.0 * n * (2.0 * (j + 1) + 3.0));
       XDG_TRY(xdg_mgs(n, j, V, n, w, sc, ws, stream));
       XDG_TRY_CUDA(sync_read(hc.data(), sc, j + 2, s));
       for (int i = 0; i <= j + 1; ++i) Hc(i, j) = hc[i];

@@ -516,6 +516,7 @@ extern "C" int xdg_batched_factor(int64_t nmat, const int64_t* off, const int* n
                                   double* A, int* perm, const int64_t* perm_off, int* info,
                                   int invert, double* ws, xdg_stream_t stream) {
   if (nmat <= 0 || max_p <= 0) return XDG_OK;
+  NvtxRange nv("xdg_batched_factor");
   XDG_REQUIRE(max_p <= max_n && nmat < 65536, XDG_ERR_ARG,
               "bad batch: nmat=%lld max_n=%d max_p=%d (nmat < 65536 per call)",
               (long long)nmat, max_n, max_p);

@@ -64,8 +64,29 @@ scatter_add_blocks_kernel(int64_t nidx, int N, const int* __restrict__ idx,
   }
 }
 
+__global__ void __launch_bounds__(kT)
+scatter_blocks_kernel(int64_t nidx, int N, const int* __restrict__ idx,
+                      const double* __restrict__ src, double* __restrict__ y) {
+  const int64_t total = nidx * N;
+  for (int64_t t = (int64_t)blockIdx.x * kT + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * kT) {
+    const int64_t k = t / N;
+    y[(int64_t)idx[k] * N + (t - k * N)] = src[t];
+  }
+}
+
 }  // namespace
 }  // namespace xdg
+
+extern "C" int xdg_scatter_blocks(int64_t nidx, int N, const int* idx, const double* src,
+                                  double* y, xdg_stream_t stream) {
+  using namespace xdg;
+  if (nidx <= 0) return XDG_OK;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  scatter_blocks_kernel<<<grid_for(nidx * N, kT, 8), kT, 0, s>>>(nidx, N, idx, src, y);
+  XDG_CHECK_LAUNCH();
+  return XDG_OK;
+}
 
 extern "C" int xdg_scatter_add_blocks(int64_t nidx, int N, const int* idx,
                                       const double* src, double* y,

@@ -418,32 +418,43 @@ int launch_rows(const xdg_mf* mf, int h, double* x, cudaStream_t s) {
 
 extern "C" int xdg_mf_rows_per_warp(void) { return xdg::kMR; }
 
-extern "C" int xdg_mf_solve(const xdg_mf* mf, const double* b, double* x,
-                            xdg_stream_t stream) {
+extern "C" int xdg_mf_solve_phase(const xdg_mf* mf, const double* b, double* x, int phase,
+                                  xdg_stream_t stream) {
   using namespace xdg;
-  XDG_REQUIRE(mf != nullptr && mf->nlevels >= 0, XDG_ERR_ARG, "bad multifrontal plan");
+  XDG_REQUIRE(mf != nullptr && mf->nlevels >= 0 && phase >= 1 && phase <= 3, XDG_ERR_ARG,
+              "bad multifrontal plan / phase");
+  NvtxRange nv("xdg_mf_solve");
   if (mf->total == 0 || mf->nlevels == 0) return XDG_OK;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int H = mf->nlevels;
   const int HF = mf->fuse_levels;  // levels [0, HF) run as fused batches
-  for (int k = 0; k < mf->nfbatch; ++k) XDG_TRY(launch_fused<true>(mf, k, b, x, s));
-  for (int h = HF; h < H; ++h) {
-    const int64_t e0 = mf->lev_ent[h], e1 = mf->lev_ent[h + 1];
-    if (e1 > e0) {
-      mf_gather_kernel<<<grid_for(e1 - e0, kT, 8), kT, 0, s>>>(
-          e0, e1, mf->ent_w, mf->ent_src, mf->ent_cptr, mf->ent_cidx, mf->ent_scale, b,
-          mf->C, mf->W);
-      XDG_CHECK_LAUNCH();
+  if (phase & 1) {  // forward: gather, lower, bound per height
+    for (int k = 0; k < mf->nfbatch; ++k) XDG_TRY(launch_fused<true>(mf, k, b, x, s));
+    for (int h = HF; h < H; ++h) {
+      const int64_t e0 = mf->lev_ent[h], e1 = mf->lev_ent[h + 1];
+      if (e1 > e0) {
+        mf_gather_kernel<<<grid_for(e1 - e0, kT, 8), kT, 0, s>>>(
+            e0, e1, mf->ent_w, mf->ent_src, mf->ent_cptr, mf->ent_cidx, mf->ent_scale, b,
+            mf->C, mf->W);
+        XDG_CHECK_LAUNCH();
+      }
+      XDG_TRY(launch_rows<kLower>(mf, h, x, s));
+      XDG_TRY(launch_rows<kBound>(mf, h, x, s));
     }
-    XDG_TRY(launch_rows<kLower>(mf, h, x, s));
-    XDG_TRY(launch_rows<kBound>(mf, h, x, s));
   }
-  for (int h = H - 1; h >= HF; --h) {
-    XDG_TRY(launch_rows<kUpb>(mf, h, x, s));
-    XDG_TRY(launch_rows<kUpper>(mf, h, x, s));
+  if (phase & 2) {  // backward: upb, upper per height
+    for (int h = H - 1; h >= HF; --h) {
+      XDG_TRY(launch_rows<kUpb>(mf, h, x, s));
+      XDG_TRY(launch_rows<kUpper>(mf, h, x, s));
+    }
+    for (int k = mf->nfbatch - 1; k >= 0; --k) XDG_TRY(launch_fused<false>(mf, k, b, x, s));
   }
-  for (int k = mf->nfbatch - 1; k >= 0; --k) XDG_TRY(launch_fused<false>(mf, k, b, x, s));
   return XDG_OK;
+}
+
+extern "C" int xdg_mf_solve(const xdg_mf* mf, const double* b, double* x,
+                            xdg_stream_t stream) {
+  return xdg_mf_solve_phase(mf, b, x, 3, stream);
 }
 
 // Setup: extend-add of the children's Schur complements into their parents'

@@ -155,8 +155,11 @@ constexpr int kMaxTiles = 4096;
 
 __global__ void __launch_bounds__(kT)
 gemv_t_partial(int64_t L, int ncols, const double* __restrict__ W, int64_t ldw,
-               const double* __restrict__ w, double* __restrict__ partial) {
+               const double* __restrict__ w, double* __restrict__ partial,
+               const int* __restrict__ ncols_dev) {
   __shared__ double ws[kTile];
+  if (ncols_dev) ncols = min(ncols, *ncols_dev);  // device-resident column count
+  if (ncols <= 0) return;
   const int ntiles = gridDim.x;
   const int64_t rows_per = ((L + ntiles - 1) / ntiles + 31) / 32 * 32;
   const int64_t lo = (int64_t)blockIdx.x * rows_per;
@@ -193,8 +196,9 @@ gemv_t_partial(int64_t L, int ncols, const double* __restrict__ W, int64_t ldw,
 
 __global__ void gemv_t_final(int ncols, int nparts,
                              const double* __restrict__ partial,
-                             double* __restrict__ coeff) {
+                             double* __restrict__ coeff, const int* __restrict__ ncols_dev) {
   // one warp per column, fixed order
+  if (ncols_dev) ncols = min(ncols, *ncols_dev);
   const int c = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (c >= ncols) return;
@@ -211,8 +215,11 @@ __global__ void __launch_bounds__(kT)
 gemv_update2_kernel(int64_t L, int ncols, const double* __restrict__ W,
                     const double* __restrict__ Z, int64_t ld,
                     const double* __restrict__ cw, const double* __restrict__ cz,
-                    double* __restrict__ w, double* __restrict__ z) {
+                    double* __restrict__ w, double* __restrict__ z,
+                    const int* __restrict__ ncols_dev) {
   extern __shared__ double sc[];
+  if (ncols_dev) ncols = min(ncols, *ncols_dev);
+  if (ncols <= 0) return;  // uniform: no column, no update
   double* scw = sc;
   double* scz = sc + ncols;
   for (int c = threadIdx.x; c < ncols; c += kT) {
@@ -246,7 +253,9 @@ gemv_update2_kernel(int64_t L, int ncols, const double* __restrict__ W,
   }
 }
 
-__global__ void add_small_kernel(int n, const double* a, const double* b, double* out) {
+__global__ void add_small_kernel(int n, const double* a, const double* b, double* out,
+                                 const int* n_dev) {
+  if (n_dev) n = min(n, *n_dev);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     out[i] = a[i] + b[i];
 }
@@ -374,9 +383,9 @@ extern "C" int xdg_gemv_t(int64_t L, int ncols, const double* W, int64_t ldw,
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int parts = gemv_t_parts(L);
   double* partial = static_cast<double*>(ws);
-  gemv_t_partial<<<parts, kT, 0, s>>>(L, ncols, W, ldw, w, partial);
+  gemv_t_partial<<<parts, kT, 0, s>>>(L, ncols, W, ldw, w, partial, nullptr);
   XDG_CHECK_LAUNCH();
-  gemv_t_final<<<(ncols + 7) / 8, 256, 0, s>>>(ncols, parts, partial, coeff);
+  gemv_t_final<<<(ncols + 7) / 8, 256, 0, s>>>(ncols, parts, partial, coeff, nullptr);
   XDG_CHECK_LAUNCH();
   return XDG_OK;
 }
@@ -397,7 +406,7 @@ extern "C" int xdg_gemv_update2(int64_t L, int ncols, const double* W,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
   gemv_update2_kernel<<<grid_for(L, kT, kPerSm), kT, smem, s>>>(
-      L, ncols, W, Z, ld, coeff, coeff_z ? coeff_z : coeff, w, z);
+      L, ncols, W, Z, ld, coeff, coeff_z ? coeff_z : coeff, w, z, nullptr);
   XDG_CHECK_LAUNCH();
   return XDG_OK;
 }
@@ -406,7 +415,51 @@ extern "C" int xdg_add_small(int n, const double* a, const double* b,
                              double* out, xdg_stream_t stream) {
   if (n <= 0) return XDG_OK;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  add_small_kernel<<<(n + 255) / 256, 256, 0, s>>>(n, a, b, out);
+  add_small_kernel<<<(n + 255) / 256, 256, 0, s>>>(n, a, b, out, nullptr);
   XDG_CHECK_LAUNCH();
   return XDG_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Device-resident column counts (the graph-captured ortho_mg_solve: the RM
+// space's column count lives on the device; launches are sized for
+// max_cols and the kernels read the actual count).  Same grids and the same
+// arithmetic as the host-count entry points above: bit-identical results.
+namespace xdg {
+
+int gemv_t_dev(int64_t L, int max_cols, const int* ncols_dev, const double* W, int64_t ldw,
+               const double* w, double* coeff, void* ws, cudaStream_t s) {
+  if (max_cols <= 0 || L <= 0) return XDG_OK;
+  const int parts = gemv_t_parts(L);
+  double* partial = static_cast<double*>(ws);
+  gemv_t_partial<<<parts, kT, 0, s>>>(L, max_cols, W, ldw, w, partial, ncols_dev);
+  XDG_CHECK_LAUNCH();
+  gemv_t_final<<<(max_cols + 7) / 8, 256, 0, s>>>(max_cols, parts, partial, coeff, ncols_dev);
+  XDG_CHECK_LAUNCH();
+  return XDG_OK;
+}
+
+int gemv_update2_dev(int64_t L, int max_cols, const int* ncols_dev, const double* W,
+                     const double* Z, int64_t ld, const double* cw, const double* cz,
+                     double* w, double* z, cudaStream_t s) {
+  if (max_cols <= 0 || L <= 0) return XDG_OK;
+  XDG_REQUIRE(max_cols <= 6000, XDG_ERR_ARG, "gemv_update2: ncols %d too large", max_cols);
+  const size_t smem = 2 * max_cols * sizeof(double);
+  if (smem > 48 * 1024)
+    XDG_TRY_CUDA(cudaFuncSetAttribute(gemv_update2_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  gemv_update2_kernel<<<grid_for(L, kT, kPerSm), kT, smem, s>>>(L, max_cols, W, Z, ld, cw,
+                                                                cz ? cz : cw, w, z, ncols_dev);
+  XDG_CHECK_LAUNCH();
+  return XDG_OK;
+}
+
+int add_small_dev(int max_n, const int* n_dev, const double* a, const double* b, double* out,
+                  cudaStream_t s) {
+  if (max_n <= 0) return XDG_OK;
+  add_small_kernel<<<(max_n + 255) / 256, 256, 0, s>>>(max_n, a, b, out, n_dev);
+  XDG_CHECK_LAUNCH();
+  return XDG_OK;
+}
+
+}  // namespace xdg

@@ -109,14 +109,17 @@ class SparseDirect:
     """Device multifrontal factor of one square uniform-block DeviceBSR:
     apply(b_dev) -> x_dev (same interface as DeviceDirect)."""
 
-    def __init__(self, D, ctx, what="matrix"):
+    def __init__(self, D, ctx, what="matrix", comm=None):
         from .multifrontal import Multifrontal
 
         self.ctx = ctx
         self.n = D.nbr * D.N
         v = np.arange(D.nbr, dtype=np.int64) * D.N
+        # comm (dist_solvers.Comm, world > 1): subtrees of the elimination
+        # forest distributed over the ranks, top fronts replicated
         self.mf = Multifrontal(ctx, D.row_ptr.cpu().numpy(), D.col.cpu().numpy(), D.val_t,
-                               D.N, [np.arange(D.nbr, dtype=np.int64)], D.N, v, v, what=what)
+                               D.N, [np.arange(D.nbr, dtype=np.int64)], D.N, v, v, what=what,
+                               comm=comm)
 
     def apply(self, b: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         if out is None:

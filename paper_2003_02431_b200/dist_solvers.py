@@ -23,6 +23,7 @@ kernel ever waits on another rank).
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 from time import perf_counter
 
@@ -113,8 +114,11 @@ def local_operator(rp, col, val, N, row_starts, rank, ctx) -> LocalOperator:
 
 class DistPmg:
     """Degree-separated preconditioner over ALL cells (the GMRES-PMG cell
-    set, solvers.py:800), distributed: replicated global low-order solve +
-    rank-local high-order stage."""
+    set, solvers.py:800), distributed: the global low-order solve through
+    the multifrontal factor whose elimination subtrees are mapped to the
+    ranks (each rank factors and stores only its subtrees plus the shared
+    top fronts: multifrontal.proportional_map), or a replicated dense factor
+    for small systems; the high-order stage is rank-local."""
 
     def __init__(self, rp, col, val, N, m, op: LocalOperator, row_starts, comm: Comm, ctx):
         self.ctx, self.comm, self.op = ctx, comm, op
@@ -124,12 +128,14 @@ class DistPmg:
         nloc = op.r1 - op.r0
         self.nloc = nloc
         self.counts = [int(row_starts[q + 1] - row_starts[q]) * m for q in range(comm.world)]
-        # replicated low-order factor from the global blocks' (:m, :m) parts
+        # low-order factor from the global blocks' (:m, :m) parts
         lo_val = np.ascontiguousarray(np.asarray(val)[:, :m, :m])
         Dlo = DeviceBSR.from_arrays(rp, col, lo_val, m, nbr, ctx)
+        mode = os.environ.get("XDG_LOW_ORDER", "auto")
+        sparse = mode == "sparse" or (mode != "dense" and nbr * m > SPARSE_DIRECT_MIN)
         try:
-            if nbr * m > SPARSE_DIRECT_MIN:  # multifrontal (cfg2: 336,610 unknowns)
-                self.low = SparseDirect(Dlo, ctx, "low-order system")
+            if sparse:  # multifrontal (cfg2: 336,610 unknowns), subtrees over the ranks
+                self.low = SparseDirect(Dlo, ctx, "low-order system", comm=comm)
             else:
                 A = dense_from_device_bsr(Dlo)
                 self.low = DeviceDirect(A, ctx, "low-order system")

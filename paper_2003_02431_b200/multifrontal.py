@@ -318,6 +318,52 @@ def nested_dissection_py(g_ptr, g_col, nv, leaf):
     return nd.P, nd.kids
 
 
+def proportional_map(kids, parent, work, world: int, slack: float = 1.1) -> np.ndarray:
+    """Subtree-to-rank mapping of an elimination forest (post-ordered: a
+    subtree is the contiguous id range ending at its root) for `world`
+    ranks: rank_of[t] = the rank owning front t with its whole subtree, or
+    -1 for a shared top front (factored and solved redundantly on every
+    rank).  The candidate subtrees start as the forest's roots; while the
+    heaviest candidate (subtree factor bytes) exceeds `slack` x the average
+    share of a rank, it becomes shared and its children replace it; the
+    candidates then go to the least-loaded rank, heaviest first (LPT).
+    Deterministic: every rank computes the same map."""
+    nn = len(parent)
+    rank_of = np.full(nn, -1, np.int64)
+    if nn == 0:
+        return rank_of
+    sub = np.asarray(work, np.float64).copy()
+    size = np.ones(nn, np.int64)
+    for t in range(nn):
+        if parent[t] >= 0:
+            sub[parent[t]] += sub[t]
+            size[parent[t]] += size[t]
+    cand = [t for t in range(nn) if parent[t] < 0]
+    while True:
+        tot = sum(sub[t] for t in cand)
+        h = max(cand, key=lambda t: (sub[t], t))
+        if world == 1 or not kids[h] or sub[h] <= slack * tot / world:
+            break
+        cand.remove(h)
+        cand += list(kids[h])
+    load = np.zeros(world)
+    for t in sorted(cand, key=lambda t: (-sub[t], t)):
+        r = int(np.argmin(load))
+        load[r] += sub[t]
+        rank_of[t - size[t] + 1:t + 1] = r
+    # a shared front all of whose subtrees landed on one rank is owned by it
+    below = {}
+    for t in range(nn):  # post-order: children first
+        if rank_of[t] < 0:
+            rs = set()
+            for c in kids[t]:
+                rs |= below[c] if rank_of[c] < 0 else {int(rank_of[c])}
+            if len(rs) == 1:
+                rank_of[t] = rs.pop()
+            below[t] = rs if rank_of[t] < 0 else set()
+    return rank_of
+
+
 def _group(n: int) -> int:
     """Lanes per row for rows of length n: the smallest power of two with
     8 loads per lane covering the row, at most a warp."""
@@ -345,7 +391,7 @@ class Multifrontal:
 
     def __init__(self, ctx, rp, col, val_t, N, sets, m, vsrc, vdst,
                  leaf_unknowns: int = 100, what: str = "system",
-                 equilibrate: bool = True, front_factor=None):
+                 equilibrate: bool = True, front_factor=None, comm=None):
         import time
 
         t0 = time.perf_counter()
@@ -378,6 +424,25 @@ class Multifrontal:
         self.nlevels = H
         pp = np.array([_pad(int(x)) for x in pn], np.int64)
         bp = np.array([_pad(int(x)) if x else 0 for x in bn], np.int64)
+        # multi-GPU (comm with world > 1): subtree-to-rank proportional
+        # mapping; a rank factors and solves its owned subtrees plus the
+        # shared top fronts (replicated), see proportional_map
+        self.comm = comm if (comm is not None and comm.world > 1) else None
+        if self.comm is not None:
+            work = (pn * pn + 2 * pn * bn).astype(np.float64)
+            self.rank_of = proportional_map(kids, parent, work, self.comm.world)
+            me = self.comm.rank
+            need = (self.rank_of == me) | (self.rank_of < 0)
+        else:
+            self.rank_of = np.zeros(nn, np.int64)
+            need = np.ones(nn, bool)
+        self.need = need
+        # roots of owned subtrees whose parent is a shared front: their Schur
+        # complements / contributions cross ranks (sorted by (rank, id))
+        xroot = np.flatnonzero((self.rank_of >= 0) & (parent >= 0) & (bn > 0)
+                               & (self.rank_of[np.maximum(parent, 0)] < 0))
+        xroot = xroot[np.lexsort((xroot, self.rank_of[xroot]))] if len(xroot) else xroot
+        self.xroot = xroot
 
         # position of every vertex inside its owner's P; B positions by key
         ppos = np.empty(nv, np.int64)
@@ -406,14 +471,18 @@ class Multifrontal:
         t1 = time.perf_counter()
         # ---- factor storage / workspace layout ---------------------------
         order = np.lexsort((np.arange(nn), height))  # by height, then id
-        buckets = {}  # (h, pp, bp) -> node list
+        buckets = {}  # (h, pp, bp) -> node list: fronts of the first pass
+        buckets_sh = {}  # the shared (replicated) top fronts: second pass
+        shared = self.rank_of < 0
         for t in order:
-            buckets.setdefault((int(height[t]), int(pp[t]), int(bp[t])), []).append(int(t))
+            if need[t]:
+                (buckets_sh if shared[t] else buckets).setdefault(
+                    (int(height[t]), int(pp[t]), int(bp[t])), []).append(int(t))
         inv_off = np.zeros(nn, np.int64)
         lbp_off = np.zeros(nn, np.int64)
         upb_off = np.zeros(nn, np.int64)
         fst = 0
-        for (h, P_, B_), ts in buckets.items():
+        for (h, P_, B_), ts in list(buckets.items()) + list(buckets_sh.items()):
             nb = len(ts)
             inv_off[ts] = fst + np.arange(nb) * P_ * P_
             fst += nb * P_ * P_
@@ -422,11 +491,14 @@ class Multifrontal:
             upb_off[ts] = fst + np.arange(nb) * P_ * B_
             fst += nb * P_ * B_
         # the padded factors plus the largest height's front buffer must fit
-        front_max = max((sum(len(ts) * (P_ + B_) ** 2 for (hh, P_, B_), ts in buckets.items()
-                             if hh == h) for h in range(H)), default=0)
+        front_max = max((sum(len(ts) * (P_ + B_) ** 2 for bk in (buckets, buckets_sh)
+                             for (hh, P_, B_), ts in bk.items() if hh == h)
+                         for h in range(H)), default=0)
+        # received Schur complements of the cross-rank subtree roots
+        xs_sz = int(sum(int(bn[t]) ** 2 for t in self.xroot))
         free = (torch.cuda.mem_get_info(dev)[0] if torch.device(dev).type == "cuda"
                 else float("inf"))
-        if 8 * (fst + 2 * front_max) > free:
+        if 8 * (fst + 2 * front_max + xs_sz) > free:
             raise NotImplementedError(
                 f"multifrontal {what}: factors need {8 * fst / 1e9:.1f} GB + fronts "
                 f"{8 * front_max / 1e9:.1f} GB, {free / 1e9:.1f} GB of HBM free "
@@ -465,103 +537,141 @@ class Multifrontal:
         fronts = {}  # h -> flat tensor;  node -> (h, base, stride)
         fbase = np.zeros(nn, np.int64)
         fstride = pp + bp
-        last_use = np.full(H, -1, np.int64)
-        for t in range(nn):
-            if parent[t] >= 0:
-                last_use[height[t]] = max(last_use[height[t]], height[parent[t]])
+        cpad = pp.copy()          # pivot padding of a child's stored Schur complement
+        ckey = height.copy()      # fronts[] key of a child's stored Schur complement
         perms = [None] * nn
         # extend-add on the device (xdg_mf_extend_add) or, XDG_MF_EXTEND=torch
         # / host plans, by per-child indexed adds (bit-identical)
         ext_kernel = (ctx is not None and torch.device(dev).type == "cuda"
                       and os.environ.get("XDG_MF_EXTEND", "kernel") == "kernel")
+        if self.comm is not None and not ext_kernel:
+            raise NotImplementedError("the multi-GPU factorization needs the device extend-add")
         bad_nodes, dev_perms = [], []
-        for h in range(H):
-            hb = [(k, ts) for k, ts in buckets.items() if k[0] == h]
-            size = 0
-            for (_, P_, B_), ts in hb:
-                fbase[ts] = size + np.arange(len(ts)) * (P_ + B_) ** 2
-                size += len(ts) * (P_ + B_) ** 2
-            flat = torch.zeros(max(size, 1), dtype=F64, device=dev)
-            fronts[h] = flat
-            # identity on the pivot padding
-            pad_idx = []
-            for (_, P_, B_), ts in hb:
-                for t in ts:
-                    if pn[t] < P_:
-                        i = np.arange(pn[t], P_)
-                        pad_idx.append(fbase[t] + i * (P_ + B_) + i)
-            if pad_idx:
-                flat[torch.from_numpy(np.concatenate(pad_idx)).to(dev)] = 1.0
-            # original entries whose earlier-eliminated end is a front of h
-            sel = np.flatnonzero(a_h == h)
-            if sel.size:
-                nd_ = a_node[sel]
-                rpos = front_pos(nd_, G.a_row[sel])
-                cpos = front_pos(nd_, G.a_col[sel])
-                st = fstride[nd_]
-                am = np.arange(m)
-                tgt = (fbase[nd_][:, None, None] + (rpos[:, None, None] + am[None, :, None])
-                       * st[:, None, None] + cpos[:, None, None] + am[None, None, :])
-                ks = torch.from_numpy(G.a_k[sel]).to(dev)
-                blocks = vblk[ks][:, :m, :m].transpose(1, 2)
-                sr = scale.view(nv, m)[torch.from_numpy(G.a_row[sel]).to(dev)]
-                scl = scale.view(nv, m)[torch.from_numpy(G.a_col[sel]).to(dev)]
-                blocks = blocks * sr[:, :, None] * scl[:, None, :]
-                flat[torch.from_numpy(tgt.reshape(-1)).to(dev)] = blocks.reshape(-1)
-            # children's Schur complements (extend-add), child by child
-            if ext_kernel:
-                self._extend_add(ctx, hb, kids, bn, pp, fbase, fstride, height, fronts, flat,
-                                 B_list, front_pos, m)
-            for t in (t for (_, _, _), ts in hb for t in ts if not ext_kernel):
-                if not kids[t]:
+        xpos = {int(t): i for i, t in enumerate(self.xroot)}
+        xsend = []  # this rank's cross-rank roots' Schur complements, in xroot order
+        for pass_buckets in (buckets, buckets_sh):
+            if not pass_buckets:
+                continue
+            in_pass = np.zeros(nn, bool)
+            for ts in pass_buckets.values():
+                in_pass[ts] = True
+            last_use = np.full(H, -1, np.int64)
+            for t in np.flatnonzero(in_pass):
+                if parent[t] >= 0 and in_pass[parent[t]]:
+                    last_use[height[t]] = max(last_use[height[t]], height[parent[t]])
+            for h in range(H):
+                hb = [(k, ts) for k, ts in pass_buckets.items() if k[0] == h]
+                if not hb:
+                    for hh in range(h + 1):
+                        if hh in fronts and last_use[hh] <= h:
+                            del fronts[hh]
                     continue
-                Ft = flat[fbase[t]:fbase[t] + fstride[t] ** 2].view(fstride[t], fstride[t])
-                for c in kids[t]:
-                    if bn[c] == 0:
+                size = 0
+                for (_, P_, B_), ts in hb:
+                    fbase[ts] = size + np.arange(len(ts)) * (P_ + B_) ** 2
+                    size += len(ts) * (P_ + B_) ** 2
+                flat = torch.zeros(max(size, 1), dtype=F64, device=dev)
+                fronts[h] = flat
+                # identity on the pivot padding
+                pad_idx = []
+                for (_, P_, B_), ts in hb:
+                    for t in ts:
+                        if pn[t] < P_:
+                            i = np.arange(pn[t], P_)
+                            pad_idx.append(fbase[t] + i * (P_ + B_) + i)
+                if pad_idx:
+                    flat[torch.from_numpy(np.concatenate(pad_idx)).to(dev)] = 1.0
+                # original entries whose earlier-eliminated end is a front of h
+                sel = np.flatnonzero((a_h == h) & in_pass[a_node]) if len(a_node) else a_node
+                if sel.size:
+                    nd_ = a_node[sel]
+                    rpos = front_pos(nd_, G.a_row[sel])
+                    cpos = front_pos(nd_, G.a_col[sel])
+                    st = fstride[nd_]
+                    am = np.arange(m)
+                    tgt = (fbase[nd_][:, None, None]
+                           + (rpos[:, None, None] + am[None, :, None]) * st[:, None, None]
+                           + cpos[:, None, None] + am[None, None, :])
+                    ks = torch.from_numpy(G.a_k[sel]).to(dev)
+                    blocks = vblk[ks][:, :m, :m].transpose(1, 2)
+                    sr = scale.view(nv, m)[torch.from_numpy(G.a_row[sel]).to(dev)]
+                    scl = scale.view(nv, m)[torch.from_numpy(G.a_col[sel]).to(dev)]
+                    blocks = blocks * sr[:, :, None] * scl[:, None, :]
+                    flat[torch.from_numpy(tgt.reshape(-1)).to(dev)] = blocks.reshape(-1)
+                # children's Schur complements (extend-add), child by child
+                if ext_kernel:
+                    self._extend_add(ctx, hb, kids, bn, cpad, fbase, fstride, ckey, fronts,
+                                     flat, B_list, front_pos, m)
+                for t in (t for (_, _, _), ts in hb for t in ts if not ext_kernel):
+                    if not kids[t]:
                         continue
-                    fc = fronts[int(height[c])]
-                    sc = fstride[c]
-                    S = fc[fbase[c]:fbase[c] + sc * sc].view(sc, sc)[
-                        pp[c]:pp[c] + bn[c], pp[c]:pp[c] + bn[c]]
-                    U = (front_pos(np.full(len(B_list[c]), t), B_list[c])[:, None]
-                         + np.arange(m)[None, :]).reshape(-1)
-                    Ut = torch.from_numpy(U).to(dev)
-                    Ft[Ut[:, None], Ut[None, :]] += S
-            # factor every bucket of this height
-            for (_, P_, B_), ts in hb:
-                nb = len(ts)
-                n_ = P_ + B_
-                Fb = flat[fbase[ts[0]]:fbase[ts[0]] + nb * n_ * n_].view(nb, n_, n_)
-                if P_ == 0:
-                    continue
-                # partial LU of every front of the bucket in place
-                # (xdg_batched_factor, p = P_ of n = P_ + B_ columns): L_BP,
-                # U_PB, the Schur complement for the parent and the
-                # triangular inverses of the pivot block, no library calls
-                if front_factor is not None:  # CPU planning tests (tests/mf_emulation.py)
-                    perm, bad = front_factor(Fb, P_)
-                else:
-                    foff = fbase[ts[0]] + np.arange(nb, dtype=np.int64) * n_ * n_
-                    perm, _, info = batched_factor(
-                        ctx, flat, foff, np.full(nb, n_, np.int32),
-                        np.full(nb, P_, np.int32), invert=True,
-                        perm_off=np.arange(nb, dtype=np.int64) * P_)
-                    perm = perm[:nb * P_].view(nb, P_)
-                    bad = info[:nb] != 0
-                if B_:
-                    LBP = Fb[:, P_:, :P_]
-                    bad |= ~torch.isfinite(LBP).flatten(1).all(1)
-                    o = int(lbp_off[ts[0]])
-                    self.F[o:o + nb * B_ * P_].view(nb, B_, P_).copy_(LBP)
-                    o = int(upb_off[ts[0]])
-                    self.F[o:o + nb * P_ * B_].view(nb, P_, B_).copy_(Fb[:, :P_, P_:])
-                o = int(inv_off[ts[0]])
-                self.F[o:o + nb * P_ * P_].view(nb, P_, P_).copy_(Fb[:, :P_, :P_])
-                bad_nodes.append((ts, bad))
-                dev_perms.append((ts, perm))  # read back once, after all heights
-            for hh in range(h + 1):
-                if hh in fronts and last_use[hh] <= h:
-                    del fronts[hh]
+                    Ft = flat[fbase[t]:fbase[t] + fstride[t] ** 2].view(fstride[t], fstride[t])
+                    for c in kids[t]:
+                        if bn[c] == 0:
+                            continue
+                        fc = fronts[int(height[c])]
+                        sc = fstride[c]
+                        S = fc[fbase[c]:fbase[c] + sc * sc].view(sc, sc)[
+                            pp[c]:pp[c] + bn[c], pp[c]:pp[c] + bn[c]]
+                        U = (front_pos(np.full(len(B_list[c]), t), B_list[c])[:, None]
+                             + np.arange(m)[None, :]).reshape(-1)
+                        Ut = torch.from_numpy(U).to(dev)
+                        Ft[Ut[:, None], Ut[None, :]] += S
+                # factor every bucket of this height
+                for (_, P_, B_), ts in hb:
+                    nb = len(ts)
+                    n_ = P_ + B_
+                    Fb = flat[fbase[ts[0]]:fbase[ts[0]] + nb * n_ * n_].view(nb, n_, n_)
+                    if P_ == 0:
+                        continue
+                    # partial LU of every front of the bucket in place
+                    # (xdg_batched_factor, p = P_ of n = P_ + B_ columns): L_BP,
+                    # U_PB, the Schur complement for the parent and the
+                    # triangular inverses of the pivot block, no library calls
+                    if front_factor is not None:  # CPU planning tests (tests/mf_emulation.py)
+                        perm, bad = front_factor(Fb, P_)
+                    else:
+                        foff = fbase[ts[0]] + np.arange(nb, dtype=np.int64) * n_ * n_
+                        perm, _, info = batched_factor(
+                            ctx, flat, foff, np.full(nb, n_, np.int32),
+                            np.full(nb, P_, np.int32), invert=True,
+                            perm_off=np.arange(nb, dtype=np.int64) * P_)
+                        perm = perm[:nb * P_].view(nb, P_)
+                        bad = info[:nb] != 0
+                    if B_:
+                        LBP = Fb[:, P_:, :P_]
+                        bad |= ~torch.isfinite(LBP).flatten(1).all(1)
+                        o = int(lbp_off[ts[0]])
+                        self.F[o:o + nb * B_ * P_].view(nb, B_, P_).copy_(LBP)
+                        o = int(upb_off[ts[0]])
+                        self.F[o:o + nb * P_ * B_].view(nb, P_, B_).copy_(Fb[:, :P_, P_:])
+                    o = int(inv_off[ts[0]])
+                    self.F[o:o + nb * P_ * P_].view(nb, P_, P_).copy_(Fb[:, :P_, :P_])
+                    bad_nodes.append((ts, bad))
+                    dev_perms.append((ts, perm))  # read back once, after all heights
+                    for q, t in enumerate(ts):  # Schur complements other ranks need
+                        if t in xpos:
+                            b_ = int(bn[t])
+                            xsend.append(Fb[q, P_:P_ + b_, P_:P_ + b_].reshape(-1).clone())
+                for hh in range(h + 1):
+                    if hh in fronts and last_use[hh] <= h:
+                        del fronts[hh]
+            fronts.clear()
+            if pass_buckets is buckets and self.comm is not None:
+                # every rank receives every cross-rank root's Schur complement
+                # (rank order, then id: the xroot order) for the replicated
+                # top fronts; they are read in place by the extend-add
+                per_rank = [int(sum(int(bn[t]) ** 2 for t in self.xroot
+                                    if self.rank_of[t] == r)) for r in range(self.comm.world)]
+                mine = (torch.cat(xsend) if xsend
+                        else torch.zeros(0, dtype=F64, device=dev))
+                recv = self.comm.allgather_cat(mine, per_rank)
+                off = 0
+                for t in self.xroot:
+                    fbase[t], fstride[t], cpad[t], ckey[t] = off, int(bn[t]), 0, -1
+                    off += int(bn[t]) ** 2
+                fronts[-1] = recv
+                del xsend
         if bad_nodes:
             flags = torch.cat([b.reshape(-1) for _, b in bad_nodes]).cpu().numpy()
             allts = [t for ts, _ in bad_nodes for t in ts]
@@ -573,7 +683,7 @@ class Multifrontal:
             ph = perm.cpu().numpy()
             for q, t in enumerate(ts):
                 perms[t] = ph[q, :pn[t]].astype(np.int64)
-        del fronts
+        fronts.clear()
         t2 = time.perf_counter()
 
         # ---- solve plan ---------------------------------------------------
@@ -581,12 +691,18 @@ class Multifrontal:
         vsrc = np.asarray(vsrc, np.int64)
         vdst = np.asarray(vdst, np.int64)
         # gather entries, node by node in (height, id) order
-        ent_w, ent_src, ent_scale, lev_ent = [], [], [], [0]
+        # (multi-GPU: entries and tasks of the owned fronts first, then of the
+        # shared top fronts -- two sweeps over the heights, self.lev_*[k])
+        classes = [need & ~shared, need & shared]
+        ent_w, ent_src, ent_scale = [], [], []
+        lev_ent_k = []
         ent_first = np.zeros(nn, np.int64)  # first entry id of each node
         inv_perm = [None] * nn
         cur = 0
-        for h in range(H):
-            for t in order[height[order] == h]:
+        for cls in classes:
+          lev_ent = [cur]
+          for h in range(H):
+            for t in order[(height[order] == h) & cls[order]]:
                 p, b = int(pn[t]), int(bn[t])
                 ent_first[t] = cur
                 pu = perms[t]  # permuted position i <- front unknown pu[i]
@@ -603,6 +719,7 @@ class Multifrontal:
                 ent_w.append(w_off[t] + np.arange(p + b))
                 cur += p + b
             lev_ent.append(cur)
+          lev_ent_k.append(lev_ent)
         ent_w = np.concatenate(ent_w) if ent_w else np.zeros(0, np.int64)
         ent_src = np.concatenate(ent_src) if ent_src else np.zeros(0, np.int64)
         ent_scale = np.concatenate(ent_scale) if ent_scale else np.zeros(0)
@@ -610,7 +727,7 @@ class Multifrontal:
         c_tgt, c_src = [], []
         for c in range(nn):
             t = parent[c]
-            if t < 0 or bn[c] == 0:
+            if t < 0 or bn[c] == 0 or not need[t]:
                 continue
             Bc = B_list[c]
             inP = owner[Bc] == t
@@ -633,7 +750,7 @@ class Multifrontal:
         gp = np.array([_group(int(x)) for x in pn], np.int64)
         gb = np.array([_group(int(x)) if x else g for x, g in zip(bn, gp)], np.int64)
 
-        def tasks(phase):
+        def tasks(phase, cls):
             """int4 warp tasks (node, first row, rows, -1) of one phase, level
             by level: fronts whose rows take a whole warp (G = 32) get MR rows
             per task; shorter rows 32/G rows per task (rows field 0)."""
@@ -641,7 +758,7 @@ class Multifrontal:
             nrows = bn if phase == 1 else pn
             out, lev = [], []
             for h in range(H):
-                ts = order[height[order] == h]
+                ts = order[(height[order] == h) & cls[order]]
                 sh = ts[g[ts] < 32]
                 # bound / upb rows all span the same columns: two row sets
                 # per task share the vector loads (kernel: group_dot2)
@@ -663,16 +780,22 @@ class Multifrontal:
 
         MR = _rows_per_warp()
         SETS = _row_sets()
-        all_tasks, lev_task = [], []
+        all_tasks, lev_task_k = [], []
         base = 0
-        for phase in range(4):
-            tl, lv = tasks(phase)
-            all_tasks += tl
-            lev_task.append(base + np.concatenate([[0], np.cumsum(lv)]))
-            base += int(np.sum(lv))
+        for cls in classes:
+            lev_task = []
+            for phase in range(4):
+                tl, lv = tasks(phase, cls)
+                all_tasks += tl
+                lev_task.append(base + np.concatenate([[0], np.cumsum(lv)]))
+                base += int(np.sum(lv))
+            lev_task_k.append(lev_task)
         task_arr = (np.concatenate(all_tasks) if all_tasks
                     else np.zeros((0, 4), np.int64))
-        self._fused_plan(task_arr, lev_task, ent_first, pn, bn, height, parent, order, H)
+        lev_task = lev_task_k[0]
+        lev_ent = lev_ent_k[0]
+        self._fused_plan(task_arr, lev_task, ent_first, pn, bn, height, parent, order, H,
+                         off=self.comm is not None)
         bidx = np.zeros(int(bn.sum()), np.int64)
         pdst = np.zeros(int(pn.sum()), np.int64)
         pscale = np.ones(int(pn.sum()))
@@ -695,6 +818,9 @@ class Multifrontal:
 
         self.lev_ent = np.asarray(lev_ent, np.int64)
         self.lev_task = np.ascontiguousarray(np.concatenate(lev_task), np.int64)
+        # second sweep (shared top fronts, multi-GPU only)
+        self.lev_ent_sh = np.asarray(lev_ent_k[1], np.int64)
+        self.lev_task_sh = np.ascontiguousarray(np.concatenate(lev_task_k[1]), np.int64)
         self.task_host = task_arr
         self.ent_w, self.ent_src = up(ent_w, I64), up(ent_src, I64)
         self.ent_cptr, self.ent_cidx = up(ent_cptr, I64), up(c_src, I64)
@@ -706,8 +832,11 @@ class Multifrontal:
         self.W = torch.zeros(max(int((pn + bn).sum()), 1), dtype=F64, device=dev)
         self.Y = torch.zeros(max(int(pn.sum()), 1), dtype=F64, device=dev)
         self.C = torch.zeros(max(int(bn.sum()), 1), dtype=F64, device=dev)
-        self.factor_bytes = 8 * int((pn * pn + 2 * pn * bn).sum())
-        self.apply_bytes = self.factor_bytes + 8 * int(4 * (pn + bn).sum() + 4 * pn.sum())
+        self.factor_bytes = 8 * int((pn * pn + 2 * pn * bn)[need].sum())
+        self.apply_bytes = self.factor_bytes + 8 * int(4 * (pn + bn)[need].sum()
+                                                       + 4 * pn[need].sum())
+        if self.comm is not None:
+            self._dist_plan(pn, bn, c_off, y_off, vdst, P_list, am, dev)
         self.pn, self.bn = pn, bn
         self._s = None
         self.times = {"symbolic": t1 - t0, "numeric": t2 - t1,
@@ -747,13 +876,14 @@ class Multifrontal:
                                                 child.data_ptr(), flat.data_ptr(),
                                                 int(n.max()), ctx.stream), "mf_extend_add")
 
-    def _fused_plan(self, task_arr, lev_task, ent_first, pn, bn, height, parent, order, H):
+    def _fused_plan(self, task_arr, lev_task, ent_first, pn, bn, height, parent, order, H,
+                    off=False):
         """Groups / stages of the fused low levels (XDG_MF_FUSE).  A stage is
         a set of fronts of one height; its gather entries and its warp tasks
         of each phase are copied out stage by stage (the same int4 tasks the
         per-level launches run)."""
         mode, K = _fuse_mode()
-        K = min(K, H)
+        K = 0 if off else min(K, H)
         nn = len(pn)
         dev = self.F.device
         if K == 0:
@@ -832,7 +962,45 @@ class Multifrontal:
         self.fent = torch.from_numpy(np.ascontiguousarray(fe, np.int64)).to(dev)
         self.ftask = torch.from_numpy(np.ascontiguousarray(ft)).to(dev, I32)
 
-    def struct(self) -> XdgMf:
+    def _dist_plan(self, pn, bn, c_off, y_off, vdst, P_list, am, dev):
+        """Index lists of the two exchanges of a multi-GPU solve: the
+        contributions C of the cross-rank subtree roots (after the owned
+        forward sweep) and the solution entries of every rank's owned fronts
+        (after the owned backward sweep), both in (rank, front id) order."""
+        comm, me = self.comm, self.comm.rank
+        W = comm.world
+
+        def pack(sel_fronts, rng):
+            per, mine, allv = [], None, []
+            for r in range(W):
+                ts = [t for t in sel_fronts if self.rank_of[t] == r]
+                idx = (np.concatenate([rng(t) for t in ts]) if ts
+                       else np.zeros(0, np.int64))
+                per.append(len(idx))
+                allv.append(idx)
+                if r == me:
+                    mine = idx
+            up = (lambda a: torch.from_numpy(np.ascontiguousarray(a, np.int32)).to(dev))
+            return per, up(mine), up(np.concatenate(allv))
+
+        self.xc_counts, self.xc_mine, self.xc_all = pack(
+            list(self.xroot), lambda t: c_off[t] + np.arange(bn[t]))
+        owned = [t for t in range(len(pn)) if self.rank_of[t] >= 0 and pn[t] > 0]
+        self.xo_counts, self.xo_mine, self.xo_all = pack(
+            owned, lambda t: (vdst[P_list[t]][:, None] + am).reshape(-1))
+        self.xc_send = torch.empty(max(len(self.xc_mine), 1), dtype=F64, device=dev)
+        self.xo_send = torch.empty(max(len(self.xo_mine), 1), dtype=F64, device=dev)
+
+    def struct(self, shared: bool = False) -> XdgMf:
+        if shared:  # the replicated top fronts' sweep (multi-GPU)
+            if getattr(self, "_s_sh", None) is None:
+                s = XdgMf()
+                C.memmove(C.addressof(s), C.addressof(self.struct()), C.sizeof(XdgMf))
+                s.lev_ent = self.lev_ent_sh.ctypes.data
+                s.lev_task = self.lev_task_sh.ctypes.data
+                s.fuse_levels = s.nfbatch = 0
+                self._s_sh = s
+            return self._s_sh
         if self._s is None:
             s = XdgMf()
             s.nlevels, s.nnodes, s.total = self.nlevels, self.nnodes, self.total
@@ -850,10 +1018,34 @@ class Multifrontal:
         return self._s
 
     def solve(self, b: torch.Tensor, x: torch.Tensor) -> torch.Tensor:
-        """x[vdst + a] = A^-1 b[vsrc + a] for every system (device tensors)."""
-        nat.check(self.ctx.lib.xdg_mf_solve(C.byref(self.struct()), b.data_ptr(),
-                                            x.data_ptr(), self.ctx.stream), "mf_solve")
+        """x[vdst + a] = A^-1 b[vsrc + a] for every system (device tensors).
+        Multi-GPU: every rank passes the whole b and receives the whole x;
+        it sweeps its owned subtrees and the replicated top fronts, with one
+        all-gather of the subtree roots' contributions in between and one of
+        the owned fronts' solution entries at the end."""
+        lib, st = self.ctx.lib, self.ctx.stream
+        if self.comm is None:
+            nat.check(lib.xdg_mf_solve(C.byref(self.struct()), b.data_ptr(), x.data_ptr(), st),
+                      "mf_solve")
+            return x
+        nat.check(lib.xdg_mf_solve_phase(C.byref(self.struct()), b.data_ptr(), x.data_ptr(),
+                                         1, st), "mf_solve(owned forward)")
+        self._exchange(self.C, self.xc_mine, self.xc_all, self.xc_counts, self.xc_send)
+        nat.check(lib.xdg_mf_solve_phase(C.byref(self.struct(True)), b.data_ptr(),
+                                         x.data_ptr(), 3, st), "mf_solve(shared)")
+        nat.check(lib.xdg_mf_solve_phase(C.byref(self.struct()), b.data_ptr(), x.data_ptr(),
+                                         2, st), "mf_solve(owned backward)")
+        self._exchange(x, self.xo_mine, self.xo_all, self.xo_counts, self.xo_send)
         return x
+
+    def _exchange(self, buf, mine, allv, counts, send):
+        """buf[allv] = concatenation over ranks of buf_r[mine_r]."""
+        lib, st = self.ctx.lib, self.ctx.stream
+        nat.check(lib.xdg_gather_blocks(len(mine), 1, mine.data_ptr(), buf.data_ptr(),
+                                        send.data_ptr(), st), "gather(exchange)")
+        recv = self.comm.allgather_cat(send[:len(mine)], counts)
+        nat.check(lib.xdg_scatter_blocks(len(allv), 1, allv.data_ptr(), recv.data_ptr(),
+                                         buf.data_ptr(), st), "scatter(exchange)")
 
 
 def _ipiv_to_perm(ctx, piv: torch.Tensor, n: int) -> torch.Tensor:

@@ -155,3 +155,37 @@ def test_native_ordering_matches_numpy_restatement(shape, leaf, seed):
     B = boundaries(G.g_ptr, G.g_col, G.nv, P, kids)
     Bp = boundaries_py(G.g_ptr, G.g_col, P, kids, owner)
     assert all(np.array_equal(a, b) for a, b in zip(B, Bp))
+
+
+def test_proportional_map_subtrees_and_shared_tops():
+    """Subtree-to-rank mapping (multi-GPU factor): every front mapped;
+    owned subtrees closed under children; a shared front has only shared or
+    owned descendants and at least two ranks below it; world 1 owns all."""
+    from paper_2003_02431_b200.multifrontal import proportional_map
+
+    rp, col, _ = grid_bsr((12, 12, 6), 1)
+    G = SystemGraph(rp, col, [np.arange(12 * 12 * 6)])
+    P, kids = nested_dissection(G.g_ptr, G.g_col, G.nv, 8)
+    nn = len(P)
+    parent = np.full(nn, -1)
+    for t, ks in enumerate(kids):
+        for c in ks:
+            parent[c] = t
+    work = np.array([len(p) ** 2 for p in P], float)
+    assert (proportional_map(kids, parent, work, 1) == 0).all()
+    for world in (2, 3, 4, 8):
+        r = proportional_map(kids, parent, work, world)
+        assert set(np.unique(r[r >= 0])) == set(range(world))
+        for t in range(nn):
+            if r[t] >= 0:
+                assert all(r[c] == r[t] for c in kids[t])
+            else:
+                below = set()
+                stack = list(kids[t])
+                while stack:
+                    c = stack.pop()
+                    if r[c] >= 0:
+                        below.add(int(r[c]))
+                    stack += kids[c]
+                assert len(below) >= 2 or not kids[t]
+        assert (r < 0).sum() < nn // 4  # only the top of the tree is replicated
