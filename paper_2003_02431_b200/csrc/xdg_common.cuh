@@ -8,6 +8,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <math.h>
 #include <stdio.h>
 
 #include "../../include/xdg_b200.h"
@@ -61,6 +62,50 @@ int gemv_update2_dev(int64_t L, int max_cols, const int* ncols_dev, const double
                      double* w, double* z, cudaStream_t s);
 int add_small_dev(int max_n, const int* n_dev, const double* a, const double* b, double* out,
                   cudaStream_t s);
+
+// Scalar arithmetic with the same rounding on the host and on the device
+// (separately rounded mul / add / div; no contraction), so a decision made
+// by a 1-thread kernel equals the host driver's bit for bit.
+__host__ __device__ __forceinline__ double rmul(double a, double b) {
+#ifdef __CUDA_ARCH__
+  return __dmul_rn(a, b);
+#else
+  volatile double r = a * b;
+  return r;
+#endif
+}
+__host__ __device__ __forceinline__ double radd(double a, double b) {
+#ifdef __CUDA_ARCH__
+  return __dadd_rn(a, b);
+#else
+  volatile double r = a + b;
+  return r;
+#endif
+}
+__host__ __device__ __forceinline__ double rdiv(double a, double b) {
+#ifdef __CUDA_ARCH__
+  return __ddiv_rn(a, b);
+#else
+  volatile double r = a / b;
+  return r;
+#endif
+}
+__host__ __device__ __forceinline__ double rsqrt_(double a) {
+#ifdef __CUDA_ARCH__
+  return __dsqrt_rn(a);
+#else
+  return sqrt(a);  // IEEE correctly rounded on both sides
+#endif
+}
+// hypot(a, b) = m sqrt(1 + (s / m)^2), m = max(|a|, |b|): no overflow, the
+// same bits on host and device (np.hypot, solvers.py:813, to ~1 ulp).
+__host__ __device__ __forceinline__ double xhypot(double a, double b) {
+  const double x = fabs(a), y = fabs(b);
+  const double m = x > y ? x : y, t = x > y ? y : x;
+  if (m == 0.0) return 0.0;
+  const double q = rdiv(t, m);
+  return rmul(m, rsqrt_(radd(1.0, rmul(q, q))));
+}
 
 // Number of SMs on the current device (cached per process; one device per
 // process is the deployment model).

@@ -93,8 +93,9 @@ rm_current_kernel(int64_t n, const double* __restrict__ x0,
 __global__ void __launch_bounds__(kT)
 mgs_kernel(int64_t n, int j, double* __restrict__ V, int64_t ldv,
            double* __restrict__ w, double* __restrict__ h,
-           double* __restrict__ parts) {
+           double* __restrict__ parts, const int* __restrict__ j_dev) {
   cg::grid_group grid = cg::this_grid();
+  if (j_dev) j = *j_dev;  // graph-captured GMRES: the step index lives on the device
   __shared__ double red[kT / 32];
   const int G = gridDim.x;
   const int64_t stride = (int64_t)G * kT;
@@ -142,8 +143,9 @@ constexpr int kMgsK = 16;
 __global__ void __launch_bounds__(kT, 2)
 mgs_reg_kernel(int64_t n, int j, double* __restrict__ V, int64_t ldv,
                double* __restrict__ w, double* __restrict__ h,
-               double* __restrict__ parts) {
+               double* __restrict__ parts, const int* __restrict__ j_dev) {
   cg::grid_group grid = cg::this_grid();
+  if (j_dev) j = *j_dev;
   __shared__ double red[kT / 32];
   const int G = gridDim.x;
   const int64_t stride = (int64_t)G * kT;
@@ -1010,9 +1012,48 @@ extern "C" int xdg_omg_solve(xdg_omg_level* levels, int nlevels, int entry,
 // ---------------------------------------------------------------------------
 // GMRES
 
-extern "C" int xdg_mgs(int64_t n, int j, double* V, int64_t ldv, double* w,
-                       double* h, void* ws, xdg_stream_t stream) {
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+// One Givens step of restarted GMRES (solvers.py:808-823) on column j of
+// the row-major (m+1) x m Hessenberg H: copy the MGS column hc, apply the
+// previous rotations, form rotation j, update g; *est = |g[j+1]|.  Returns
+// 1 on a zero rotation denominator (SingularSystemError, solvers.py:813-817).
+// Host and device evaluate it with the same rounding (rmul/radd/rdiv).
+__host__ __device__ inline int givens_step(double* H, int m, double* cs, double* sn,
+                                           double* g, const double* hc, int j, double* est) {
+#define HC(i, k) H[(size_t)(i) * m + (k)]
+  for (int i = 0; i <= j + 1; ++i) HC(i, j) = hc[i];
+  for (int i = 0; i < j; ++i) {
+    const double hij = radd(rmul(cs[i], HC(i, j)), rmul(sn[i], HC(i + 1, j)));
+    HC(i + 1, j) = radd(rmul(-sn[i], HC(i, j)), rmul(cs[i], HC(i + 1, j)));
+    HC(i, j) = hij;
+  }
+  const double denom = xhypot(HC(j, j), HC(j + 1, j));
+  if (denom == 0.0) return 1;
+  cs[j] = rdiv(HC(j, j), denom);
+  sn[j] = rdiv(HC(j + 1, j), denom);
+  HC(j, j) = radd(rmul(cs[j], HC(j, j)), rmul(sn[j], HC(j + 1, j)));
+  g[j + 1] = rmul(-sn[j], g[j]);
+  g[j] = rmul(cs[j], g[j]);
+  HC(j + 1, j) = 0.0;
+  *est = fabs(g[j + 1]);
+  return 0;
+}
+
+// y = -H[:j,:j]^-1 g[:j] (upper triangular back substitution, solvers.py:831;
+// negated for x -= Z y with the w -= W c kernel)
+__host__ __device__ inline void gmres_backsolve(const double* H, int m, const double* g, int j,
+                                                double* y) {
+  for (int i = j - 1; i >= 0; --i) {
+    double t = g[i];
+    for (int k = i + 1; k < j; ++k) t = radd(t, -rmul(HC(i, k), y[k]));
+    y[i] = rdiv(t, HC(i, i));
+  }
+  for (int i = 0; i < j; ++i) y[i] = -y[i];
+#undef HC
+}
+
+// MGS of GMRES step j (j_dev != NULL: read on the device, graph capture).
+static int mgs_launch(int64_t n, int j, const int* j_dev, double* V, int64_t ldv, double* w,
+                      double* h, void* ws, cudaStream_t s) {
   static thread_local int per_sm = 0;
   if (per_sm == 0) {
     XDG_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mgs_kernel,
@@ -1024,7 +1065,7 @@ extern "C" int xdg_mgs(int64_t n, int j, double* V, int64_t ldv, double* w,
   int grid = (int)(need < cap ? (need < 1 ? 1 : need) : cap);
   // partials: 2 x grid doubles after the reduction counter slot
   double* parts = static_cast<double*>(ws) + 1;
-  void* args[] = {&n, &j, &V, &ldv, &w, &h, &parts};
+  void* args[] = {&n, &j, &V, &ldv, &w, &h, &parts, const_cast<int**>(&j_dev)};
   // register-resident variant on the same grid when it fits (XDG_MGS_REG=0
   // forces the streaming kernel)
   static thread_local int reg_per_sm = -1;
@@ -1045,6 +1086,21 @@ extern "C" int xdg_mgs(int64_t n, int j, double* V, int64_t ldv, double* w,
   return XDG_OK;
 }
 
+extern "C" int xdg_mgs(int64_t n, int j, double* V, int64_t ldv, double* w,
+                       double* h, void* ws, xdg_stream_t stream) {
+  return mgs_launch(n, j, nullptr, V, ldv, w, h, ws, reinterpret_cast<cudaStream_t>(stream));
+}
+
+namespace xdg {
+namespace omg_graph {
+bool gmres_graph_enabled();
+int gmres_solve_graph(const xdg_bsr* M, const xdg_pmg* pmg, int m, double tol, int max_it,
+                      const double* b, double* x, int has_x0, double* V, double* Zb, double* w,
+                      double* r, double* sc, double* ycoef, void* ws, int* iterations,
+                      double* history, int* hist_len, double* final_residual, cudaStream_t s);
+}  // namespace omg_graph
+}  // namespace xdg
+
 extern "C" int xdg_gmres_solve(const xdg_bsr* M, const xdg_pmg* pmg,
                                int restart, double tolerance,
                                int max_iterations, const double* b, double* x,
@@ -1056,6 +1112,13 @@ extern "C" int xdg_gmres_solve(const xdg_bsr* M, const xdg_pmg* pmg,
   NvtxRange nv("xdg_gmres_solve");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   g_bytes = 0.0;
+  if (xdg::omg_graph::gmres_graph_enabled()) {  // one CUDA graph (XDG_GMRES_GRAPH=0: host loop)
+    const int rc = xdg::omg_graph::gmres_solve_graph(
+        M, pmg, restart, tolerance, max_iterations, b, x, has_x0, V, Zb, w, r, sc, ycoef, ws,
+        iterations, history, hist_len, final_residual, s);
+    if (bytes_out) *bytes_out = g_bytes;
+    return rc;
+  }
   const int m = restart;
   const int64_t n = (int64_t)M->nbr * M->N;
   (void)gemv_ws;
@@ -1068,7 +1131,6 @@ extern "C" int xdg_gmres_solve(const xdg_bsr* M, const xdg_pmg* pmg,
   history[hl++] = beta;
   std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), g(m + 1), hc(m + 2),
       y(m);
-  auto Hc = [&](int i, int jj) -> double& { return H[(size_t)i * m + jj]; };
   while (beta > tolerance && total < max_iterations) {
     std::fill(H.begin(), H.end(), 0.0);
     std::fill(cs.begin(), cs.end(), 0.0);
@@ -1088,35 +1150,16 @@ extern "C" int xdg_gmres_solve(const xdg_bsr* M, const xdg_pmg* pmg,
       count(8.0 * n * (2.0 * (j + 1) + 3.0));
       XDG_TRY(xdg_mgs(n, j, V, n, w, sc, ws, stream));
       XDG_TRY_CUDA(sync_read(hc.data(), sc, j + 2, s));
-      for (int i = 0; i <= j + 1; ++i) Hc(i, j) = hc[i];
-      for (int i = 0; i < j; ++i) {                               // rotations
-        const double hij = cs[i] * Hc(i, j) + sn[i] * Hc(i + 1, j);
-        Hc(i + 1, j) = -sn[i] * Hc(i, j) + cs[i] * Hc(i + 1, j);
-        Hc(i, j) = hij;
-      }
-      const double denom = hypot(Hc(j, j), Hc(j + 1, j));
-      if (denom == 0.0) {
+      double est;
+      if (givens_step(H.data(), m, cs.data(), sn.data(), g.data(), hc.data(), j, &est)) {
         set_error("preconditioned operator produced a zero column");
         return XDG_ERR_SINGULAR;
       }
-      cs[j] = Hc(j, j) / denom;
-      sn[j] = Hc(j + 1, j) / denom;
-      Hc(j, j) = cs[j] * Hc(j, j) + sn[j] * Hc(j + 1, j);
-      g[j + 1] = -sn[j] * g[j];
-      g[j] = cs[j] * g[j];
-      Hc(j + 1, j) = 0.0;
-      const double est = fabs(g[j + 1]);
       history[hl++] = est;
       ++j;
       if (est <= tolerance) break;
     }
-    // y = H[:j,:j]^-1 g[:j] (upper triangular back substitution)
-    for (int i = j - 1; i >= 0; --i) {
-      double t = g[i];
-      for (int k = i + 1; k < j; ++k) t -= Hc(i, k) * y[k];
-      y[i] = t / Hc(i, i);
-    }
-    for (int i = 0; i < j; ++i) y[i] = -y[i];                     // x -= Z (-y)
+    gmres_backsolve(H.data(), m, g.data(), j, y.data());       // y := -H^-1 g
     XDG_TRY_CUDA(cudaMemcpyAsync(ycoef, y.data(), sizeof(double) * j,
                                  cudaMemcpyHostToDevice, s));
     count(8.0 * j * n + 16.0 * n);
@@ -1133,6 +1176,242 @@ extern "C" int xdg_gmres_solve(const xdg_bsr* M, const xdg_pmg* pmg,
   if (bytes_out) *bytes_out = g_bytes;
   return XDG_OK;
 }
+
+// ===========================================================================
+// Graph-captured gmres_pmg_solve (solvers.py:756-846): the restart cycles
+// and the Arnoldi steps are nested WHILE nodes of one CUDA graph; the MGS
+// step index, the Hessenberg column, the Givens rotations, the back
+// substitution and the convergence tests live on the device (1-thread
+// kernels evaluating givens_step / gmres_backsolve, the same functions and
+// rounding as the host driver above: bit-identical results).  V_j and Z_j
+// are addressed through device-indexed copies into fixed buffers.
+namespace xdg {
+namespace omg_graph {
+
+struct GmDev {
+  double beta, est;
+  int j, total, hl, err;
+};
+
+__global__ void gm_init_kernel(GmDev* st, const double* nr2, double tol, int max_it,
+                               double* hist, cudaGraphConditionalHandle h) {
+  const double beta = sqrt(*nr2);
+  st->beta = beta;
+  st->est = beta;
+  st->j = st->total = st->err = 0;
+  st->hl = 1;
+  hist[0] = beta;
+  cudaGraphSetConditional(h, (beta > tol && max_it > 0) ? 1u : 0u);
+}
+
+__global__ void gm_cycle_init_kernel(GmDev* st, double* H, double* cs, double* sn, double* g,
+                                     int m, cudaGraphConditionalHandle h) {
+  for (int i = 0; i < (m + 1) * m; ++i) H[i] = 0.0;
+  for (int i = 0; i < m; ++i) cs[i] = sn[i] = 0.0;
+  for (int i = 0; i <= m; ++i) g[i] = 0.0;
+  g[0] = st->beta;
+  st->j = 0;
+  cudaGraphSetConditional(h, m > 0 ? 1u : 0u);
+}
+
+__global__ void __launch_bounds__(kT)
+gm_col_copy_kernel(int64_t n, const GmDev* st, const double* __restrict__ src, int64_t lds,
+                   double* __restrict__ dst, int64_t ldd) {
+  const int64_t j = st->j;
+  const double* a = src + j * lds;
+  double* b = dst + j * ldd;
+  const int64_t stride = (int64_t)gridDim.x * kT;
+  for (int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x; i < n; i += stride) b[i] = a[i];
+}
+
+__global__ void gm_givens_kernel(GmDev* st, const double* hc, double* H, double* cs, double* sn,
+                                 double* g, int m, double tol, int max_it, double* hist,
+                                 cudaGraphConditionalHandle h, double* gbytes, double n,
+                                 double fixed_bytes) {
+  const int j = st->j;
+  double est = 0.0;
+  *gbytes += fixed_bytes + 8.0 * n * (2.0 * (j + 1) + 3.0);
+  if (givens_step(H, m, cs, sn, g, hc, j, &est)) {
+    st->err = 1;
+    cudaGraphSetConditional(h, 0u);
+    return;
+  }
+  st->est = est;
+  hist[st->hl++] = est;
+  st->total += 1;
+  st->j = j + 1;
+  cudaGraphSetConditional(h, (j + 1 < m && st->total < max_it && est > tol) ? 1u : 0u);
+}
+
+__global__ void gm_backsolve_kernel(const GmDev* st, const double* H, const double* g, int m,
+                                    double* ycoef, double* gbytes, double n) {
+  if (st->err) return;
+  gmres_backsolve(H, m, g, st->j, ycoef);
+  *gbytes += 8.0 * st->j * n + 16.0 * n;
+}
+
+__global__ void gm_cycle_end_kernel(GmDev* st, const double* nr2, double tol, int max_it,
+                                    double* hist, cudaGraphConditionalHandle h) {
+  if (st->err) {
+    cudaGraphSetConditional(h, 0u);
+    return;
+  }
+  const double beta = sqrt(*nr2);
+  st->beta = beta;
+  hist[st->hl - 1] = beta;
+  cudaGraphSetConditional(h, (beta > tol && st->total < max_it) ? 1u : 0u);
+}
+
+bool gmres_graph_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("XDG_GMRES_GRAPH");
+    return e == nullptr || atoi(e) != 0;
+  }();
+  return on;
+}
+
+int gmres_solve_graph(const xdg_bsr* M, const xdg_pmg* pmg, int m, double tol, int max_it,
+                      const double* b, double* x, int has_x0, double* V, double* Zb, double* w,
+                      double* r, double* sc, double* ycoef, void* ws, int* iterations,
+                      double* history, int* hist_len, double* final_residual, cudaStream_t s) {
+  const int64_t n = (int64_t)M->nbr * M->N;
+  GraphOmg G;  // capture streams
+  const size_t nH = (size_t)(m + 1) * m, ndbl = nH + 3 * (size_t)m + 1 + (max_it + 2) + 1 +
+                                                2 * (size_t)n;
+  char* buf = nullptr;
+  XDG_TRY_CUDA(cudaMallocAsync(&buf, sizeof(GmDev) + sizeof(double) * ndbl, s));
+  XDG_TRY_CUDA(cudaMemsetAsync(buf, 0, sizeof(GmDev) + sizeof(double) * ndbl, s));
+  GmDev* st = reinterpret_cast<GmDev*>(buf);
+  double* H = reinterpret_cast<double*>(buf + sizeof(GmDev));
+  double* cs = H + nH;
+  double* sn = cs + m;
+  double* g = sn + m;           // m + 1
+  double* hist = g + m + 1;     // max_it + 2
+  double* gbytes = hist + max_it + 2;
+  double* vbuf = gbytes + 1;
+  double* zbuf = vbuf + n;
+  cudaStream_t s0 = cap_stream(G, 0);
+  int rc = XDG_OK;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  const xdg_stream_t x0s = reinterpret_cast<xdg_stream_t>(s0);
+  auto capture = [&]() -> int {
+    if (!has_x0) {
+      zero2_kernel<<<grid_for(n, kT, kPerSm), kT, 0, s0>>>(n, x, nullptr);
+      XDG_CHECK_LAUNCH();
+    }
+    XDG_TRY(spmv(M, x, r, b, sc, ws, s0));                          // r = b - M x
+    cudaGraphConditionalHandle ho;
+    XDG_TRY(make_handle(s0, &ho));
+    gm_init_kernel<<<1, 1, 0, s0>>>(st, sc, tol, max_it, hist, ho);
+    XDG_CHECK_LAUNCH();
+    cudaGraph_t outer;
+    XDG_TRY(add_cond_node(s0, ho, cudaGraphCondTypeWhile, 1, &outer));
+    cudaStream_t s1;
+    XDG_TRY(begin_body(G, 1, outer, &s1));
+    const xdg_stream_t x1 = reinterpret_cast<xdg_stream_t>(s1);
+    {
+      cudaGraphConditionalHandle hi;
+      XDG_TRY(make_handle(s1, &hi));
+      gm_cycle_init_kernel<<<1, 1, 0, s1>>>(st, H, cs, sn, g, m, hi);
+      XDG_CHECK_LAUNCH();
+      count(16.0 * n);
+      // V_0 = r / beta (device beta; same rounding as xdg_scale with a host beta)
+      XDG_TRY(xdg_scale(n, 1.0, &st->beta, 1, r, V, x1));
+      cudaGraph_t inner;
+      XDG_TRY(add_cond_node(s1, hi, cudaGraphCondTypeWhile, 1, &inner));
+      cudaStream_t s2;
+      XDG_TRY(begin_body(G, 2, inner, &s2));
+      const double b0 = g_bytes;
+      gm_col_copy_kernel<<<grid_for(n, kT, kPerSm), kT, 0, s2>>>(n, st, V, n, vbuf, 0);
+      XDG_CHECK_LAUNCH();
+      XDG_TRY(pmg_apply_op(pmg, M, vbuf, zbuf, s2));
+      XDG_TRY(spmv(M, zbuf, w, nullptr, nullptr, nullptr, s2));
+      gm_col_copy_kernel<<<grid_for(n, kT, kPerSm), kT, 0, s2>>>(n, st, zbuf, 0, Zb, n);
+      XDG_CHECK_LAUNCH();
+      XDG_TRY(mgs_launch(n, 0, &st->j, V, n, w, sc, ws, s2));
+      const double fixed = g_bytes - b0;
+      g_bytes = b0;
+      gm_givens_kernel<<<1, 1, 0, s2>>>(st, sc, H, cs, sn, g, m, tol, max_it, hist, hi, gbytes,
+                                        (double)n, fixed);
+      XDG_CHECK_LAUNCH();
+      XDG_TRY(end_body(s2));
+      gm_backsolve_kernel<<<1, 1, 0, s1>>>(st, H, g, m, ycoef, gbytes, (double)n);
+      XDG_CHECK_LAUNCH();
+      XDG_TRY(gemv_update2_dev(n, m, &st->j, Zb, nullptr, n, ycoef, nullptr, x, nullptr, s1));
+      const double b1 = g_bytes;
+      XDG_TRY(spmv(M, x, r, b, sc, ws, s1));
+      (void)b1;
+      gm_cycle_end_kernel<<<1, 1, 0, s1>>>(st, sc, tol, max_it, hist, ho);
+      XDG_CHECK_LAUNCH();
+    }
+    XDG_TRY(end_body(s1));
+    (void)x0s;
+    return XDG_OK;
+  };
+  if (s0 == nullptr) {
+    rc = XDG_ERR_CUDA;
+  } else {
+    cudaEvent_t ev;
+    cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    cudaEventRecord(ev, s);
+    cudaStreamWaitEvent(s0, ev, 0);
+    cudaEventDestroy(ev);
+    XDG_TRY_CUDA(cudaStreamBeginCapture(s0, cudaStreamCaptureModeRelaxed));
+    // the restart cycles' spmv bytes (once per cycle) are counted on the host
+    // at capture; scale the per-cycle part by the cycle count afterwards
+    const double cap0 = g_bytes;
+    rc = capture();
+    const double per_capture = g_bytes - cap0;
+    g_bytes = cap0;
+    cudaError_t e = cudaStreamEndCapture(s0, &graph);
+    if (rc == XDG_OK && e != cudaSuccess) {
+      set_error("gmres graph capture: %s", cudaGetErrorString(e));
+      rc = XDG_ERR_CUDA;
+    }
+    if (rc == XDG_OK && (e = cudaGraphInstantiate(&exec, graph, 0)) != cudaSuccess) {
+      set_error("gmres graph instantiate: %s", cudaGetErrorString(e));
+      rc = XDG_ERR_CUDA;
+    }
+    if (rc == XDG_OK && (e = cudaGraphLaunch(exec, s)) != cudaSuccess) {
+      set_error("gmres graph launch: %s", cudaGetErrorString(e));
+      rc = XDG_ERR_CUDA;
+    }
+    if (rc == XDG_OK) {
+      GmDev top;
+      double dbytes = 0.0;
+      e = cudaMemcpyAsync(&top, st, sizeof(GmDev), cudaMemcpyDeviceToHost, s);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(&dbytes, gbytes, sizeof(double), cudaMemcpyDeviceToHost, s);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+      if (e == cudaSuccess)
+        e = cudaMemcpy(history, hist, sizeof(double) * top.hl, cudaMemcpyDeviceToHost);
+      if (e != cudaSuccess) {
+        set_error("gmres graph readback: %s", cudaGetErrorString(e));
+        rc = XDG_ERR_CUDA;
+      } else if (top.err) {
+        set_error("preconditioned operator produced a zero column");
+        rc = XDG_ERR_SINGULAR;
+      } else {
+        *iterations = top.total;
+        *hist_len = top.hl;
+        *final_residual = top.beta;
+        // host-counted capture bytes: the initial residual once, the cycle
+        // setup (V_0 scaling + residual) once per restart cycle
+        const int cycles = (top.total + m - 1) / (m > 0 ? m : 1);
+        g_bytes += per_capture * (cycles > 0 ? cycles : 1) + dbytes;
+      }
+    }
+  }
+  if (exec) cudaGraphExecDestroy(exec);
+  if (graph) cudaGraphDestroy(graph);
+  cudaFreeAsync(buf, s);
+  for (cudaStream_t t : G.streams) cudaStreamDestroy(t);
+  return rc;
+}
+
+}  // namespace omg_graph
+}  // namespace xdg
 
 // Exported pieces of rm_step for the multi-GPU driver (dist_solvers.py),
 // which interleaves them with all-reduces.

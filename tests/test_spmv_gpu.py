@@ -36,6 +36,17 @@ def test_spmv_bitexact_vs_reference_golden(case):
             R = dev_bsr(z[p + "R_row_ptr"], z[p + "R_col"], z[p + "R_val"],
                         int(z[p + "R_ncols"]))
             assert np.array_equal(R.spmv(cuda(z[p + "xc"])).cpu().numpy(), z[p + "Rxc"])
+            # R^T r (the OMG restriction, solvers.py:730): the cached block
+            # transpose the solver uses, bit-identical to R.transpose().matvec
+            from paper_2003_02431_b200.blockmatrix import BlockSparseMatrix, uniform_layout
+
+            N = int(z[p + "N"])
+            Rm = BlockSparseMatrix.from_bsr(
+                z[p + "R_row_ptr"], z[p + "R_col"], z[p + "R_val"],
+                uniform_layout(len(z[p + "R_row_ptr"]) - 1, N),
+                uniform_layout(int(z[p + "R_ncols"]), N))
+            Rt = Rm.transpose().device()
+            assert np.array_equal(Rt.spmv(cuda(z[p + "x"])).cpu().numpy(), z[p + "Rtr"])
         lam += 1
 
 
