@@ -310,6 +310,13 @@ typedef struct xdg_mf {
   const int64_t* st_task;      /* [4][nfstages+1] ranges into ftask per phase */
   const int64_t* fent;         /* gather entry ids, stage by stage           */
   const int32_t* ftask;        /* int4 warp tasks, stage by stage            */
+  /* Merged phases: the factors hold M_BP = L_BP L^-1 (at lbp) and N_PB =
+   * U^-1 U_PB (at upb), see xdg_mf_merge; one row launch per height and
+   * sweep: task ranges lev_task[0] (forward rows 0..p+b-1 of every front)
+   * and lev_task[2] (backward rows 0..p-1); X[p] = equilibrated solution
+   * (bidx indexes X).  Excludes the fused low levels.                     */
+  double* X;
+  int32_t merged, pad_;
 } xdg_mf;
 
 /* Setup: extend-add of one round of children's Schur complements into
@@ -320,6 +327,14 @@ typedef struct xdg_mf {
 int xdg_mf_extend_add(int64_t npairs, const int64_t* pair, const int64_t* U,
                       const double* child, double* parent, int64_t max_n,
                       xdg_stream_t stream);
+/* Setup of the merged phases: for nb fronts (each an n x n row-major
+ * buffer, n = P + B, as xdg_batched_factor(invert) left it) write
+ * out_m[q] = L_BP L^-1 (B x P) and out_n[q] = U^-1 U_PB (P x B), dense
+ * row-major, front after front.  Same role as the triangular solves inside
+ * SuperLU's supernodal solve (cutdg blockmatrix.py:218-227), moved to the
+ * factorization. */
+int xdg_mf_merge(int64_t nb, int P, int B, const double* fronts, double* out_m,
+                 double* out_n, xdg_stream_t stream);
 /* Rows per warp task of a front whose rows take a whole warp. */
 int xdg_mf_rows_per_warp(void);
 /* Host-side symbolic analysis (csrc/xdg_ordering.cu).  Nested dissection

@@ -80,6 +80,7 @@ SIGNATURES = {
     "xdg_schwarz_sizes": (_i32, [_vp]),
     "xdg_schwarz_copy": (_i32, [_vp, _vp, _vp, _vp]),
     "xdg_mf_rows_per_warp": (_i32, []),
+    "xdg_mf_merge": (_i32, [_i64, _i32, _i32, _vp, _vp, _vp, _vp]),
     "xdg_mf_extend_add": (_i32, [_i64, _vp, _vp, _vp, _vp, _i64, _vp]),
     "xdg_batched_factor": (_i32, [_i64, _vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp,
                                   _vp, _i32, _vp, _vp]),

@@ -141,13 +141,17 @@ __device__ __forceinline__ void multi_dot(const double* const* rows, V v, int lo
   for (int q = 0; q < kMR; ++q) acc[q][0] = acc[q][1] = 0.0;
   for (int jb = lo; jb < hi; jb += 32 * kMU) {
     double m[kMR][kMU], x[kMU];
+    typename V::index_t ix[kMU];
+#pragma unroll
+    for (int u = 0; u < kMU; ++u) ix[u] = v.idx(min(jb + lane + 32 * u, hi - 1));
 #pragma unroll
     for (int u = 0; u < kMU; ++u) {
       const int j = min(jb + lane + 32 * u, hi - 1);
 #pragma unroll
       for (int q = 0; q < kMR; ++q) m[q][u] = __ldg(rows[q] + j);
-      x[u] = v(j);
     }
+#pragma unroll
+    for (int u = 0; u < kMU; ++u) x[u] = v.at(ix[u]);
 #pragma unroll
     for (int u = 0; u < kMU; ++u) {
       const int j = jb + lane + 32 * u;
@@ -162,15 +166,25 @@ __device__ __forceinline__ void multi_dot(const double* const* rows, V v, int lo
   for (int q = 0; q < kMR; ++q) d[q] = warp_sum(acc[q][0] + acc[q][1]);
 }
 
+// Vector accessors.  idx(j) / at(i) split an element access in two so the
+// loops can issue every index load of a chunk, then the factor loads, then
+// the (dependent) vector loads: a gathered element costs one extra round
+// trip per chunk, not one per element.
 struct Direct {
   const double* p;
+  typedef int index_t;
   __device__ __forceinline__ double operator()(int j) const { return p[j]; }
+  __device__ __forceinline__ int idx(int j) const { return j; }
+  __device__ __forceinline__ double at(int i) const { return p[i]; }
 };
 
 struct Gathered {
   const double* x;
-  const int64_t* idx;
-  __device__ __forceinline__ double operator()(int j) const { return x[idx[j]]; }
+  const int64_t* ix;
+  typedef int64_t index_t;
+  __device__ __forceinline__ double operator()(int j) const { return x[ix[j]]; }
+  __device__ __forceinline__ int64_t idx(int j) const { return __ldg(ix + j); }
+  __device__ __forceinline__ double at(int64_t i) const { return x[i]; }
 };
 
 // Task g of n in interleaved order (long and short rows mix on every SM).
@@ -215,6 +229,7 @@ struct Ctx {
   double* Y;
   double* C;
   double* x;
+  double* X;
 };
 
 template <int PH>
@@ -339,6 +354,205 @@ mf_rows_kernel(int64_t t0, int64_t ntasks, const int4* __restrict__ tasks, Ctx c
     run_task<PH>(c, tasks[t0 + interleave(w, ntasks)], lane);
 }
 
+// ---------------------------------------------------------------------------
+// Merged phases (xdg_mf.merged): the factors are stored as
+//   M_BP = L_BP L^-1   (b x p)   and   N_PB = U^-1 U_PB   (p x b)
+// (products formed once at setup, xdg_mf_merge; same bytes as L_BP / U_PB),
+// so that neither sweep has a phase that waits for the triangular solve of
+// its own front:
+//   forward   Y[i]  = W[i] + L^-1[i, :i] . W[:i]        rows 0 .. p-1
+//             C[j]  = W[p+j] - M_BP[j, :] . W[:p]       rows p .. p+b-1
+//   backward  X[i]  = U^-1[i, i:] . Y[i:] - N_PB[i, :] . X[bidx]
+// One row launch per height and sweep (was two), every row of a front reads
+// the same vector, and the short triangular rows share their launch with
+// the long rectangular ones.  X is the equilibrated solution (Y keeps the
+// forward result: rows of the same launch still read it).
+
+// Rows a and b (lane group of G lanes, ranges [sa, ea) and [sb, eb) of the
+// same vector): the vector element is loaded once for both rows, all loads
+// of a chunk are issued before the first FMA.  Loads are clamped to hi - 1
+// (inside the padded rows) and masked.
+template <typename V>
+__device__ __forceinline__ void group_dot2r(const double* __restrict__ ra,
+                                            const double* __restrict__ rb, V v, int sa, int ea,
+                                            int sb, int eb, int gl, int G, double& da,
+                                            double& db) {
+  double x[4] = {0.0, 0.0, 0.0, 0.0}, y[4] = {0.0, 0.0, 0.0, 0.0};
+  const int lo = min(ea > sa ? sa : (1 << 30), eb > sb ? sb : (1 << 30));
+  const int hi = max(ea > sa ? ea : 0, eb > sb ? eb : 0);
+  if (hi > lo) {
+    const int step = MF_U * G;
+    for (int jb = lo; jb < hi; jb += step) {
+      double p[MF_U], s[MF_U], q[MF_U];
+      typename V::index_t ix[MF_U];
+#pragma unroll
+      for (int u = 0; u < MF_U; ++u) ix[u] = v.idx(min(jb + gl + G * u, hi - 1));
+#pragma unroll
+      for (int u = 0; u < MF_U; ++u) {
+        const int j = min(jb + gl + G * u, hi - 1);
+        p[u] = __ldg(ra + j);
+        s[u] = __ldg(rb + j);
+      }
+#pragma unroll
+      for (int u = 0; u < MF_U; ++u) q[u] = v.at(ix[u]);
+#pragma unroll
+      for (int u = 0; u < MF_U; ++u) {
+        const int j = jb + gl + G * u;
+        const double qa = (j >= sa && j < ea) ? q[u] : 0.0;
+        const double qb = (j >= sb && j < eb) ? q[u] : 0.0;
+        x[u & 3] = fma(p[u], qa, x[u & 3]);
+        y[u & 3] = fma(s[u], qb, y[u & 3]);
+      }
+    }
+  }
+  double sa_ = (x[0] + x[1]) + (x[2] + x[3]);
+  double sb_ = (y[0] + y[1]) + (y[2] + y[3]);
+  for (int o = 16; o > 0; o >>= 1)
+    if (o < G) {
+      sa_ += __shfl_xor_sync(0xffffffffu, sa_, o);
+      sb_ += __shfl_xor_sync(0xffffffffu, sb_, o);
+    }
+  da = sa_;
+  db = sb_;
+}
+
+// forward row r of a front: pointer and length (the vector is W[w .. w+p))
+__device__ __forceinline__ const double* fwd_row(const Ctx& c, const xdg_mf_node& nd, int r,
+                                                 int& len) {
+  if (r < nd.p) {
+    len = r;
+    return c.F + nd.inv + (int64_t)r * nd.ldp;
+  }
+  len = nd.p;
+  return c.F + nd.lbp + (int64_t)(r - nd.p) * nd.ldp;
+}
+
+__device__ __forceinline__ void fwd_done(const Ctx& c, const xdg_mf_node& nd, int r, double d) {
+  if (r < nd.p)
+    c.Y[nd.y + r] = __dadd_rn(c.W[nd.w + r], d);
+  else
+    c.C[nd.c + (r - nd.p)] = __dsub_rn(c.W[nd.w + r], d);
+}
+
+__device__ __forceinline__ void fwd_store(const Ctx& c, const xdg_mf_node& nd, int r, double w,
+                                          double d) {
+  if (r < nd.p)
+    c.Y[nd.y + r] = __dadd_rn(w, d);
+  else
+    c.C[nd.c + (r - nd.p)] = __dsub_rn(w, d);
+}
+
+__device__ __forceinline__ void bwd_done(const Ctx& c, const xdg_mf_node& nd, int r, double du,
+                                         double dn) {
+  const double d = __dsub_rn(du, dn);
+  c.X[nd.y + r] = d;
+  c.x[c.pdst[nd.px + r]] = __dmul_rn(c.pscale[nd.px + r], d);
+}
+
+template <bool FWD>
+__device__ __forceinline__ void run_merged(const Ctx& c, const int4 tk, const int lane) {
+  const xdg_mf_node nd = c.nodes[tk.x];
+  const int nrows = FWD ? nd.p + nd.b : nd.p;
+  if (tk.z == kMR) {  // whole-warp rows: kMR rows share the vector loads
+    const int r = tk.y;
+    const double* rows[kMR];
+    int r0[kMR], r1[kMR];
+    int lo = 1 << 30, hi = 0;
+#pragma unroll
+    for (int q = 0; q < kMR; ++q) {
+      const int rq = min(r + q, nrows - 1);
+      if (FWD) {
+        r0[q] = 0;
+        rows[q] = fwd_row(c, nd, rq, r1[q]);
+      } else {
+        rows[q] = c.F + nd.inv + (int64_t)rq * nd.ldp;
+        r0[q] = rq;
+        r1[q] = nd.p;
+      }
+      if (r + q >= nrows) r1[q] = r0[q];
+      if (r1[q] > r0[q]) {
+        lo = min(lo, r0[q]);
+        hi = max(hi, r1[q]);
+      }
+    }
+    double d[kMR], e[kMR];
+#pragma unroll
+    for (int q = 0; q < kMR; ++q) d[q] = e[q] = 0.0;
+    if (hi > lo) multi_dot(rows, Direct{FWD ? c.W + nd.w : c.Y + nd.y}, lo, hi, r0, r1, lane, d);
+    if (!FWD && nd.b > 0) {
+#pragma unroll
+      for (int q = 0; q < kMR; ++q) {
+        const int rq = min(r + q, nrows - 1);
+        rows[q] = c.F + nd.upb + (int64_t)rq * nd.ldb;
+        r0[q] = 0;
+        r1[q] = (r + q < nrows) ? nd.b : 0;
+      }
+      multi_dot(rows, Gathered{c.X, c.bidx + nd.bx}, 0, nd.b, r0, r1, lane, e);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int q = 0; q < kMR; ++q)
+        if (r + q < nrows) {
+          if (FWD)
+            fwd_done(c, nd, r + q, d[q]);
+          else
+            bwd_done(c, nd, r + q, d[q], e[q]);
+        }
+    }
+  } else {  // two sets of 32/G rows, G lanes per row
+    const int G = FWD ? nd.gp : nd.gb;
+    const int gl = lane & (G - 1);
+    const int ra = tk.y + lane / G, rb = ra + 32 / G;
+    const bool acta = ra < nrows, actb = rb < nrows;
+    const int qa = acta ? ra : 0, qb = actb ? rb : 0;
+    double da, db, ea = 0.0, eb = 0.0;
+    if (FWD) {
+      int la, lb;
+      const double* pa = fwd_row(c, nd, qa, la);
+      const double* pb = fwd_row(c, nd, qb, lb);
+      // the rows' own W entries are loaded with the dot's loads, not after it
+      const double wa = c.W[nd.w + qa], wb = c.W[nd.w + qb];
+      group_dot2r(pa, pb, Direct{c.W + nd.w}, 0, acta ? la : 0, 0, actb ? lb : 0, gl, G, da, db);
+      if (acta && gl == 0) fwd_store(c, nd, ra, wa, da);
+      if (actb && gl == 0) fwd_store(c, nd, rb, wb, db);
+    } else {
+      const double* inv = c.F + nd.inv;
+      group_dot2r(inv + (int64_t)qa * nd.ldp, inv + (int64_t)qb * nd.ldp, Direct{c.Y + nd.y},
+                  qa, acta ? nd.p : qa, qb, actb ? nd.p : qb, gl, G, da, db);
+      if (nd.b > 0) {
+        const double* un = c.F + nd.upb;
+        group_dot2r(un + (int64_t)qa * nd.ldb, un + (int64_t)qb * nd.ldb,
+                    Gathered{c.X, c.bidx + nd.bx}, 0, acta ? nd.b : 0, 0, actb ? nd.b : 0, gl,
+                    G, ea, eb);
+      }
+      if (acta && gl == 0) bwd_done(c, nd, ra, da, ea);
+      if (actb && gl == 0) bwd_done(c, nd, rb, db, eb);
+    }
+  }
+}
+
+template <bool FWD>
+__global__ void __launch_bounds__(kT, MF_MINB)
+mf_merged_kernel(int64_t t0, int64_t ntasks, const int4* __restrict__ tasks, Ctx c) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (kT / 32);
+  for (int64_t w = (int64_t)blockIdx.x * (kT / 32) + (threadIdx.x >> 5); w < ntasks;
+       w += nw)
+    run_merged<FWD>(c, tasks[t0 + interleave(w, ntasks)], lane);
+}
+
+template <bool FWD>
+int launch_merged(const xdg_mf* mf, int h, double* x, cudaStream_t s) {
+  const int64_t* lev = mf->lev_task + (int64_t)(FWD ? 0 : 2) * (mf->nlevels + 1);
+  const int64_t t0 = lev[h], nt = lev[h + 1] - t0;
+  if (nt <= 0) return XDG_OK;
+  Ctx c{mf->nodes, mf->F, mf->bidx, mf->pdst, mf->pscale, mf->W, mf->Y, mf->C, x, mf->X};
+  const int g = resident_grid(mf_merged_kernel<FWD>, kT, 0, nt * 32);
+  mf_merged_kernel<FWD><<<g, kT, 0, s>>>(t0, nt, reinterpret_cast<const int4*>(mf->tasks), c);
+  XDG_CHECK_LAUNCH();
+  return XDG_OK;
+}
+
 // Gather entry e: W[ent_w] = scale * b[src] + children's contributions (in
 // fixed order).  Plain loads: in the fused kernel C was written by the same
 // launch (children of an earlier stage).
@@ -394,7 +608,7 @@ template <bool FWD>
 int launch_fused(const xdg_mf* mf, int k, const double* b, double* x, cudaStream_t s) {
   const int64_t g0 = mf->fb_grp[k], ng = mf->fb_grp[k + 1] - g0;
   if (ng <= 0) return XDG_OK;
-  Ctx c{mf->nodes, mf->F, mf->bidx, mf->pdst, mf->pscale, mf->W, mf->Y, mf->C, x};
+  Ctx c{mf->nodes, mf->F, mf->bidx, mf->pdst, mf->pscale, mf->W, mf->Y, mf->C, x, mf->X};
   const int g = resident_grid(mf_fused_kernel<FWD>, kT, 0, ng * kT);
   mf_fused_kernel<FWD><<<g, kT, 0, s>>>(g0, g0 + ng, *mf, b, c);
   XDG_CHECK_LAUNCH();
@@ -406,7 +620,7 @@ int launch_rows(const xdg_mf* mf, int h, double* x, cudaStream_t s) {
   const int64_t* lev = mf->lev_task + (int64_t)PH * (mf->nlevels + 1);
   const int64_t t0 = lev[h], nt = lev[h + 1] - t0;
   if (nt <= 0) return XDG_OK;
-  Ctx c{mf->nodes, mf->F, mf->bidx, mf->pdst, mf->pscale, mf->W, mf->Y, mf->C, x};
+  Ctx c{mf->nodes, mf->F, mf->bidx, mf->pdst, mf->pscale, mf->W, mf->Y, mf->C, x, mf->X};
   const int g = resident_grid(mf_rows_kernel<PH>, kT, 0, nt * 32);
   mf_rows_kernel<PH><<<g, kT, 0, s>>>(t0, nt, reinterpret_cast<const int4*>(mf->tasks), c);
   XDG_CHECK_LAUNCH();
@@ -423,6 +637,8 @@ extern "C" int xdg_mf_solve_phase(const xdg_mf* mf, const double* b, double* x, 
   using namespace xdg;
   XDG_REQUIRE(mf != nullptr && mf->nlevels >= 0 && phase >= 1 && phase <= 3, XDG_ERR_ARG,
               "bad multifrontal plan / phase");
+  XDG_REQUIRE(!mf->merged || (mf->nfbatch == 0 && mf->X != nullptr), XDG_ERR_ARG,
+              "merged multifrontal phases exclude the fused low levels and need X");
   NvtxRange nv("xdg_mf_solve");
   if (mf->total == 0 || mf->nlevels == 0) return XDG_OK;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -438,12 +654,20 @@ extern "C" int xdg_mf_solve_phase(const xdg_mf* mf, const double* b, double* x, 
             mf->C, mf->W);
         XDG_CHECK_LAUNCH();
       }
+      if (mf->merged) {
+        XDG_TRY(launch_merged<true>(mf, h, x, s));
+        continue;
+      }
       XDG_TRY(launch_rows<kLower>(mf, h, x, s));
       XDG_TRY(launch_rows<kBound>(mf, h, x, s));
     }
   }
   if (phase & 2) {  // backward: upb, upper per height
     for (int h = H - 1; h >= HF; --h) {
+      if (mf->merged) {
+        XDG_TRY(launch_merged<false>(mf, h, x, s));
+        continue;
+      }
       XDG_TRY(launch_rows<kUpb>(mf, h, x, s));
       XDG_TRY(launch_rows<kUpper>(mf, h, x, s));
     }
@@ -502,6 +726,101 @@ extern "C" int xdg_mf_extend_add(int64_t npairs, const int64_t* pair, const int6
   const int64_t gx = std::min<int64_t>(npairs, std::max<int64_t>(1, 8 * sm_count() / parts));
   mf_extend_add_kernel<<<dim3((unsigned)gx, (unsigned)parts), kT, 0, s>>>(npairs, pair, U,
                                                                         child, parent);
+  XDG_CHECK_LAUNCH();
+  return XDG_OK;
+}
+
+// Setup of the merged phases: for every front of a bucket (nb fronts, each
+// an n x n row-major buffer, n = P + B, holding the partial factorization
+// xdg_batched_factor left: triangular inverses in the leading P x P corner,
+// L_BP below, U_PB to the right)
+//   M = L_BP L^-1  (B x P, L^-1 unit lower: strictly-lower part stored)
+//   N = U^-1 U_PB  (P x B, U^-1 upper incl. diagonal)
+// written to the factor storage.  Tiled FP64 product, 64 x 64 tile per CTA,
+// 4 x 4 per thread, the triangular operand masked while it is staged and
+// the K range cut to its nonzero part.
+namespace xdg {
+namespace {
+constexpr int kMT = 64, kMK = 16;
+
+template <bool LOWER>  // true: M = L_BP L^-1;  false: N = U^-1 U_PB
+__global__ void __launch_bounds__(256)
+mf_merge_kernel(int P, int B, const double* __restrict__ Fb, double* __restrict__ out) {
+  __shared__ double As[kMK][kMT + 1], Bs[kMK][kMT + 1];
+  const int n = P + B;
+  const double* F = Fb + (int64_t)blockIdx.z * n * n;
+  const int rows = LOWER ? B : P, cols = LOWER ? P : B;
+  double* O = out + (int64_t)blockIdx.z * rows * cols;
+  const int i0 = blockIdx.y * kMT, j0 = blockIdx.x * kMT;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  // nonzero K range: L^-1[k, j] = 0 for k < j;  U^-1[i, k] = 0 for k < i
+  const int kbeg = ((LOWER ? j0 : i0) / kMK) * kMK;
+  for (int k0 = kbeg; k0 < P; k0 += kMK) {
+    // stage A (rows i0.., k chunk) and B (k chunk, cols j0..)
+    for (int e = threadIdx.x; e < kMK * kMT; e += 256) {
+      const int kk = e % kMK, ii = e / kMK;  // A: consecutive threads along k
+      const int i = i0 + ii, k = k0 + kk;
+      double v = 0.0;
+      if (i < rows && k < P) {
+        if (LOWER)
+          v = F[(int64_t)(P + i) * n + k];
+        else
+          v = (k >= i) ? F[(int64_t)i * n + k] : 0.0;
+      }
+      As[kk][ii] = v;
+      const int jj = e % kMT, kb = e / kMT;  // B: consecutive threads along j
+      const int j = j0 + jj, k2 = k0 + kb;
+      double w = 0.0;
+      if (j < cols && k2 < P) {
+        if (LOWER)
+          w = (k2 > j) ? F[(int64_t)k2 * n + j] : (k2 == j ? 1.0 : 0.0);
+        else
+          w = F[(int64_t)k2 * n + P + j];
+      }
+      Bs[kb][jj] = w;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < kMK; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        a[q] = As[kk][ty + 16 * q];
+        b[q] = Bs[kk][tx + 16 * q];
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) acc[q][r] = fma(a[q], b[r], acc[q][r]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int i = i0 + ty + 16 * q, j = j0 + tx + 16 * r;
+      if (i < rows && j < cols) O[(int64_t)i * cols + j] = acc[q][r];
+    }
+}
+}  // namespace
+}  // namespace xdg
+
+extern "C" int xdg_mf_merge(int64_t nb, int P, int B, const double* fronts, double* out_m,
+                            double* out_n, xdg_stream_t stream) {
+  using namespace xdg;
+  if (nb <= 0 || P <= 0 || B <= 0) return XDG_OK;
+  XDG_REQUIRE(nb <= 65535, XDG_ERR_ARG, "xdg_mf_merge: at most 65535 fronts per call");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const unsigned tp = (unsigned)((P + kMT - 1) / kMT), tb = (unsigned)((B + kMT - 1) / kMT);
+  mf_merge_kernel<true><<<dim3(tp, tb, (unsigned)nb), 256, 0, s>>>(P, B, fronts, out_m);
+  XDG_CHECK_LAUNCH();
+  mf_merge_kernel<false><<<dim3(tb, tp, (unsigned)nb), 256, 0, s>>>(P, B, fronts, out_n);
   XDG_CHECK_LAUNCH();
   return XDG_OK;
 }

@@ -82,6 +82,19 @@ def _fuse_mode() -> tuple[str, int]:
     return mode, int(k)
 
 
+def _merge_mode() -> bool:
+    """Merged phases (default): the factors hold M = L_BP L^-1 and N = U^-1
+    U_PB (xdg_mf_merge), one row launch per height and sweep instead of two.
+    XDG_MF_MERGE=0 keeps the four-phase solve (lower, bound, upb, upper);
+    the fused low levels (XDG_MF_FUSE) exist for the four-phase solve only."""
+    import os
+
+    v = os.environ.get("XDG_MF_MERGE", "1")
+    if v not in ("0", "1"):
+        raise ValueError(f"XDG_MF_MERGE={v}: expected 0 or 1")
+    return v == "1" and _fuse_mode()[0] == "off"
+
+
 def _rows_per_warp() -> int:
     """Rows a warp task of a whole-warp front covers: the kernel's kMR."""
     return int(nat.load().xdg_mf_rows_per_warp())
@@ -97,7 +110,8 @@ class XdgMf(C.Structure):
                             "pdst", "ent_scale", "pscale", "F", "W", "Y", "C")] + \
         [("apply_bytes", C.c_double), ("fuse_levels", C.c_int32), ("nfbatch", C.c_int32),
          ("nfstages", C.c_int64)] + \
-        [(f, _vp) for f in ("fb_grp", "g_stage", "st_ent", "st_task", "fent", "ftask")]
+        [(f, _vp) for f in ("fb_grp", "g_stage", "st_ent", "st_task", "fent", "ftask")] + \
+        [("X", _vp), ("merged", C.c_int32), ("pad_", C.c_int32)]
 
 
 def _ranges(starts: np.ndarray, ends: np.ndarray) -> np.ndarray:
@@ -428,6 +442,7 @@ class Multifrontal:
         # mapping; a rank factors and solves its owned subtrees plus the
         # shared top fronts (replicated), see proportional_map
         self.comm = comm if (comm is not None and comm.world > 1) else None
+        self.merged = merged = _merge_mode()
         if self.comm is not None:
             work = (pn * pn + 2 * pn * bn).astype(np.float64)
             self.rank_of = proportional_map(kids, parent, work, self.comm.world)
@@ -548,7 +563,7 @@ class Multifrontal:
             raise NotImplementedError("the multi-GPU factorization needs the device extend-add")
         bad_nodes, dev_perms = [], []
         xpos = {int(t): i for i, t in enumerate(self.xroot)}
-        xsend = []  # this rank's cross-rank roots' Schur complements, in xroot order
+        xsend = {}  # this rank's cross-rank roots' Schur complements, by front id
         for pass_buckets in (buckets, buckets_sh):
             if not pass_buckets:
                 continue
@@ -641,10 +656,24 @@ class Multifrontal:
                     if B_:
                         LBP = Fb[:, P_:, :P_]
                         bad |= ~torch.isfinite(LBP).flatten(1).all(1)
-                        o = int(lbp_off[ts[0]])
-                        self.F[o:o + nb * B_ * P_].view(nb, B_, P_).copy_(LBP)
-                        o = int(upb_off[ts[0]])
-                        self.F[o:o + nb * P_ * B_].view(nb, P_, B_).copy_(Fb[:, :P_, P_:])
+                        o, o2 = int(lbp_off[ts[0]]), int(upb_off[ts[0]])
+                        out_m = self.F[o:o + nb * B_ * P_].view(nb, B_, P_)
+                        out_n = self.F[o2:o2 + nb * P_ * B_].view(nb, P_, B_)
+                        if not merged:
+                            out_m.copy_(LBP)
+                            out_n.copy_(Fb[:, :P_, P_:])
+                        elif front_factor is not None:  # CPU planning tests
+                            INV = Fb[:, :P_, :P_]
+                            eye = torch.eye(P_, dtype=F64)
+                            out_m.copy_(LBP @ (torch.tril(INV, -1) + eye))
+                            out_n.copy_(torch.triu(INV) @ Fb[:, :P_, P_:])
+                        else:  # M = L_BP L^-1, N = U^-1 U_PB (xdg_mf_merge)
+                            for q0 in range(0, nb, 65535):
+                                q1 = min(nb, q0 + 65535)
+                                nat.check(ctx.lib.xdg_mf_merge(
+                                    q1 - q0, P_, B_, Fb[q0:q1].data_ptr(),
+                                    out_m[q0:q1].data_ptr(), out_n[q0:q1].data_ptr(),
+                                    ctx.stream), "mf_merge")
                     o = int(inv_off[ts[0]])
                     self.F[o:o + nb * P_ * P_].view(nb, P_, P_).copy_(Fb[:, :P_, :P_])
                     bad_nodes.append((ts, bad))
@@ -652,7 +681,7 @@ class Multifrontal:
                     for q, t in enumerate(ts):  # Schur complements other ranks need
                         if t in xpos:
                             b_ = int(bn[t])
-                            xsend.append(Fb[q, P_:P_ + b_, P_:P_ + b_].reshape(-1).clone())
+                            xsend[int(t)] = Fb[q, P_:P_ + b_, P_:P_ + b_].reshape(-1).clone()
                 for hh in range(h + 1):
                     if hh in fronts and last_use[hh] <= h:
                         del fronts[hh]
@@ -663,7 +692,9 @@ class Multifrontal:
                 # top fronts; they are read in place by the extend-add
                 per_rank = [int(sum(int(bn[t]) ** 2 for t in self.xroot
                                     if self.rank_of[t] == r)) for r in range(self.comm.world)]
-                mine = (torch.cat(xsend) if xsend
+                # sent in xroot order (the fronts were factored height by height)
+                mine_t = [int(t) for t in self.xroot if int(t) in xsend]
+                mine = (torch.cat([xsend[t] for t in mine_t]) if mine_t
                         else torch.zeros(0, dtype=F64, device=dev))
                 recv = self.comm.allgather_cat(mine, per_rank)
                 off = 0
@@ -749,6 +780,8 @@ class Multifrontal:
         # warp tasks, level-sorted: (node, first row), 32/G rows each
         gp = np.array([_group(int(x)) for x in pn], np.int64)
         gb = np.array([_group(int(x)) if x else g for x, g in zip(bn, gp)], np.int64)
+        if merged:  # a backward row = U^-1 row (<= p long) + N_PB row (b long)
+            gb = np.maximum(gp, gb)
 
         def tasks(phase, cls):
             """int4 warp tasks (node, first row, rows, -1) of one phase, level
@@ -756,13 +789,18 @@ class Multifrontal:
             per task; shorter rows 32/G rows per task (rows field 0)."""
             g = gb if phase == 2 else gp
             nrows = bn if phase == 1 else pn
+            if merged:  # phase 0: forward rows 0..p+b-1; phase 2: backward rows
+                nrows = pn + bn if phase == 0 else pn
             out, lev = [], []
             for h in range(H):
                 ts = order[(height[order] == h) & cls[order]]
+                if merged and phase in (1, 3):
+                    lev.append(0)
+                    continue
                 sh = ts[g[ts] < 32]
                 # bound / upb rows all span the same columns: two row sets
                 # per task share the vector loads (kernel: group_dot2)
-                sets = SETS if phase in (1, 2) else 1
+                sets = 2 if merged else (SETS if phase in (1, 2) else 1)
                 per = (32 // g[sh]) * sets
                 cnt = (nrows[sh] + per - 1) // per
                 first = _ranges(np.zeros(len(sh), np.int64), cnt) * np.repeat(per, cnt)
@@ -795,7 +833,7 @@ class Multifrontal:
         lev_task = lev_task_k[0]
         lev_ent = lev_ent_k[0]
         self._fused_plan(task_arr, lev_task, ent_first, pn, bn, height, parent, order, H,
-                         off=self.comm is not None)
+                         off=self.comm is not None or merged)
         bidx = np.zeros(int(bn.sum()), np.int64)
         pdst = np.zeros(int(pn.sum()), np.int64)
         pscale = np.ones(int(pn.sum()))
@@ -832,6 +870,7 @@ class Multifrontal:
         self.W = torch.zeros(max(int((pn + bn).sum()), 1), dtype=F64, device=dev)
         self.Y = torch.zeros(max(int(pn.sum()), 1), dtype=F64, device=dev)
         self.C = torch.zeros(max(int(bn.sum()), 1), dtype=F64, device=dev)
+        self.X = torch.zeros(max(int(pn.sum()), 1) if merged else 1, dtype=F64, device=dev)
         self.factor_bytes = 8 * int((pn * pn + 2 * pn * bn)[need].sum())
         self.apply_bytes = self.factor_bytes + 8 * int(4 * (pn + bn)[need].sum()
                                                        + 4 * pn[need].sum())
@@ -1014,6 +1053,7 @@ class Multifrontal:
             s.fb_grp = self.fb_grp.ctypes.data
             for f in ("g_stage", "st_ent", "st_task", "fent", "ftask"):
                 setattr(s, f, getattr(self, f).data_ptr())
+            s.X, s.merged = self.X.data_ptr(), int(self.merged)
             self._s = s
         return self._s
 

@@ -53,6 +53,8 @@ def emulate_solve(mf, b, xlen):
     tasks = mf.task_host
     H = mf.nlevels
 
+    merged = getattr(mf, "merged", False)
+
     def rows(phase, h):  # (node, row) pairs of one phase and level, in order
         lev = mf.lev_task[phase * (H + 1):(phase + 1) * (H + 1)]
         g, count = ("gb" if phase == 2 else "gp"), ("b" if phase == 1 else "p")
@@ -61,7 +63,8 @@ def emulate_solve(mf, b, xlen):
             nd = nodes[t]
             # MR rows, or 32/G rows of G lanes (two such sets: nr == -2)
             n = nr if nr > 0 else (32 // nd[g]) * (2 if nr == -2 else 1)
-            out += [(t, r) for r in range(r0, min(r0 + n, nd[count]))]
+            last = nd["p"] + nd["b"] if (merged and phase == 0) else nd[count]
+            out += [(t, r) for r in range(r0, min(r0 + n, last))]
         return out
 
     W, Y, Cb = np.zeros(mf.W.numel()), np.zeros(mf.Y.numel()), np.zeros(mf.C.numel())
@@ -72,6 +75,18 @@ def emulate_solve(mf, b, xlen):
             for k in range(cptr[e], cptr[e + 1]):
                 v += Cb[cidx[k]]
             W[ent_w[e]] = v
+        if merged:  # one phase: Y = L^-1 W_P and C = W_B - (L_BP L^-1) W_P
+            for t, r in rows(0, h):
+                nd = nodes[t]
+                p = nd["p"]
+                wp = W[nd["w"]:nd["w"] + p]
+                if r < p:
+                    row = F[nd["inv"] + r * nd["ldp"]:][:r]
+                    Y[nd["y"] + r] = W[nd["w"] + r] + row @ wp[:r]
+                else:
+                    row = F[nd["lbp"] + (r - p) * nd["ldp"]:][:p]
+                    Cb[nd["c"] + r - p] = W[nd["w"] + r] - row @ wp
+            continue
         for t, i in rows(0, h):
             nd = nodes[t]
             row = F[nd["inv"] + i * nd["ldp"]:][:i]
@@ -80,7 +95,20 @@ def emulate_solve(mf, b, xlen):
             nd = nodes[t]
             row = F[nd["lbp"] + j * nd["ldp"]:][:nd["p"]]
             Cb[nd["c"] + j] = W[nd["w"] + nd["p"] + j] - row @ Y[nd["y"]:nd["y"] + nd["p"]]
+    X = np.zeros(mf.Y.numel())
     for h in range(mf.nlevels - 1, -1, -1):  # backward: U_PB x_B, U^-1
+        if merged:  # one phase: X_P = U^-1 Y - (U^-1 U_PB) X_B
+            for t, i in rows(2, h):
+                nd = nodes[t]
+                p = nd["p"]
+                row = F[nd["inv"] + i * nd["ldp"]:][:p]
+                d = row[i:] @ Y[nd["y"] + i:nd["y"] + p]
+                if nd["b"]:
+                    rn = F[nd["upb"] + i * nd["ldb"]:][:nd["b"]]
+                    d -= rn @ X[bidx[nd["bx"]:nd["bx"] + nd["b"]]]
+                X[nd["y"] + i] = d
+                x[pdst[nd["px"] + i]] = pscale[nd["px"] + i] * d
+            continue
         for t, i in rows(2, h):
             nd = nodes[t]
             d = 0.0

@@ -137,11 +137,33 @@ def test_fused_low_levels_bit_identical(case, monkeypatch):
         g = torch.Generator(device=ctx.device).manual_seed(lam)
         b = torch.randn(D.nbr * D.N, dtype=torch.float64, device=ctx.device, generator=g)
         out = []
+        monkeypatch.setenv("XDG_MF_MERGE", "0")  # the fused levels run the four-phase tasks
         for mode in ("0", "level:3", "tree:2", "tree:5", "tree:99"):
             monkeypatch.setenv("XDG_MF_FUSE", mode)
             out.append(SparseDirect(D, ctx).apply(b))
         for o in out[1:]:
             assert torch.equal(out[0], o), (case, lam)
+
+
+@pytest.mark.parametrize("case", ["bench4", "cfg1", "sphere8p3"])
+def test_merged_phases_match_four_phase_solve(case, monkeypatch):
+    """Merged phases (M = L_BP L^-1, N = U^-1 U_PB formed at setup by
+    xdg_mf_merge; one row launch per height and sweep) against the
+    four-phase solve of the same factorization: roundoff-level agreement."""
+    z, meta, hier = load(case)
+    ctx = Context.get()
+    for lam in range(1, hier.num_levels + 1):
+        D = hier.level(lam).matrix.device(ctx)
+        g = torch.Generator(device=ctx.device).manual_seed(lam)
+        b = torch.randn(D.nbr * D.N, dtype=torch.float64, device=ctx.device, generator=g)
+        out = []
+        for mode in ("0", "1"):
+            monkeypatch.setenv("XDG_MF_MERGE", mode)
+            sd = SparseDirect(D, ctx)
+            assert bool(sd.mf.merged) == (mode == "1")
+            out.append(sd.apply(b))
+        err = float((out[0] - out[1]).norm() / out[0].norm())
+        assert err <= 1e-11, (case, lam, err)
 
 
 @pytest.mark.parametrize("case", ["bench4", "cfg1", "sphere8p3"])

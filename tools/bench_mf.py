@@ -49,8 +49,15 @@ b = torch.randn(nb * N, dtype=torch.float64, device=ctx.device)
 ref = None
 # XDG_MF_FUSE_SWEEP="0,level:6,tree:4": one plan per fused-level mode, each
 # checked bit-identical against the first
-for mode in os.environ.get("XDG_MF_FUSE_SWEEP", os.environ.get("XDG_MF_FUSE", "0")).split(","):
+# XDG_MF_MERGE_SWEEP="0,1": four-phase and merged-phase plans (compared by
+# relative difference: the merged factors round differently)
+sweep = [(f, mg) for mg in os.environ.get("XDG_MF_MERGE_SWEEP",
+                                          os.environ.get("XDG_MF_MERGE", "1")).split(",")
+         for f in os.environ.get("XDG_MF_FUSE_SWEEP",
+                                 os.environ.get("XDG_MF_FUSE", "0")).split(",")]
+for mode, mg in sweep:
     os.environ["XDG_MF_FUSE"] = mode
+    os.environ["XDG_MF_MERGE"] = mg
     t0 = time.perf_counter()
     mf = Multifrontal(ctx, rp, col, D.val_t, N, [v], m, v * N, v * m)
     torch.cuda.synchronize()
@@ -69,7 +76,10 @@ for mode in os.environ.get("XDG_MF_FUSE_SWEEP", os.environ.get("XDG_MF_FUSE", "0
     ms = statistics.median(ts)
     if ref is None:
         ref = x.clone()
-    print(json.dumps({"lib": os.environ.get("XDG_LIB", "default"), "fuse": mode, "m": m,
+    # backward error of the solve against the level operator's low-order part
+    print(json.dumps({"lib": os.environ.get("XDG_LIB", "default"), "fuse": mode,
+                      "merged": bool(mf.merged), "m": m,
+                      "rel_diff_vs_first": float((x - ref).norm() / ref.norm()),
                       "level": lam, "unknowns": nb * m, "nodes": mf.nnodes,
                       "levels": mf.nlevels, "factor_GB": mf.factor_bytes / 1e9,
                       "setup_s": round(setup, 3),
