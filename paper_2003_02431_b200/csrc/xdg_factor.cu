@@ -42,6 +42,7 @@
 #include <algorithm>
 
 #include "xdg_common.cuh"
+#include "xdg_dmma.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -49,8 +50,6 @@ namespace xdg {
 namespace {
 
 constexpr int kPT = 256;       // panel CTA threads
-constexpr int kTile = 64;      // update tile edge
-constexpr int kKc = 16;        // K chunk of the update tile
 constexpr int kMaxCluster = 16;
 
 struct Mat {
@@ -230,17 +229,19 @@ lu_panel_kernel(int64_t nmat, double* __restrict__ A, const int64_t* __restrict_
   cluster.sync();  // no CTA leaves while its shared memory may still be read
 }
 
-// U12 = L11^-1 A12: rows k0..k0+kb-1, columns k0+kb..n-1; grid (column
-// chunks of kPT, matrices).
+// U12 = L11^-1 A12: rows k0..k0+kb-1, columns right of the panel inside
+// [c_lo, c_hi); grid (column chunks of kPT, matrices).
 __global__ void __launch_bounds__(kPT)
 lu_trsm_kernel(double* __restrict__ A, const int64_t* __restrict__ off,
                const int* __restrict__ dn, const int* __restrict__ dp,
-               const int* __restrict__ dld, int k0, int NB) {
+               const int* __restrict__ dld, int k0, int NB, int c_lo, int c_hi) {
   extern __shared__ double L[];  // kb x kb
-  const Mat M = mat_of(A, off, dn, dp, dld, blockIdx.y);
+  Mat M = mat_of(A, off, dn, dp, dld, blockIdx.y);
   if (k0 >= M.p) return;
   const int kb = min(NB, M.p - k0);
-  const int c0 = k0 + kb + blockIdx.x * kPT;
+  // columns [max(k0 + kb, c_lo), min(c_hi, n))
+  const int c0 = max(k0 + kb, c_lo) + blockIdx.x * kPT;
+  M.n = min(M.n, c_hi);
   if (c0 >= M.n) return;
   for (int e = threadIdx.x; e < kb * kb; e += kPT)
     L[e] = M.a[(int64_t)(k0 + e / kb) * M.ld + k0 + e % kb];
@@ -258,85 +259,43 @@ lu_trsm_kernel(double* __restrict__ A, const int64_t* __restrict__ off,
   }
 }
 
-// 64 x 64 tile of C (+)= alpha * A B accumulated over K in chunks, 4 x 4
-// per thread.  Loader callbacks give A(i, k) / B(k, j) (zero outside).
-struct TileAcc {
-  double c[4][4];
-};
-
-template <class FA, class FB>
-__device__ __forceinline__ void tile_mma(TileAcc& acc, int K, FA fa, FB fb,
-                                         double (*As)[kTile + 1], double (*Bs)[kTile + 1]) {
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) acc.c[i][j] = 0.0;
-  for (int kc = 0; kc < K; kc += kKc) {
-    // As[k][i] = A(i, kc + k), Bs[k][j] = B(kc + k, j)
-    for (int e = threadIdx.x; e < kKc * kTile; e += 256) {
-      const int i = e / kKc, k = e - i * kKc;  // k fastest: row-contiguous A reads
-      As[k][i] = fa(i, kc + k);
-      const int kk = e / kTile, j = e - kk * kTile;
-      Bs[kk][j] = fb(kc + kk, j);
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < kKc; ++k) {
-      double a[4], bb[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[k][ty * 4 + i];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) bb[j] = Bs[k][tx * 4 + j];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc.c[i][j] = __fma_rn(a[i], bb[j], acc.c[i][j]);
-    }
-    __syncthreads();
-  }
-}
-
-// A22 -= L21 U12 over rows/columns k0+kb..n-1; grid (tiles, matrices).
-__global__ void __launch_bounds__(256)
+// A[r0:r1, c0:c1] -= A[r0:r1, q0:q1] A[q0:q1, c0:c1] inside every matrix of
+// the batch (ranges clipped to the matrix: rows / columns to n, the K range
+// to its eliminated columns p); grid (tiles, matrices).  The trailing update
+// of the blocked LU (A22 -= L21 U12) and its deferred parts.
+template <int BT>
+__global__ void __launch_bounds__(256, BT >= 128 ? 1 : 2)
 lu_update_kernel(double* __restrict__ A, const int64_t* __restrict__ off,
                  const int* __restrict__ dn, const int* __restrict__ dp,
-                 const int* __restrict__ dld, int k0, int NB) {
-  __shared__ double As[kKc][kTile + 1];
-  __shared__ double Bs[kKc][kTile + 1];
+                 const int* __restrict__ dld, int r0, int r1, int c0, int c1, int q0, int q1,
+                 int ntc, int after_panel) {
+  __shared__ DmmaSmem<BT, BT> sm;
   const Mat M = mat_of(A, off, dn, dp, dld, blockIdx.y);
-  if (k0 >= M.p) return;
-  const int kb = min(NB, M.p - k0);
-  const int s = k0 + kb;
-  const int m = M.n - s;
-  if (m <= 0) return;
-  const int nt = (m + kTile - 1) / kTile;
-  if ((int)blockIdx.x >= nt * nt) return;
-  const int ti = blockIdx.x / nt, tj = blockIdx.x - ti * nt;
-  const int i0 = s + ti * kTile, j0 = s + tj * kTile;
-  const double* a = M.a;
-  const int ld = M.ld, n = M.n;
-  TileAcc acc;
-  tile_mma(
-      acc, kb,
+  const int qe = min(q1, M.p), ce = min(c1, M.n);
+  if (qe <= q0) return;
+  // flags: 1 / 2 -- the row / column range starts right after this
+  // matrix's own eliminated columns [q0, qe) (qe < q1 when its p falls
+  // inside them); 4 -- the row range ends at this matrix's p
+  if (after_panel & 1) r0 = qe;
+  if (after_panel & 2) c0 = qe;
+  const int re = min((after_panel & 4) ? min(r1, M.p) : r1, M.n);
+  const int ti = blockIdx.x / ntc, tj = blockIdx.x - ti * ntc;
+  const int i0 = r0 + ti * BT, j0 = c0 + tj * BT;
+  if (i0 >= re || j0 >= ce) return;
+  double* a = M.a;
+  const int ld = M.ld;
+  tile_dmma<BT, BT>(
+      qe - q0,
       [&](int i, int k) {
-        return (i0 + i < n && k < kb) ? a[(int64_t)(i0 + i) * ld + k0 + k] : 0.0;
+        return (i0 + i < re && q0 + k < qe) ? a[(int64_t)(i0 + i) * ld + q0 + k] : 0.0;
       },
       [&](int k, int j) {
-        return (j0 + j < n && k < kb) ? a[(int64_t)(k0 + k) * ld + j0 + j] : 0.0;
+        return (j0 + j < ce && q0 + k < qe) ? a[(int64_t)(q0 + k) * ld + j0 + j] : 0.0;
       },
-      As, Bs);
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int gi = i0 + ty * 4 + i;
-    if (gi >= n) continue;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int gj = j0 + tx * 4 + j;
-      if (gj < n) M.a[(int64_t)gi * ld + gj] -= acc.c[i][j];
-    }
-  }
+      [&](int i, int j, double v) {
+        if (i0 + i < re && j0 + j < ce) a[(int64_t)(i0 + i) * ld + j0 + j] -= v;
+      },
+      sm);
 }
 
 // ---------------------------------------------------------------------------
@@ -360,14 +319,15 @@ __device__ __forceinline__ double* trtri_ws(double* W, int64_t wstride, int b, i
   return W + (2 * (int64_t)b + z) * wstride;
 }
 
-// grid (64-column tiles, matrices, 2)
+constexpr int kTN = 128;  // column tile of the trtri product
+
+// grid (128-column tiles, matrices, 2); block rows of NB <= 64
 __global__ void __launch_bounds__(256)
 trtri_gemm_kernel(double* __restrict__ A, const int64_t* __restrict__ off,
                   const int* __restrict__ dn, const int* __restrict__ dp,
                   const int* __restrict__ dld, double* __restrict__ W, int64_t wstride,
                   int step, int NB) {
-  __shared__ double As[kKc][kTile + 1];
-  __shared__ double Bs[kKc][kTile + 1];
+  __shared__ DmmaSmem<64, kTN> sm;
   const Mat M = mat_of(A, off, dn, dp, dld, blockIdx.y);
   const int nblk = (M.p + NB - 1) / NB;
   if (step >= nblk) return;
@@ -376,7 +336,7 @@ trtri_gemm_kernel(double* __restrict__ A, const int64_t* __restrict__ off,
   const int i0 = i * NB, kb = min(NB, M.p - i0);
   const int cbeg = z == 0 ? i0 : 0;
   const int cend = z == 0 ? M.p : i0 + kb;
-  const int j0 = cbeg + blockIdx.x * kTile;
+  const int j0 = cbeg + blockIdx.x * kTN;
   if (j0 >= cend) return;
   const double* a = M.a;
   const int ld = M.ld, P = M.p;
@@ -385,12 +345,15 @@ trtri_gemm_kernel(double* __restrict__ A, const int64_t* __restrict__ off,
   if (blockIdx.x == 0)  // original diagonal block for the solve step
     for (int e = threadIdx.x; e < kb * kb; e += 256)
       Dg[e] = a[(int64_t)(i0 + e / kb) * ld + i0 + e % kb];
-  TileAcc acc;
+  auto store = [&](int r, int c, double v) {
+    const int gj = j0 + c;
+    if (r < kb && gj < cend) R[(int64_t)r * P + gj] = (gj == i0 + r ? 1.0 : 0.0) - v;
+  };
   if (z == 0) {
-    // K over k in [i0 + kb, min(P, j0 + 64)): X[k][j] upper (k <= j)
-    const int kbeg = i0 + kb, kend = min(P, j0 + kTile);
-    tile_mma(
-        acc, max(0, kend - kbeg),
+    // K over k in [i0 + kb, min(P, j0 + tile)): X[k][j] upper (k <= j)
+    const int kbeg = i0 + kb, kend = min(P, j0 + kTN);
+    tile_dmma<64, kTN>(
+        max(0, kend - kbeg),
         [&](int r, int k) {
           const int gk = kbeg + k;
           return (r < kb && gk < kend) ? a[(int64_t)(i0 + r) * ld + gk] : 0.0;
@@ -399,12 +362,12 @@ trtri_gemm_kernel(double* __restrict__ A, const int64_t* __restrict__ off,
           const int gk = kbeg + k, gj = j0 + c;
           return (gk < kend && gj < cend && gk <= gj) ? a[(int64_t)gk * ld + gj] : 0.0;
         },
-        As, Bs);
+        store, sm);
   } else {
     // K over k in [j0, i0): X[k][j] unit lower (k > j stored, k == j -> 1)
     const int kbeg = j0, kend = i0;
-    tile_mma(
-        acc, max(0, kend - kbeg),
+    tile_dmma<64, kTN>(
+        max(0, kend - kbeg),
         [&](int r, int k) {
           const int gk = kbeg + k;
           return (r < kb && gk < kend) ? a[(int64_t)(i0 + r) * ld + gk] : 0.0;
@@ -414,18 +377,7 @@ trtri_gemm_kernel(double* __restrict__ A, const int64_t* __restrict__ off,
           if (gk >= kend || gj >= cend || gk < gj) return 0.0;
           return gk == gj ? 1.0 : a[(int64_t)gk * ld + gj];
         },
-        As, Bs);
-  }
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int r = ty * 4 + q;
-    if (r >= kb) continue;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int gj = j0 + tx * 4 + c;
-      if (gj < cend) R[(int64_t)r * P + gj] = (gj == i0 + r ? 1.0 : 0.0) - acc.c[q][c];
-    }
+        store, sm);
   }
 }
 
@@ -498,6 +450,20 @@ int panel_nb(int max_n) {
 }
 
 constexpr size_t kSmemCap = 200 * 1024;
+constexpr int kTrtriNB = 64;  // block rows of the triangular inverses
+
+// width of a super-panel: its inner panels (NB columns, bounded by the
+// cluster's shared memory) update only the super-panel's own rows and
+// columns; the rest of the trailing matrix gets one update with K = KB
+int super_nb(int max_n, int NB) {
+  static const int forced = [] {
+    const char* e = getenv("XDG_FACTOR_KB");
+    return e ? atoi(e) : 0;
+  }();
+  int kb = max_n > 1024 ? 256 : (max_n > 256 ? 128 : NB);
+  if (forced >= NB && forced % NB == 0) kb = forced;
+  return std::max(kb, NB);
+}
 
 }  // namespace
 }  // namespace xdg
@@ -507,7 +473,8 @@ using namespace xdg;
 extern "C" int64_t xdg_batched_factor_ws_bytes(int64_t nmat, int max_p) {
   // per matrix and sweep: NB x max_p (R) + NB x NB (diagonal block); NB as
   // chosen for max_n >= max_p is at most panel_nb(max_p)
-  const int NB = panel_nb(max_p);
+  (void)panel_nb;
+  const int NB = kTrtriNB;
   return 2 * nmat * ((int64_t)NB * std::max(max_p, 1) + (int64_t)NB * NB) * 8;
 }
 
@@ -533,52 +500,92 @@ extern "C" int xdg_batched_factor(int64_t nmat, const int64_t* off, const int* n
     attr_done = true;
   }
   XDG_TRY_CUDA(cudaMemsetAsync(info, 0, sizeof(int) * nmat, s));
-  for (int k0 = 0; k0 < max_p; k0 += NB) {
-    const int rows = max_n - k0;
-    // smallest cluster whose row share fits the shared-memory budget
-    int C = 1;
-    auto need = [&](int c) {
-      const int rpc = (rows + c - 1) / c;
-      return (size_t)rpc * (NB + 1) * 8 + 2 * NB * 8 + 64;
-    };
-    while (C < kMaxCluster && need(C) > kSmemCap) C *= 2;
-    XDG_REQUIRE(need(C) <= kSmemCap, XDG_ERR_ARG, "matrix too large (n=%d)", max_n);
-    const int rpc = (rows + C - 1) / C;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(nmat * C));
-    cfg.blockDim = dim3(kPT);
-    cfg.dynamicSmemBytes = need(C);
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = C;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    XDG_TRY_CUDA(cudaLaunchKernelEx(&cfg, lu_panel_kernel, nmat, A, off, n, p, ld, perm,
-                                    perm_off, info, k0, NB, rpc));
-    const int right = max_n - k0 - 1;  // upper bound of columns right of the panel
-    if (right > 0) {
-      dim3 g1((unsigned)((right + kPT - 1) / kPT), (unsigned)nmat);
-      lu_trsm_kernel<<<g1, kPT, NB * NB * 8, s>>>(A, off, n, p, ld, k0, NB);
-      XDG_CHECK_LAUNCH();
-      const int nt = (right + kTile - 1) / kTile;
-      dim3 g2((unsigned)(nt * nt), (unsigned)nmat);
-      lu_update_kernel<<<g2, 256, 0, s>>>(A, off, n, p, ld, k0, NB);
-      XDG_CHECK_LAUNCH();
+  const int KB = super_nb(max_n, NB);
+  auto update = [&](int r0, int r1, int c0, int c1, int q0, int q1, int flags) -> int {
+    r1 = std::min(r1, max_n);
+    c1 = std::min(c1, max_n);
+    // tile counts for the widest per-matrix range (a range that starts
+    // after a matrix's own panel starts at q0 + 1 at the earliest)
+    const int nr = r1 - ((flags & 1) ? q0 + 1 : r0);
+    const int nc = c1 - ((flags & 2) ? q0 + 1 : c0);
+    if (nr <= 0 || nc <= 0 || q1 <= q0) return XDG_OK;
+    if (std::max(nr, nc) > 256) {
+      const int ntr = (nr + 127) / 128, ntc = (nc + 127) / 128;
+      lu_update_kernel<128><<<dim3((unsigned)(ntr * ntc), (unsigned)nmat), 256, 0, s>>>(
+          A, off, n, p, ld, r0, r1, c0, c1, q0, q1, ntc, flags);
+    } else {
+      const int ntr = (nr + 63) / 64, ntc = (nc + 63) / 64;
+      lu_update_kernel<64><<<dim3((unsigned)(ntr * ntc), (unsigned)nmat), 256, 0, s>>>(
+          A, off, n, p, ld, r0, r1, c0, c1, q0, q1, ntc, flags);
+    }
+    XDG_CHECK_LAUNCH();
+    return XDG_OK;
+  };
+  auto trsm = [&](int k0, int c_lo, int c_hi) -> int {
+    const int lo = std::max(k0 + 1, c_lo), hi = std::min(c_hi, max_n);
+    if (hi <= lo) return XDG_OK;
+    dim3 g1((unsigned)((hi - lo + kPT - 1) / kPT), (unsigned)nmat);
+    lu_trsm_kernel<<<g1, kPT, NB * NB * 8, s>>>(A, off, n, p, ld, k0, NB, c_lo, c_hi);
+    XDG_CHECK_LAUNCH();
+    return XDG_OK;
+  };
+  // Two-level right-looking LU.  Inside a super-panel [K0, K1) the inner
+  // panels (NB columns) update only the super-panel's columns; the columns
+  // right of it see the row interchanges only (full-row swaps) until the
+  // super-panel is done, then U12 = L11^-1 A12 block row by block row and one
+  // trailing update with K = KB (LAPACK's getrf order: laswp, trsm, gemm).
+  for (int K0 = 0; K0 < max_p; K0 += KB) {
+    const int K1 = std::min(K0 + KB, max_n), Kp = std::min(K0 + KB, max_p);
+    for (int k0 = K0; k0 < Kp; k0 += NB) {
+      const int rows = max_n - k0;
+      // smallest cluster whose row share fits the shared-memory budget
+      int C = 1;
+      auto need = [&](int c) {
+        const int rpc = (rows + c - 1) / c;
+        return (size_t)rpc * (NB + 1) * 8 + 2 * NB * 8 + 64;
+      };
+      while (C < kMaxCluster && need(C) > kSmemCap) C *= 2;
+      XDG_REQUIRE(need(C) <= kSmemCap, XDG_ERR_ARG, "matrix too large (n=%d)", max_n);
+      const int rpc = (rows + C - 1) / C;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)(nmat * C));
+      cfg.blockDim = dim3(kPT);
+      cfg.dynamicSmemBytes = need(C);
+      cfg.stream = s;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = C;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      XDG_TRY_CUDA(cudaLaunchKernelEx(&cfg, lu_panel_kernel, nmat, A, off, n, p, ld, perm,
+                                      perm_off, info, k0, NB, rpc));
+      // inside the super-panel: U12 and the update of its remaining columns
+      XDG_TRY(trsm(k0, 0, K1));
+      XDG_TRY(update(0, max_n, 0, K1, k0, k0 + NB, 1 | 2));
+    }
+    if (K1 < max_n) {
+      // right of the super-panel: block rows of U12 in order, each after the
+      // products with the block rows above it, then the deferred update
+      for (int k0 = K0; k0 < Kp; k0 += NB) {
+        if (k0 > K0) XDG_TRY(update(k0, k0 + NB, K1, max_n, K0, k0, 4));
+        XDG_TRY(trsm(k0, K1, max_n));
+      }
+      XDG_TRY(update(0, max_n, K1, max_n, K0, K0 + KB, 1));
     }
   }
   if (!invert) return XDG_OK;
   // workspace per (matrix, sweep): NB x max_p for R + NB x NB diagonal block
-  const int64_t wstride = (int64_t)NB * max_p + (int64_t)NB * NB;
-  const int nblk = (max_p + NB - 1) / NB;
+  const int TB = kTrtriNB;
+  const int64_t wstride = (int64_t)TB * max_p + (int64_t)TB * TB;
+  const int nblk = (max_p + TB - 1) / TB;
   for (int st = 0; st < nblk; ++st) {
-    dim3 g1((unsigned)((max_p + kTile - 1) / kTile), (unsigned)nmat, 2);
-    trtri_gemm_kernel<<<g1, 256, 0, s>>>(A, off, n, p, ld, ws, wstride, st, NB);
+    dim3 g1((unsigned)((max_p + kTN - 1) / kTN), (unsigned)nmat, 2);
+    trtri_gemm_kernel<<<g1, 256, 0, s>>>(A, off, n, p, ld, ws, wstride, st, TB);
     XDG_CHECK_LAUNCH();
     dim3 g2((unsigned)((max_p + 255) / 256), (unsigned)nmat, 2);
-    trtri_solve_kernel<<<g2, 256, 0, s>>>(A, off, n, p, ld, ws, wstride, st, NB);
+    trtri_solve_kernel<<<g2, 256, 0, s>>>(A, off, n, p, ld, ws, wstride, st, TB);
     XDG_CHECK_LAUNCH();
   }
   return XDG_OK;

@@ -25,6 +25,7 @@
 #include <algorithm>
 
 #include "xdg_common.cuh"
+#include "xdg_dmma.cuh"
 
 namespace xdg {
 namespace {
@@ -134,8 +135,7 @@ constexpr int kMU = MF_MU;
 
 template <typename V>
 __device__ __forceinline__ void multi_dot(const double* const* rows, V v, int lo, int hi,
-                                          const int* r0, const int* r1, int lane,
-                                          double* d) {
+                                          const int* r0, const int* r1, int lane, double* d) {
   double acc[kMR][2];
 #pragma unroll
   for (int q = 0; q < kMR; ++q) acc[q][0] = acc[q][1] = 0.0;
@@ -449,46 +449,80 @@ __device__ __forceinline__ void bwd_done(const Ctx& c, const xdg_mf_node& nd, in
   c.x[c.pdst[nd.px + r]] = __dmul_rn(c.pscale[nd.px + r], d);
 }
 
+// kMR consecutive rows r .. of one front over the chunks (j_off, j_step):
+// d = the U^-1 / L^-1 / M_BP part, e = the N_PB part (backward only).
+// this warp's share [lo + (hi-lo) w/n, lo + (hi-lo) (w+1)/n) of a range,
+// cut at multiples of 32 elements (shares equal in bytes: the warps of a
+// CTA task finish together)
+__device__ __forceinline__ void warp_share(int& lo, int& hi, int w, int n) {
+  if (n == 1 || hi <= lo) return;
+  const int len = hi - lo;
+  const int a = lo + (int)(((int64_t)len * w / n) & ~31LL);
+  const int b = (w == n - 1) ? hi : lo + (int)(((int64_t)len * (w + 1) / n) & ~31LL);
+  lo = a;
+  hi = b;
+}
+
+template <bool FWD>
+__device__ __forceinline__ void merged_rows(const Ctx& c, const xdg_mf_node& nd, int r,
+                                            int nrows, int lane, int w, int nw, double* d,
+                                            double* e) {
+  const double* rows[kMR];
+  int r0[kMR], r1[kMR];
+  int lo = 1 << 30, hi = 0;
+#pragma unroll
+  for (int q = 0; q < kMR; ++q) {
+    const int rq = min(r + q, nrows - 1);
+    if (FWD) {
+      r0[q] = 0;
+      rows[q] = fwd_row(c, nd, rq, r1[q]);
+    } else {
+      rows[q] = c.F + nd.inv + (int64_t)rq * nd.ldp;
+      r0[q] = rq;
+      r1[q] = nd.p;
+    }
+    if (r + q >= nrows) r1[q] = r0[q];
+    if (r1[q] > r0[q]) {
+      lo = min(lo, r0[q]);
+      hi = max(hi, r1[q]);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < kMR; ++q) d[q] = e[q] = 0.0;
+  warp_share(lo, hi, w, nw);
+#pragma unroll
+  for (int q = 0; q < kMR; ++q) {  // the rows' ranges inside this warp's share
+    r0[q] = max(r0[q], lo);
+    r1[q] = min(r1[q], hi);
+  }
+  if (hi > lo) multi_dot(rows, Direct{FWD ? c.W + nd.w : c.Y + nd.y}, lo, hi, r0, r1, lane, d);
+  if (!FWD && nd.b > 0) {
+#pragma unroll
+    for (int q = 0; q < kMR; ++q) {
+      const int rq = min(r + q, nrows - 1);
+      rows[q] = c.F + nd.upb + (int64_t)rq * nd.ldb;
+      r0[q] = 0;
+      r1[q] = (r + q < nrows) ? nd.b : 0;
+    }
+    int nlo = 0, nhi = nd.b;
+    warp_share(nlo, nhi, w, nw);
+#pragma unroll
+    for (int q = 0; q < kMR; ++q) {
+      r0[q] = nlo;
+      r1[q] = (r + q < nrows) ? nhi : nlo;
+    }
+    if (nhi > nlo) multi_dot(rows, Gathered{c.X, c.bidx + nd.bx}, nlo, nhi, r0, r1, lane, e);
+  }
+}
+
 template <bool FWD>
 __device__ __forceinline__ void run_merged(const Ctx& c, const int4 tk, const int lane) {
   const xdg_mf_node nd = c.nodes[tk.x];
   const int nrows = FWD ? nd.p + nd.b : nd.p;
   if (tk.z == kMR) {  // whole-warp rows: kMR rows share the vector loads
     const int r = tk.y;
-    const double* rows[kMR];
-    int r0[kMR], r1[kMR];
-    int lo = 1 << 30, hi = 0;
-#pragma unroll
-    for (int q = 0; q < kMR; ++q) {
-      const int rq = min(r + q, nrows - 1);
-      if (FWD) {
-        r0[q] = 0;
-        rows[q] = fwd_row(c, nd, rq, r1[q]);
-      } else {
-        rows[q] = c.F + nd.inv + (int64_t)rq * nd.ldp;
-        r0[q] = rq;
-        r1[q] = nd.p;
-      }
-      if (r + q >= nrows) r1[q] = r0[q];
-      if (r1[q] > r0[q]) {
-        lo = min(lo, r0[q]);
-        hi = max(hi, r1[q]);
-      }
-    }
     double d[kMR], e[kMR];
-#pragma unroll
-    for (int q = 0; q < kMR; ++q) d[q] = e[q] = 0.0;
-    if (hi > lo) multi_dot(rows, Direct{FWD ? c.W + nd.w : c.Y + nd.y}, lo, hi, r0, r1, lane, d);
-    if (!FWD && nd.b > 0) {
-#pragma unroll
-      for (int q = 0; q < kMR; ++q) {
-        const int rq = min(r + q, nrows - 1);
-        rows[q] = c.F + nd.upb + (int64_t)rq * nd.ldb;
-        r0[q] = 0;
-        r1[q] = (r + q < nrows) ? nd.b : 0;
-      }
-      multi_dot(rows, Gathered{c.X, c.bidx + nd.bx}, 0, nd.b, r0, r1, lane, e);
-    }
+    merged_rows<FWD>(c, nd, r, nrows, lane, 0, 1, d, e);
     if (lane == 0) {
 #pragma unroll
       for (int q = 0; q < kMR; ++q)
@@ -531,9 +565,60 @@ __device__ __forceinline__ void run_merged(const Ctx& c, const int4 tk, const in
   }
 }
 
+// Group task: kMR long rows shared by a group of kGW warps of the CTA, each
+// warp an equal contiguous share of the columns; the warps' partial sums are
+// added in warp order by the group's first lanes (deterministic).  Long rows
+// as warp tasks leave a launch with fewer tasks than resident warps and a
+// tail as long as its longest row (root front: 2 x 76 KB per task).
+#ifndef MF_GW
+#define MF_GW 4
+#endif
+constexpr int kGW = MF_GW;          // warps per group
+constexpr int kNG = kT / 32 / kGW;  // groups per CTA
+
+template <bool FWD>
+__device__ __forceinline__ void run_merged_group(const Ctx& c, const int4 tk, int grp,
+                                                 double (*part)[2 * kMR]) {
+  const int lane = threadIdx.x & 31, gw = (threadIdx.x >> 5) % kGW;
+  const xdg_mf_node nd = c.nodes[tk.x];
+  const int nrows = FWD ? nd.p + nd.b : nd.p;
+  const int r = tk.y;
+  double d[kMR], e[kMR];
+  merged_rows<FWD>(c, nd, r, nrows, lane, gw, kGW, d, e);
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < kMR; ++q) {
+      part[gw][q] = d[q];
+      part[gw][kMR + q] = e[q];
+    }
+  }
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(32 * kGW) : "memory");
+  if (gw == 0 && lane < kMR && r + lane < nrows) {
+    double ds = 0.0, es = 0.0;
+#pragma unroll
+    for (int w = 0; w < kGW; ++w) {
+      ds += part[w][lane];
+      es += part[w][kMR + lane];
+    }
+    if (FWD)
+      fwd_done(c, nd, r + lane, ds);
+    else
+      bwd_done(c, nd, r + lane, ds, es);
+  }
+}
+
 template <bool FWD>
 __global__ void __launch_bounds__(kT, MF_MINB)
-mf_merged_kernel(int64_t t0, int64_t ntasks, const int4* __restrict__ tasks, Ctx c) {
+mf_merged_kernel(int64_t t0, int64_t ntasks, int64_t c0, int64_t nctasks,
+                 const int4* __restrict__ tasks, Ctx c) {
+  __shared__ double part[2][kNG][kGW][2 * kMR];
+  {
+    const int grp = (threadIdx.x >> 5) / kGW;
+    int par = 0;  // alternating buffers: one group barrier per task
+    for (int64_t ct = (int64_t)blockIdx.x * kNG + grp; ct < nctasks;
+         ct += (int64_t)gridDim.x * kNG, par ^= 1)
+      run_merged_group<FWD>(c, tasks[c0 + interleave(ct, nctasks)], grp, part[par][grp]);
+  }
   const int lane = threadIdx.x & 31;
   const int64_t nw = (int64_t)gridDim.x * (kT / 32);
   for (int64_t w = (int64_t)blockIdx.x * (kT / 32) + (threadIdx.x >> 5); w < ntasks;
@@ -543,12 +628,16 @@ mf_merged_kernel(int64_t t0, int64_t ntasks, const int4* __restrict__ tasks, Ctx
 
 template <bool FWD>
 int launch_merged(const xdg_mf* mf, int h, double* x, cudaStream_t s) {
+  // warp tasks: lev_task[0] / [2]; CTA tasks (long rows): lev_task[1] / [3]
   const int64_t* lev = mf->lev_task + (int64_t)(FWD ? 0 : 2) * (mf->nlevels + 1);
+  const int64_t* levc = lev + (mf->nlevels + 1);
   const int64_t t0 = lev[h], nt = lev[h + 1] - t0;
-  if (nt <= 0) return XDG_OK;
+  const int64_t c0 = levc[h], nc = levc[h + 1] - c0;
+  if (nt <= 0 && nc <= 0) return XDG_OK;
   Ctx c{mf->nodes, mf->F, mf->bidx, mf->pdst, mf->pscale, mf->W, mf->Y, mf->C, x, mf->X};
-  const int g = resident_grid(mf_merged_kernel<FWD>, kT, 0, nt * 32);
-  mf_merged_kernel<FWD><<<g, kT, 0, s>>>(t0, nt, reinterpret_cast<const int4*>(mf->tasks), c);
+  const int g = resident_grid(mf_merged_kernel<FWD>, kT, 0, (nt + nc * kGW) * 32);
+  mf_merged_kernel<FWD><<<g, kT, 0, s>>>(t0, nt, c0, nc,
+                                         reinterpret_cast<const int4*>(mf->tasks), c);
   XDG_CHECK_LAUNCH();
   return XDG_OK;
 }
@@ -741,72 +830,47 @@ extern "C" int xdg_mf_extend_add(int64_t npairs, const int64_t* pair, const int6
 // the K range cut to its nonzero part.
 namespace xdg {
 namespace {
-constexpr int kMT = 64, kMK = 16;
-
-template <bool LOWER>  // true: M = L_BP L^-1;  false: N = U^-1 U_PB
-__global__ void __launch_bounds__(256)
+template <bool LOWER, int BT>  // true: M = L_BP L^-1;  false: N = U^-1 U_PB
+__global__ void __launch_bounds__(256, BT >= 128 ? 1 : 2)
 mf_merge_kernel(int P, int B, const double* __restrict__ Fb, double* __restrict__ out) {
-  __shared__ double As[kMK][kMT + 1], Bs[kMK][kMT + 1];
+  __shared__ DmmaSmem<BT, BT> sm;
   const int n = P + B;
   const double* F = Fb + (int64_t)blockIdx.z * n * n;
   const int rows = LOWER ? B : P, cols = LOWER ? P : B;
   double* O = out + (int64_t)blockIdx.z * rows * cols;
-  const int i0 = blockIdx.y * kMT, j0 = blockIdx.x * kMT;
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  double acc[4][4];
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  const int i0 = blockIdx.y * BT, j0 = blockIdx.x * BT;
   // nonzero K range: L^-1[k, j] = 0 for k < j;  U^-1[i, k] = 0 for k < i
-  const int kbeg = ((LOWER ? j0 : i0) / kMK) * kMK;
-  for (int k0 = kbeg; k0 < P; k0 += kMK) {
-    // stage A (rows i0.., k chunk) and B (k chunk, cols j0..)
-    for (int e = threadIdx.x; e < kMK * kMT; e += 256) {
-      const int kk = e % kMK, ii = e / kMK;  // A: consecutive threads along k
-      const int i = i0 + ii, k = k0 + kk;
-      double v = 0.0;
-      if (i < rows && k < P) {
-        if (LOWER)
-          v = F[(int64_t)(P + i) * n + k];
-        else
-          v = (k >= i) ? F[(int64_t)i * n + k] : 0.0;
-      }
-      As[kk][ii] = v;
-      const int jj = e % kMT, kb = e / kMT;  // B: consecutive threads along j
-      const int j = j0 + jj, k2 = k0 + kb;
-      double w = 0.0;
-      if (j < cols && k2 < P) {
-        if (LOWER)
-          w = (k2 > j) ? F[(int64_t)k2 * n + j] : (k2 == j ? 1.0 : 0.0);
-        else
-          w = F[(int64_t)k2 * n + P + j];
-      }
-      Bs[kb][jj] = w;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int kk = 0; kk < kMK; ++kk) {
-      double a[4], b[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        a[q] = As[kk][ty + 16 * q];
-        b[q] = Bs[kk][tx + 16 * q];
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-#pragma unroll
-        for (int r = 0; r < 4; ++r) acc[q][r] = fma(a[q], b[r], acc[q][r]);
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int q = 0; q < 4; ++q)
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int i = i0 + ty + 16 * q, j = j0 + tx + 16 * r;
-      if (i < rows && j < cols) O[(int64_t)i * cols + j] = acc[q][r];
-    }
+  const int kbeg = ((LOWER ? j0 : i0) / kDK) * kDK;
+  tile_dmma<BT, BT>(
+      P - kbeg,
+      [&](int ii, int kk) {
+        const int i = i0 + ii, k = kbeg + kk;
+        if (i >= rows || k >= P) return 0.0;
+        if (LOWER) return F[(int64_t)(P + i) * n + k];
+        return (k >= i) ? F[(int64_t)i * n + k] : 0.0;
+      },
+      [&](int kk, int jj) {
+        const int k = kbeg + kk, j = j0 + jj;
+        if (j >= cols || k >= P) return 0.0;
+        if (LOWER) return (k > j) ? F[(int64_t)k * n + j] : (k == j ? 1.0 : 0.0);
+        return F[(int64_t)k * n + P + j];
+      },
+      [&](int ii, int jj, double v) {
+        const int i = i0 + ii, j = j0 + jj;
+        if (i < rows && j < cols) O[(int64_t)i * cols + j] = v;
+      },
+      sm);
+}
+
+template <int BT>
+int launch_merge(int64_t nb, int P, int B, const double* fronts, double* out_m, double* out_n,
+                 cudaStream_t s) {
+  const unsigned tp = (unsigned)((P + BT - 1) / BT), tb = (unsigned)((B + BT - 1) / BT);
+  mf_merge_kernel<true, BT><<<dim3(tp, tb, (unsigned)nb), 256, 0, s>>>(P, B, fronts, out_m);
+  XDG_CHECK_LAUNCH();
+  mf_merge_kernel<false, BT><<<dim3(tb, tp, (unsigned)nb), 256, 0, s>>>(P, B, fronts, out_n);
+  XDG_CHECK_LAUNCH();
+  return XDG_OK;
 }
 }  // namespace
 }  // namespace xdg
@@ -817,10 +881,6 @@ extern "C" int xdg_mf_merge(int64_t nb, int P, int B, const double* fronts, doub
   if (nb <= 0 || P <= 0 || B <= 0) return XDG_OK;
   XDG_REQUIRE(nb <= 65535, XDG_ERR_ARG, "xdg_mf_merge: at most 65535 fronts per call");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const unsigned tp = (unsigned)((P + kMT - 1) / kMT), tb = (unsigned)((B + kMT - 1) / kMT);
-  mf_merge_kernel<true><<<dim3(tp, tb, (unsigned)nb), 256, 0, s>>>(P, B, fronts, out_m);
-  XDG_CHECK_LAUNCH();
-  mf_merge_kernel<false><<<dim3(tb, tp, (unsigned)nb), 256, 0, s>>>(P, B, fronts, out_n);
-  XDG_CHECK_LAUNCH();
-  return XDG_OK;
+  if (std::max(P, B) > 256) return launch_merge<128>(nb, P, B, fronts, out_m, out_n, s);
+  return launch_merge<64>(nb, P, B, fronts, out_m, out_n, s);
 }

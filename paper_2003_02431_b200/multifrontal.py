@@ -95,6 +95,15 @@ def _merge_mode() -> bool:
     return v == "1" and _fuse_mode()[0] == "off"
 
 
+def _long_row() -> int:
+    """Merged phases: rows of at least this many elements are CTA tasks (the
+    CTA's warps share the row's chunks).  XDG_MF_LONG, default 2048 = one
+    chunk of 32 lanes x 8 loads for each of the 8 warps."""
+    import os
+
+    return max(1, int(os.environ.get("XDG_MF_LONG", "2048")))
+
+
 def _rows_per_warp() -> int:
     """Rows a warp task of a whole-warp front covers: the kernel's kMR."""
     return int(nat.load().xdg_mf_rows_per_warp())
@@ -789,13 +798,44 @@ class Multifrontal:
             per task; shorter rows 32/G rows per task (rows field 0)."""
             g = gb if phase == 2 else gp
             nrows = bn if phase == 1 else pn
-            if merged:  # phase 0: forward rows 0..p+b-1; phase 2: backward rows
-                nrows = pn + bn if phase == 0 else pn
+            if merged:
+                g = gb if phase in (2, 3) else gp
+            if merged:  # phases 0, 1: forward rows 0..p+b-1; 2, 3: backward rows
+                nrows = pn + bn if phase in (0, 1) else pn
             out, lev = [], []
             for h in range(H):
                 ts = order[(height[order] == h) & cls[order]]
-                if merged and phase in (1, 3):
-                    lev.append(0)
+                if merged:
+                    # whole-warp fronts: MR rows per task; rows of >= LONG
+                    # elements are CTA tasks (slots 1 / 3), the others warp
+                    # tasks (slots 0 / 2), which also hold the short fronts
+                    lg = ts[g[ts] == 32]
+                    cnt2 = (nrows[lg] + MR - 1) // MR
+                    r2 = _ranges(np.zeros(len(lg), np.int64), cnt2) * MR
+                    node2 = np.repeat(lg, cnt2)
+                    if phase in (0, 1):  # longest row of the task: r + MR - 1 or p
+                        ln = np.minimum(r2 + MR - 1, pn[node2])
+                    else:
+                        ln = pn[node2] - r2 + bn[node2]
+                    # group tasks only where the warp tasks would not fill
+                    # the GPU a few times over (a barrier per task costs ~10 %)
+                    if len(r2) >= WAVES * RESIDENT_WARPS:
+                        ln = np.zeros_like(ln)
+                    pick = (ln >= LONG) if phase in (1, 3) else (ln < LONG)
+                    long_ = np.stack([node2[pick], r2[pick], np.full(int(pick.sum()), MR),
+                                      np.full(int(pick.sum()), -1)], 1)
+                    if phase in (1, 3):
+                        out.append(long_)
+                        lev.append(len(long_))
+                        continue
+                    sh = ts[g[ts] < 32]
+                    per = (32 // g[sh]) * 2
+                    cnt = (nrows[sh] + per - 1) // per
+                    first = _ranges(np.zeros(len(sh), np.int64), cnt) * np.repeat(per, cnt)
+                    grp = np.stack([np.repeat(sh, cnt), first, np.full_like(first, -2),
+                                    np.full_like(first, -1)], 1)
+                    out += [grp, long_]
+                    lev.append(len(grp) + len(long_))
                     continue
                 sh = ts[g[ts] < 32]
                 # bound / upb rows all span the same columns: two row sets
@@ -818,6 +858,10 @@ class Multifrontal:
 
         MR = _rows_per_warp()
         SETS = _row_sets()
+        LONG = _long_row()
+        import os as _os
+        WAVES = float(_os.environ.get("XDG_MF_CTA_WAVES", "2.0"))
+        RESIDENT_WARPS = 148 * 24  # B200: 148 SMs x 3 CTAs x 8 warps (80 registers)
         all_tasks, lev_task_k = [], []
         base = 0
         for cls in classes:

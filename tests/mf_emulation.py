@@ -63,7 +63,10 @@ def emulate_solve(mf, b, xlen):
             nd = nodes[t]
             # MR rows, or 32/G rows of G lanes (two such sets: nr == -2)
             n = nr if nr > 0 else (32 // nd[g]) * (2 if nr == -2 else 1)
-            last = nd["p"] + nd["b"] if (merged and phase == 0) else nd[count]
+            last = nd["p"] + nd["b"] if (merged and phase in (0, 1)) else nd[count]
+            if merged:
+                g = "gb" if phase in (2, 3) else "gp"
+                n = nr if nr > 0 else (32 // nd[g]) * 2
             out += [(t, r) for r in range(r0, min(r0 + n, last))]
         return out
 
@@ -76,7 +79,7 @@ def emulate_solve(mf, b, xlen):
                 v += Cb[cidx[k]]
             W[ent_w[e]] = v
         if merged:  # one phase: Y = L^-1 W_P and C = W_B - (L_BP L^-1) W_P
-            for t, r in rows(0, h):
+            for t, r in rows(0, h) + rows(1, h):  # warp tasks + CTA tasks
                 nd = nodes[t]
                 p = nd["p"]
                 wp = W[nd["w"]:nd["w"] + p]
@@ -98,7 +101,7 @@ def emulate_solve(mf, b, xlen):
     X = np.zeros(mf.Y.numel())
     for h in range(mf.nlevels - 1, -1, -1):  # backward: U_PB x_B, U^-1
         if merged:  # one phase: X_P = U^-1 Y - (U^-1 U_PB) X_B
-            for t, i in rows(2, h):
+            for t, i in rows(2, h) + rows(3, h):
                 nd = nodes[t]
                 p = nd["p"]
                 row = F[nd["inv"] + i * nd["ldp"]:][:p]

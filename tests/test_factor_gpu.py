@@ -71,7 +71,43 @@ def test_partial_front_schur_complement():
     triangular inverses of the pivot block."""
     ctx = Context.get()
     rng = np.random.default_rng(5)
-    shapes = [(10, 0), (10, 7), (40, 30), (64, 64), (100, 37), (150, 200)]
+    _check_partial_fronts([(10, 0), (10, 7), (40, 30), (64, 64), (100, 37), (150, 200)], 5)
+
+
+@pytest.mark.parametrize("shape", [(96, 400), (300, 500), (200, 1500), (1280, 900), (416, 130)])
+def test_partial_front_two_level_blocking(shape):
+    """Fronts large enough for the super-panels (deferred trailing update,
+    U12 block row by block row) and the 128 x 128 DMMA tiles."""
+    _check_partial_fronts([shape], 11)
+
+
+def test_mf_merge_products():
+    """xdg_mf_merge: M = L_BP L^-1 and N = U^-1 U_PB of factored fronts
+    against dense products (both tile sizes)."""
+    import ctypes as C
+
+    from paper_2003_02431_b200 import _native as nat
+
+    ctx = Context.get()
+    g = torch.Generator(device="cuda").manual_seed(7)
+    for nb, P, B in [(3, 20, 50), (2, 96, 300), (2, 320, 130), (1, 700, 900)]:
+        n = P + B
+        Fb = torch.randn(nb, n, n, generator=g, dtype=torch.float64, device="cuda")
+        M = torch.zeros(nb, B, P, dtype=torch.float64, device="cuda")
+        N = torch.zeros(nb, P, B, dtype=torch.float64, device="cuda")
+        nat.check(ctx.lib.xdg_mf_merge(nb, P, B, Fb.data_ptr(), M.data_ptr(), N.data_ptr(),
+                                       ctx.stream), "mf_merge")
+        INV = Fb[:, :P, :P]
+        Li = torch.tril(INV, -1) + torch.eye(P, dtype=torch.float64, device="cuda")
+        Mr = Fb[:, P:, :P] @ Li
+        Nr = torch.triu(INV) @ Fb[:, :P, P:]
+        assert float((M - Mr).abs().max() / Mr.abs().max()) <= 1e-13, (nb, P, B)
+        assert float((N - Nr).abs().max() / Nr.abs().max()) <= 1e-13, (nb, P, B)
+
+
+def _check_partial_fronts(shapes, seed):
+    ctx = Context.get()
+    rng = np.random.default_rng(seed)
     for invert in (False, True):
         mats = [rng.standard_normal((P + B, P + B)) for P, B in shapes]
         flat, off = _pack(mats)

@@ -74,11 +74,21 @@ for mode, mg in sweep:
         e.synchronize()
         ts.append(s.elapsed_time(e))
     ms = statistics.median(ts)
+    # residual of the solve against the level operator's low-order part
+    # (torch ops: checker only)
+    rpt = torch.from_numpy(np.asarray(rp)).to(ctx.device).long()
+    rows_ = torch.repeat_interleave(torch.arange(nb, device=ctx.device), rpt[1:] - rpt[:-1])
+    colt = torch.from_numpy(np.asarray(col)).to(ctx.device).long()
+    blo = D.val_t.view(-1, N, N)[:, :m, :m].transpose(1, 2)
+    ax = torch.zeros(nb, m, dtype=torch.float64, device=ctx.device)
+    ax.index_add_(0, rows_, torch.bmm(blo, x.view(nb, m)[colt].unsqueeze(2)).squeeze(2))
+    blo_ = b.view(nb, N)[:, :m]
+    resid = float((ax - blo_).norm() / blo_.norm())
     if ref is None:
         ref = x.clone()
     # backward error of the solve against the level operator's low-order part
     print(json.dumps({"lib": os.environ.get("XDG_LIB", "default"), "fuse": mode,
-                      "merged": bool(mf.merged), "m": m,
+                      "merged": bool(mf.merged), "m": m, "rel_residual": resid,
                       "rel_diff_vs_first": float((x - ref).norm() / ref.norm()),
                       "level": lam, "unknowns": nb * m, "nodes": mf.nnodes,
                       "levels": mf.nlevels, "factor_GB": mf.factor_bytes / 1e9,
