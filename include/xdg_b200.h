@@ -272,7 +272,9 @@ int xdg_assemble_blocks(int nout, int N, const int* tptr, const int* tid,
  * (p x b, ld ldb). */
 typedef struct xdg_mf_node {
   int32_t p, b, ldp, ldb;      /* pivot / boundary unknowns, leading dims */
-  int32_t gp, gb, pad0, pad1;  /* lanes per row for p- / b-long rows (2^k) */
+  int32_t gp, gb, ldr, pad1;   /* lanes per row for p- / b-long rows (2^k);
+                                  ldr > 0: lbp holds the column-major forward
+                                  copy FT[k][r] of [L^-1; M_BP], ld = ldr   */
   int64_t inv, lbp, upb;       /* offsets into F */
   int64_t w, y, c;             /* offsets into W (p+b), Y (p), C (b) */
   int64_t bx, px;              /* offsets into bidx (b), pdst (p) */
@@ -312,9 +314,12 @@ typedef struct xdg_mf {
   const int32_t* ftask;        /* int4 warp tasks, stage by stage            */
   /* Merged phases: the factors hold M_BP = L_BP L^-1 (at lbp) and N_PB =
    * U^-1 U_PB (at upb), see xdg_mf_merge; one row launch per height and
-   * sweep: task ranges lev_task[0] (forward rows 0..p+b-1 of every front)
-   * and lev_task[2] (backward rows 0..p-1); X[p] = equilibrated solution
-   * (bidx indexes X).  Excludes the fused low levels.                     */
+   * sweep: lev_task then has 6 ranges per level -- [0] forward warp tasks
+   * (rows 0..p+b-1 of every front), [1] forward group tasks (long rows),
+   * [2] / [3] the same for the backward rows 0..p-1, [4] forward
+   * thread-per-row tasks of the fronts with a column-major copy (ldr > 0),
+   * [5] reserved; X[p] = equilibrated solution (bidx indexes X).
+   * Excludes the fused low levels.                                        */
   double* X;
   int32_t merged, pad_;
 } xdg_mf;

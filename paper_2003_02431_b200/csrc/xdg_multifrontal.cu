@@ -166,6 +166,14 @@ __device__ __forceinline__ void multi_dot(const double* const* rows, V v, int lo
   for (int q = 0; q < kMR; ++q) d[q] = warp_sum(acc[q][0] + acc[q][1]);
 }
 
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
 // Vector accessors.  idx(j) / at(i) split an element access in two so the
 // loops can issue every index load of a chunk, then the factor loads, then
 // the (dependent) vector loads: a gathered element costs one extra round
@@ -516,8 +524,8 @@ __device__ __forceinline__ void merged_rows(const Ctx& c, const xdg_mf_node& nd,
 }
 
 template <bool FWD>
-__device__ __forceinline__ void run_merged(const Ctx& c, const int4 tk, const int lane) {
-  const xdg_mf_node nd = c.nodes[tk.x];
+__device__ __forceinline__ void run_merged(const Ctx& c, const int4 tk, const xdg_mf_node& nd,
+                                           const int lane) {
   const int nrows = FWD ? nd.p + nd.b : nd.p;
   if (tk.z == kMR) {  // whole-warp rows: kMR rows share the vector loads
     const int r = tk.y;
@@ -619,11 +627,43 @@ mf_merged_kernel(int64_t t0, int64_t ntasks, int64_t c0, int64_t nctasks,
          ct += (int64_t)gridDim.x * kNG, par ^= 1)
       run_merged_group<FWD>(c, tasks[c0 + interleave(ct, nctasks)], grp, part[par][grp]);
   }
-  const int lane = threadIdx.x & 31;
+  // Warp tasks, software-pipelined through shared memory: while task k runs,
+  // the node of task k + 1 and the descriptor of task k + 2 are in flight
+  // (cp.async), so a task's chain of dependent loads is its factor rows only
+  // -- not descriptor -> node -> rows.  The low levels (thousands of fronts
+  // of 10-300 pivots, a few KB per task) are bound by exactly that chain.
+  __shared__ __align__(16) int4 tks[kT / 32][2];
+  __shared__ __align__(16) xdg_mf_node nds[kT / 32][2];
+  static_assert(sizeof(xdg_mf_node) == 96, "node copies are 6 x 16 bytes");
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
   const int64_t nw = (int64_t)gridDim.x * (kT / 32);
-  for (int64_t w = (int64_t)blockIdx.x * (kT / 32) + (threadIdx.x >> 5); w < ntasks;
-       w += nw)
-    run_merged<FWD>(c, tasks[t0 + interleave(w, ntasks)], lane);
+  const int64_t w0 = (int64_t)blockIdx.x * (kT / 32) + wp;
+  if (w0 >= ntasks) return;
+  auto fetch_task = [&](int64_t w, int slot) {  // lane 6: 16-byte descriptor
+    if (lane == 6) cp_async16(&tks[wp][slot], tasks + t0 + interleave(w, ntasks));
+  };
+  auto fetch_node = [&](int node, int slot) {  // lanes 0-5: 96-byte node
+    if (lane < 6)
+      cp_async16(reinterpret_cast<char*>(&nds[wp][slot]) + 16 * lane,
+                 reinterpret_cast<const char*>(c.nodes + node) + 16 * lane);
+  };
+  fetch_task(w0, 0);
+  cp_async_wait_all();
+  __syncwarp();
+  fetch_node(tks[wp][0].x, 0);
+  if (w0 + nw < ntasks) fetch_task(w0 + nw, 1);
+  int k = 0;
+  for (int64_t w = w0; w < ntasks; w += nw, k ^= 1) {
+    cp_async_wait_all();
+    __syncwarp();  // nds[k] and tks[k ^ 1] have landed
+    const int4 tk = tks[wp][k];
+    const bool more = w + nw < ntasks;
+    const int next_node = more ? tks[wp][k ^ 1].x : 0;
+    __syncwarp();  // every lane has read tks[k] before it is refilled
+    if (more) fetch_node(next_node, k ^ 1);
+    if (w + 2 * nw < ntasks) fetch_task(w + 2 * nw, k);
+    run_merged<FWD>(c, tk, nds[wp][k], lane);
+  }
 }
 
 template <bool FWD>
@@ -638,6 +678,67 @@ int launch_merged(const xdg_mf* mf, int h, double* x, cudaStream_t s) {
   const int g = resident_grid(mf_merged_kernel<FWD>, kT, 0, (nt + nc * kGW) * 32);
   mf_merged_kernel<FWD><<<g, kT, 0, s>>>(t0, nt, c0, nc,
                                          reinterpret_cast<const int4*>(mf->tasks), c);
+  XDG_CHECK_LAUNCH();
+  return XDG_OK;
+}
+
+// Forward rows of the fronts with a column-major copy FT[k][r] of
+// [L^-1 (strictly lower); M_BP] (nd.ldr > 0): one THREAD per row, a warp
+// task = 32 consecutive rows.  Loads are coalesced across the rows, the
+// vector entry W[k] is the same for every lane (one broadcast load), no
+// reductions, no per-entry masks: ~0.15 instructions per matrix entry
+// instead of ~2 for the lane groups on fronts of 10-300 pivots, and few
+// enough registers for twice the resident warps.
+#ifndef MF_CU
+#define MF_CU 8  // columns (independent loads) in flight per thread
+#endif
+__global__ void __launch_bounds__(kT, 6)
+mf_fwd_cols_kernel(int64_t t0, int64_t ntasks, const int4* __restrict__ tasks, Ctx c) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (kT / 32);
+  for (int64_t w = (int64_t)blockIdx.x * (kT / 32) + (threadIdx.x >> 5); w < ntasks; w += nw) {
+    const int4 tk = tasks[t0 + interleave(w, ntasks)];
+    const xdg_mf_node nd = c.nodes[tk.x];
+    const int p = nd.p, R = nd.p + nd.b;
+    const int r = tk.y + lane;
+    const bool act = r < R;
+    // storage row: boundary rows sit after the padded pivot rows
+    const int rs = act ? (r < p ? r : r + (nd.ldp - p)) : 0;
+    // a block of pivot rows only needs the columns left of its last row
+    const int kend = (tk.y + 32 <= p) ? tk.y + 31 : p;
+    const double* ft = c.F + nd.lbp + rs;
+    const double* wv = c.W + nd.w;
+    const double wr = act ? wv[r] : 0.0;
+    double acc[2] = {0.0, 0.0};
+    for (int k0 = 0; k0 < kend; k0 += MF_CU) {
+      double a[MF_CU], x[MF_CU];
+#pragma unroll
+      for (int u = 0; u < MF_CU; ++u) {
+        const int k = min(k0 + u, kend - 1);
+        a[u] = __ldg(ft + (int64_t)k * nd.ldr);
+        x[u] = wv[k];
+      }
+#pragma unroll
+      for (int u = 0; u < MF_CU; ++u)
+        acc[u & 1] = fma(a[u], (k0 + u < kend) ? x[u] : 0.0, acc[u & 1]);
+    }
+    const double d = acc[0] + acc[1];
+    if (act) {
+      if (r < p)
+        c.Y[nd.y + r] = __dadd_rn(wr, d);
+      else
+        c.C[nd.c + (r - p)] = __dsub_rn(wr, d);
+    }
+  }
+}
+
+int launch_fwd_cols(const xdg_mf* mf, int h, double* x, cudaStream_t s) {
+  const int64_t* lev = mf->lev_task + (int64_t)4 * (mf->nlevels + 1);
+  const int64_t t0 = lev[h], nt = lev[h + 1] - t0;
+  if (nt <= 0) return XDG_OK;
+  Ctx c{mf->nodes, mf->F, mf->bidx, mf->pdst, mf->pscale, mf->W, mf->Y, mf->C, x, mf->X};
+  const int g = resident_grid(mf_fwd_cols_kernel, kT, 0, nt * 32);
+  mf_fwd_cols_kernel<<<g, kT, 0, s>>>(t0, nt, reinterpret_cast<const int4*>(mf->tasks), c);
   XDG_CHECK_LAUNCH();
   return XDG_OK;
 }
@@ -744,6 +845,7 @@ extern "C" int xdg_mf_solve_phase(const xdg_mf* mf, const double* b, double* x, 
         XDG_CHECK_LAUNCH();
       }
       if (mf->merged) {
+        XDG_TRY(launch_fwd_cols(mf, h, x, s));
         XDG_TRY(launch_merged<true>(mf, h, x, s));
         continue;
       }

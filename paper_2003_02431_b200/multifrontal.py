@@ -48,7 +48,7 @@ I32 = torch.int32
 I64 = torch.int64
 
 NODE_DT = np.dtype([("p", "<i4"), ("b", "<i4"), ("ldp", "<i4"), ("ldb", "<i4"),
-                    ("gp", "<i4"), ("gb", "<i4"), ("pad0", "<i4"), ("pad1", "<i4"),
+                    ("gp", "<i4"), ("gb", "<i4"), ("ldr", "<i4"), ("pad1", "<i4"),
                     ("inv", "<i8"), ("lbp", "<i8"), ("upb", "<i8"), ("w", "<i8"),
                     ("y", "<i8"), ("c", "<i8"), ("bx", "<i8"), ("px", "<i8")])
 assert NODE_DT.itemsize == 96
@@ -102,6 +102,20 @@ def _long_row() -> int:
     import os
 
     return max(1, int(os.environ.get("XDG_MF_LONG", "2048")))
+
+
+def _col_pivots() -> int:
+    """Merged phases: fronts with at most this many (padded) pivot unknowns
+    run their forward rows one THREAD per row over a column-major copy of
+    [L^-1; M_BP] (coalesced across rows, no reductions or masks: the row-major
+    lane groups spend ~2 instructions per matrix entry on fronts of 10-300
+    pivots).  XDG_MF_PCOL; 0 (default) disables: measured SLOWER on the cfg2
+    low-order system (PCOL 0 / 128 / 320 / 640 -> 2.54 / 2.72 / 2.96 / 3.23 ms,
+    profiles/r2_mf_pcol_sweep.jsonl) -- the low levels are bound by the
+    dependent loads per task, not by the lane mapping."""
+    import os
+
+    return max(0, int(os.environ.get("XDG_MF_PCOL", "0")))
 
 
 def _rows_per_warp() -> int:
@@ -506,10 +520,21 @@ class Multifrontal:
         lbp_off = np.zeros(nn, np.int64)
         upb_off = np.zeros(nn, np.int64)
         fst = 0
+        PCOL = _col_pivots() if merged else 0
+        colf = np.zeros(nn, bool)      # forward rows thread-per-row (column-major copy)
+        ldr = np.zeros(nn, np.int64)   # its leading dimension (rows, padded to 4)
         for (h, P_, B_), ts in list(buckets.items()) + list(buckets_sh.items()):
             nb = len(ts)
             inv_off[ts] = fst + np.arange(nb) * P_ * P_
             fst += nb * P_ * P_
+            if 0 < P_ <= PCOL:
+                colf[ts] = True
+                ldr[ts] = (P_ + B_ + 3) // 4 * 4
+                lbp_off[ts] = fst + np.arange(nb) * P_ * ldr[ts[0]]
+                fst += nb * P_ * int(ldr[ts[0]])
+                upb_off[ts] = fst + np.arange(nb) * P_ * B_
+                fst += nb * P_ * B_
+                continue
             lbp_off[ts] = fst + np.arange(nb) * B_ * P_
             fst += nb * B_ * P_
             upb_off[ts] = fst + np.arange(nb) * P_ * B_
@@ -662,11 +687,13 @@ class Multifrontal:
                             perm_off=np.arange(nb, dtype=np.int64) * P_)
                         perm = perm[:nb * P_].view(nb, P_)
                         bad = info[:nb] != 0
+                    is_col = bool(colf[ts[0]])
                     if B_:
                         LBP = Fb[:, P_:, :P_]
                         bad |= ~torch.isfinite(LBP).flatten(1).all(1)
                         o, o2 = int(lbp_off[ts[0]]), int(upb_off[ts[0]])
-                        out_m = self.F[o:o + nb * B_ * P_].view(nb, B_, P_)
+                        out_m = (torch.empty(nb, B_, P_, dtype=F64, device=dev) if is_col
+                                 else self.F[o:o + nb * B_ * P_].view(nb, B_, P_))
                         out_n = self.F[o2:o2 + nb * P_ * B_].view(nb, P_, B_)
                         if not merged:
                             out_m.copy_(LBP)
@@ -685,6 +712,12 @@ class Multifrontal:
                                     ctx.stream), "mf_merge")
                     o = int(inv_off[ts[0]])
                     self.F[o:o + nb * P_ * P_].view(nb, P_, P_).copy_(Fb[:, :P_, :P_])
+                    if is_col:  # FT[k][r] = [strict-lower L^-1; M_BP][r][k]
+                        ld_ = int(ldr[ts[0]])
+                        ft = self.F[int(lbp_off[ts[0]]):][:nb * P_ * ld_].view(nb, P_, ld_)
+                        ft[:, :, :P_].copy_(torch.tril(Fb[:, :P_, :P_], -1).transpose(1, 2))
+                        if B_:
+                            ft[:, :, P_:P_ + B_].copy_(out_m.transpose(1, 2))
                     bad_nodes.append((ts, bad))
                     dev_perms.append((ts, perm))  # read back once, after all heights
                     for q, t in enumerate(ts):  # Schur complements other ranks need
@@ -805,6 +838,20 @@ class Multifrontal:
             out, lev = [], []
             for h in range(H):
                 ts = order[(height[order] == h) & cls[order]]
+                if merged and phase == 4:  # one thread per forward row
+                    cf = ts[colf[ts]]
+                    cnt = (pn[cf] + bn[cf] + 31) // 32
+                    first = _ranges(np.zeros(len(cf), np.int64), cnt) * 32
+                    ct_ = np.stack([np.repeat(cf, cnt), first, np.full_like(first, -3),
+                                    np.full_like(first, -1)], 1)
+                    out.append(ct_)
+                    lev.append(len(ct_))
+                    continue
+                if merged and phase == 5:
+                    lev.append(0)
+                    continue
+                if merged and phase in (0, 1):
+                    ts = ts[~colf[ts]]
                 if merged:
                     # whole-warp fronts: MR rows per task; rows of >= LONG
                     # elements are CTA tasks (slots 1 / 3), the others warp
@@ -866,7 +913,7 @@ class Multifrontal:
         base = 0
         for cls in classes:
             lev_task = []
-            for phase in range(4):
+            for phase in range(6 if merged else 4):
                 tl, lv = tasks(phase, cls)
                 all_tasks += tl
                 lev_task.append(base + np.concatenate([[0], np.cumsum(lv)]))
@@ -891,6 +938,7 @@ class Multifrontal:
         nodes = np.zeros(nn, NODE_DT)
         nodes["p"], nodes["b"], nodes["ldp"], nodes["ldb"] = pn, bn, pp, bp
         nodes["gp"], nodes["gb"] = gp, gb
+        nodes["ldr"] = ldr  # leading dimension of the column-major forward copy
         nodes["inv"], nodes["lbp"], nodes["upb"] = inv_off, lbp_off, upb_off
         nodes["w"], nodes["y"], nodes["c"] = w_off, y_off, c_off
         nodes["bx"], nodes["px"] = bx_off, px_off
@@ -921,6 +969,7 @@ class Multifrontal:
         if self.comm is not None:
             self._dist_plan(pn, bn, c_off, y_off, vdst, P_list, am, dev)
         self.pn, self.bn = pn, bn
+        self.colf = colf
         self._s = None
         self.times = {"symbolic": t1 - t0, "numeric": t2 - t1,
                       "plan": time.perf_counter() - t2}

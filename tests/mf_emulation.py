@@ -79,6 +79,20 @@ def emulate_solve(mf, b, xlen):
                 v += Cb[cidx[k]]
             W[ent_w[e]] = v
         if merged:  # one phase: Y = L^-1 W_P and C = W_B - (L_BP L^-1) W_P
+            lev4 = mf.lev_task[4 * (H + 1):5 * (H + 1)]
+            for t, r0, _, _ in tasks[lev4[h]:lev4[h + 1]]:  # thread-per-row tasks
+                nd = nodes[t]
+                p, R, ld_ = nd["p"], nd["p"] + nd["b"], nd["ldr"]
+                wp = W[nd["w"]:nd["w"] + p]
+                for r in range(r0, min(r0 + 32, R)):
+                    rs = r if r < p else r + (nd["ldp"] - p)
+                    kend = r0 + 31 if r0 + 32 <= p else p
+                    col = F[nd["lbp"] + rs:][:kend * ld_:ld_] if kend else np.zeros(0)
+                    d = col @ wp[:kend]
+                    if r < p:
+                        Y[nd["y"] + r] = W[nd["w"] + r] + d
+                    else:
+                        Cb[nd["c"] + r - p] = W[nd["w"] + r] - d
             for t, r in rows(0, h) + rows(1, h):  # warp tasks + CTA tasks
                 nd = nodes[t]
                 p = nd["p"]

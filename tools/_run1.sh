@@ -1,4 +1,6 @@
 cd $GRAFT_REPO_ROOT
-python -m pytest tests -m gpu -q --timeout 1500 -k "not cfg2 and not cfg5_10_p3 and not cfg5_10_p4 and not cfg5_10_p5 and not cfg4_16" > gpurun_out/r2_gpu_tests_s4b.txt 2>&1
-echo "pytest exit $?" >> gpurun_out/r2_gpu_tests_s4b.txt
-tail -n 25 gpurun_out/r2_gpu_tests_s4b.txt
+python -m pytest tests -m gpu -q --timeout 2400 -k "not cfg5_10_p5" > gpurun_out/r2_gpu_tests_s4c.txt 2>&1
+echo "pytest exit $?" >> gpurun_out/r2_gpu_tests_s4c.txt
+tail -n 25 gpurun_out/r2_gpu_tests_s4c.txt
+python bench.py --steps 10 --warmup 3 > gpurun_out/r2_bench_s4c.json 2> gpurun_out/r2_bench_s4c.err
+echo "bench exit $?"
