@@ -250,13 +250,17 @@ lu_trsm_kernel(double* __restrict__ A, const int64_t* __restrict__ off,
   if (c >= M.n) return;
   double x[64];
   double* col = M.a + (int64_t)k0 * M.ld + c;
-#pragma unroll 4
-  for (int i = 0; i < kb; ++i) {
-    double s = col[(int64_t)i * M.ld];
+  // the column's kb entries first (independent loads, all in flight), then
+  // the substitution, then the stores
+#pragma unroll 16
+  for (int i = 0; i < kb; ++i) x[i] = col[(int64_t)i * M.ld];
+  for (int i = 1; i < kb; ++i) {
+    double s = x[i];
     for (int t = 0; t < i; ++t) s = __fma_rn(-L[i * kb + t], x[t], s);
     x[i] = s;
-    col[(int64_t)i * M.ld] = s;
   }
+#pragma unroll 16
+  for (int i = 1; i < kb; ++i) col[(int64_t)i * M.ld] = x[i];
 }
 
 // A[r0:r1, c0:c1] -= A[r0:r1, q0:q1] A[q0:q1, c0:c1] inside every matrix of
@@ -407,12 +411,10 @@ trtri_solve_kernel(double* __restrict__ A, const int64_t* __restrict__ off,
   double x[64];
   if (z == 0) {  // back substitution, rows kb-1 .. 0
     const int rmax = j < i0 + kb ? j - i0 : kb - 1;  // X_ii upper: rows <= j - i0
-    for (int r = kb - 1; r >= 0; --r) {
-      if (r > rmax) {
-        x[r] = 0.0;
-        continue;
-      }
-      double v = R[(int64_t)r * P + j];
+#pragma unroll 16
+    for (int r = 0; r < kb; ++r) x[r] = (r <= rmax) ? R[(int64_t)r * P + j] : 0.0;
+    for (int r = rmax; r >= 0; --r) {
+      double v = x[r];
       for (int c = r + 1; c <= rmax; ++c) v = __fma_rn(-D[r * 65 + c], x[c], v);
       x[r] = v / D[r * 65 + r];
     }
@@ -421,12 +423,10 @@ trtri_solve_kernel(double* __restrict__ A, const int64_t* __restrict__ off,
     // X_ii unit lower: column j - i0 of it starts at its unit diagonal
     // (R = 1 there), which takes part in the substitution but is not stored
     const int rlo = j >= i0 ? j - i0 : 0;
-    for (int r = 0; r < kb; ++r) {
-      if (r < rlo) {
-        x[r] = 0.0;
-        continue;
-      }
-      double v = R[(int64_t)r * P + j];
+#pragma unroll 16
+    for (int r = 0; r < kb; ++r) x[r] = (r >= rlo) ? R[(int64_t)r * P + j] : 0.0;
+    for (int r = rlo + 1; r < kb; ++r) {
+      double v = x[r];
       for (int c = rlo; c < r; ++c) v = __fma_rn(-D[r * 65 + c], x[c], v);
       x[r] = v;
     }

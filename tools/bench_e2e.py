@@ -68,7 +68,17 @@ for c in chunk_list:
     ms = timed(lambda: (step(), hs.wait()))
     out[f"chunks{c}_ms"] = ms
     out[f"chunks{c}_GBs"] = B / ms / 1e6
-    # back-to-back products (the bench's e2e loop: one wait after K steps)
+    # host-synchronous products (BlockSparseMatrix.matvec on pinned vectors,
+    # the bench's e2e): the pipeline fills and drains inside every call
+    import time as _t
+
+    for _ in range(2):
+        hs(xh, yh, sync=True)
+    t0 = _t.perf_counter()
+    for _ in range(10):
+        hs(xh, yh, sync=True)
+    out[f"chunks{c}_sync_GBs"] = B / ((_t.perf_counter() - t0) / 10) / 1e9
+    # back-to-back products (one wait after K steps)
     for _ in range(2):
         step()
     hs.wait()

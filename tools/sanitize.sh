@@ -1,11 +1,15 @@
 #!/usr/bin/env bash
 # compute-sanitizer over tools/sanitize_solves.py; one log per tool under
-# ${1:-gpurun_out}/ (summaries copied to profiles/ by hand).
+# OUT (default gpurun_out/), summaries copied to profiles/ by hand.
+#   tools/sanitize.sh [OUT] [tool ...]      tools default: memcheck racecheck synccheck initcheck
 set -u
 OUT="${1:-gpurun_out}"
+shift || true
+TOOLS=("$@")
+[ ${#TOOLS[@]} -eq 0 ] && TOOLS=(memcheck racecheck synccheck initcheck)
 mkdir -p "$OUT"
 CS=/usr/local/cuda/bin/compute-sanitizer
-for tool in memcheck racecheck synccheck initcheck; do
+for tool in "${TOOLS[@]}"; do
   extra=""
   [ "$tool" = memcheck ] && extra="--leak-check full"
   timeout 1500 "$CS" --tool "$tool" $extra --error-exitcode 9 --print-limit 50 \
