@@ -238,10 +238,19 @@ def omg(h: Hierarchy, b, cfg, lam=1, entry=1):
     return x, it, hist
 
 
-def gmres(M, rp, col, val, b, cfg, dim):
-    """Restarted right-preconditioned GMRES with MGS (solvers.py:756-846)."""
+def gmres(M, rp, col, val, b, cfg, dim, timing=None):
+    """Restarted right-preconditioned GMRES with MGS (solvers.py:756-846).
+    timing (optional dict): receives "setup_s" (the lazy PMG factorization,
+    which the reference counts inside its solve timer, solvers.py:778) and
+    "iter_s" (seconds of every iteration) -- for the CPU-baseline tools."""
+    import time as _time
+
     N = val.shape[1]
+    _t0 = _time.perf_counter()
     F = PmgFactors(rp, col, val, np.arange(len(rp) - 1), modes_low(cfg["k_lo"], dim, N))
+    if timing is not None:
+        timing["setup_s"] = _time.perf_counter() - _t0
+        timing["iter_s"] = []
     m, tol, maxit = cfg["gmres_restart"], cfg["tolerance"], cfg["max_iterations"]
     x = np.zeros_like(b)
     r = b - M @ x
@@ -257,6 +266,7 @@ def gmres(M, rp, col, val, b, cfg, dim):
         j = 0
         while j < m and total < maxit:
             total += 1
+            _ti = _time.perf_counter()
             Z[:, j] = F.apply(V[:, j])
             w = M @ Z[:, j]
             for i in range(j + 1):
@@ -277,6 +287,8 @@ def gmres(M, rp, col, val, b, cfg, dim):
             H[j + 1, j] = 0.0
             est = abs(float(g[j + 1]))
             hist.append(est)
+            if timing is not None:
+                timing["iter_s"].append(_time.perf_counter() - _ti)
             j += 1
             if est <= tol:
                 break

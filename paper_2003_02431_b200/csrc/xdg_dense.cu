@@ -10,6 +10,8 @@
 // but with no sequential dependence chain -- every row is an independent,
 // coalesced dot product.  Bound: HBM.  The pivot is pre-composed with the
 // gather from the global vector: rhs_i = b[src_i].
+#include <stdlib.h>
+
 #include "xdg_common.cuh"
 
 namespace xdg {
@@ -239,6 +241,103 @@ inv_rows_smem_kernel(int64_t ntasks, const int* __restrict__ task_sys,
   }
 }
 
+// Ring variant: the factor rows stream through a per-warp ring of
+// shared-memory stages filled by cp.async (LDGSTS: no registers held by
+// loads in flight), kRingStages - 1 chunks of kRingChunk doubles ahead of
+// the FMAs.  A warp's rows of a task form one chunk stream, so the memory
+// pipeline does not drain between rows (the register version issues a row's
+// loads, reduces, then starts the next row).
+constexpr int kRingChunk = 512;  // doubles per stage (4 KB)
+constexpr int kRingStages = 4;
+
+__device__ __forceinline__ void cp_async8(double* smem_dst, const double* gmem_src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gmem_src) : "memory");
+}
+
+template <bool LOWER>
+__global__ void __launch_bounds__(256, 1)
+inv_rows_ring_kernel(int64_t ntasks, const int* __restrict__ task_sys,
+                     const int* __restrict__ task_row0, int rows_per_task, int sv_len,
+                     const int64_t* __restrict__ off, const int* __restrict__ dims,
+                     const int64_t* __restrict__ vec_off, const double* __restrict__ INV,
+                     const double* __restrict__ v, double* __restrict__ out) {
+  extern __shared__ double sm[];
+  double* sv = sm;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* ring = sm + sv_len + warp * (kRingStages * kRingChunk);
+  for (int64_t t = blockIdx.x; t < ntasks; t += gridDim.x) {
+    const int s = task_sys[t];
+    const int i0 = task_row0[t];
+    const int n = dims[s];
+    const int64_t base = vec_off[s];
+    __syncthreads();  // the previous task is done with sv
+    for (int j = threadIdx.x; j < n; j += 256) sv[j] = v[base + j];
+    __syncthreads();
+    const int i1 = min(i0 + rows_per_task, n);
+    const double* A = INV + off[s];
+    // prefetch cursor (pi, pj) and consume cursor (ci, cj) over this warp's
+    // rows i0 + warp, + 8, ...; row i spans columns [lo(i), hi(i))
+    auto lo = [&](int i) { return LOWER ? 0 : i; };
+    auto hi = [&](int i) { return LOWER ? i : n; };
+    int pi = i0 + warp, pj = pi < i1 ? lo(pi) : 0;
+    int ci = pi, cj = pj;
+    int pstage = 0, cstage = 0;
+    auto issue = [&]() {  // one chunk of the prefetch stream (or an empty group)
+      while (pi < i1 && pj >= hi(pi)) {  // next row (rows may be empty: L^-1 row 0)
+        pi += 8;
+        pj = pi < i1 ? lo(pi) : 0;
+      }
+      if (pi < i1) {
+        const int len = min(kRingChunk, hi(pi) - pj);
+        const double* src = A + (int64_t)pi * n + pj;
+        double* dst = ring + pstage * kRingChunk;
+        for (int e = lane; e < len; e += 32) cp_async8(dst + e, src + e);
+        pj += len;
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      pstage = (pstage + 1) % kRingStages;
+    };
+#pragma unroll
+    for (int q = 0; q < kRingStages - 1; ++q) issue();
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    while (ci < i1) {
+      if (cj >= hi(ci)) {  // row done (or empty)
+        const double d = warp_sum((a0 + a1) + (a2 + a3));
+        if (lane == 0) out[base + ci] = LOWER ? __dadd_rn(sv[ci], d) : d;
+        a0 = a1 = a2 = a3 = 0.0;
+        ci += 8;
+        cj = ci < i1 ? lo(ci) : 0;
+        continue;
+      }
+      issue();
+      asm volatile("cp.async.wait_group %0;" ::"n"(kRingStages - 1) : "memory");
+      __syncwarp();
+      const int len = min(kRingChunk, hi(ci) - cj);
+      const double* buf = ring + cstage * kRingChunk;
+#pragma unroll 4
+      for (int e = lane; e < len; e += 128) {
+        a0 = fma(buf[e], sv[cj + e], a0);
+        if (e + 32 < len) a1 = fma(buf[e + 32], sv[cj + e + 32], a1);
+        if (e + 64 < len) a2 = fma(buf[e + 64], sv[cj + e + 64], a2);
+        if (e + 96 < len) a3 = fma(buf[e + 96], sv[cj + e + 96], a3);
+      }
+      __syncwarp();  // the stage is refilled by the next issue()
+      cj += len;
+      cstage = (cstage + 1) % kRingStages;
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  }
+}
+
+bool inv_ring_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("XDG_INV_RING");
+    return e != nullptr && atoi(e) != 0;
+  }();
+  return on;
+}
+
 }  // namespace
 }  // namespace xdg
 
@@ -266,6 +365,30 @@ extern "C" int xdg_lu_inv_apply_tasks(int64_t ntasks, const int* task_sys,
   double* y = scratch + total;
   gather_kernel<<<grid_for(total, 256, 4), 256, 0, s>>>(total, src, b, t);
   XDG_CHECK_LAUNCH();
+  const int sv_len = (max_dim + 1) & ~1;
+  const size_t rsmem = sizeof(double) * ((size_t)sv_len + 8 * kRingStages * kRingChunk);
+  if (inv_ring_enabled() && rsmem <= 200 * 1024) {
+    static size_t rattr = 0;
+    if (rsmem > rattr) {
+      XDG_TRY_CUDA(cudaFuncSetAttribute(inv_rows_ring_kernel<true>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)rsmem));
+      XDG_TRY_CUDA(cudaFuncSetAttribute(inv_rows_ring_kernel<false>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)rsmem));
+      rattr = rsmem;
+    }
+    const int g = resident_grid(inv_rows_ring_kernel<true>, 256, rsmem, ntasks * 256);
+    inv_rows_ring_kernel<true><<<g, 256, rsmem, s>>>(ntasks, task_sys, task_row0,
+                                                      rows_per_task, sv_len, off, dims,
+                                                      vec_off, INV, t, y);
+    XDG_CHECK_LAUNCH();
+    inv_rows_ring_kernel<false><<<g, 256, rsmem, s>>>(ntasks, task_sys, task_row0,
+                                                       rows_per_task, sv_len, off, dims,
+                                                       vec_off, INV, y, x);
+    XDG_CHECK_LAUNCH();
+    return XDG_OK;
+  }
   const int g = resident_grid(inv_rows_smem_kernel<true>, 256, smem, ntasks * 256);
   inv_rows_smem_kernel<true><<<g, 256, smem, s>>>(ntasks, task_sys, task_row0, rows_per_task,
                                                   off, dims, vec_off, INV, t, y);

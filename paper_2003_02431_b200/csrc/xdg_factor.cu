@@ -76,7 +76,7 @@ lu_panel_kernel(int64_t nmat, double* __restrict__ A, const int64_t* __restrict_
                 const int* __restrict__ dn, const int* __restrict__ dp,
                 const int* __restrict__ dld, int* __restrict__ perm,
                 const int64_t* __restrict__ perm_off, int* __restrict__ info, int k0,
-                int NB, int rpc) {
+                int NB, int rpc, int S) {
   extern __shared__ double smem[];
   cg::cluster_group cluster = cg::this_cluster();
   const int C = (int)cluster.num_blocks();
@@ -84,7 +84,8 @@ lu_panel_kernel(int64_t nmat, double* __restrict__ A, const int64_t* __restrict_
   const int64_t b = blockIdx.x / C;
   if (b >= nmat) return;  // whole clusters only (grid = nmat * C)
   const Mat M = mat_of(A, off, dn, dp, dld, (int)b);
-  const int S = NB + 1;
+  // S = widest panel of this launch + 1 (min(NB, max_p - k0) + 1: fronts of
+  // 10-60 pivots leave room for several CTAs per SM)
   double* pan = smem;                       // rpc x S
   double* prow = pan + (size_t)rpc * S;     // pivot row (NB)
   double* xrow = prow + NB;                 // row received in an exchange (NB)
@@ -540,9 +541,10 @@ extern "C" int xdg_batched_factor(int64_t nmat, const int64_t* off, const int* n
       const int rows = max_n - k0;
       // smallest cluster whose row share fits the shared-memory budget
       int C = 1;
+      const int S = (std::min(NB, max_p - k0) + 1) | 1;  // odd: conflict-free column walks
       auto need = [&](int c) {
         const int rpc = (rows + c - 1) / c;
-        return (size_t)rpc * (NB + 1) * 8 + 2 * NB * 8 + 64;
+        return (size_t)rpc * S * 8 + 2 * NB * 8 + 64;
       };
       while (C < kMaxCluster && need(C) > kSmemCap) C *= 2;
       XDG_REQUIRE(need(C) <= kSmemCap, XDG_ERR_ARG, "matrix too large (n=%d)", max_n);
@@ -560,7 +562,7 @@ extern "C" int xdg_batched_factor(int64_t nmat, const int64_t* off, const int* n
       cfg.attrs = attr;
       cfg.numAttrs = 1;
       XDG_TRY_CUDA(cudaLaunchKernelEx(&cfg, lu_panel_kernel, nmat, A, off, n, p, ld, perm,
-                                      perm_off, info, k0, NB, rpc));
+                                      perm_off, info, k0, NB, rpc, S));
       // inside the super-panel: U12 and the update of its remaining columns
       XDG_TRY(trsm(k0, 0, K1));
       XDG_TRY(update(0, max_n, 0, K1, k0, k0 + NB, 1 | 2));
