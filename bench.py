@@ -41,7 +41,7 @@ def ncu_traffic(kernel_substr: str = "spmv_warp_rows<10"):
     committed `ncu --set full` capture (profiles/), or None."""
     import csv
 
-    path = os.path.join(ROOT, "profiles", "r1_spmv_ncu_raw_v2.csv")
+    path = os.path.join(ROOT, "profiles", "r2_spmv_ncu_raw.csv")
     try:
         rows = list(csv.reader(open(path)))
         h, units = rows[0], rows[1]
@@ -718,7 +718,7 @@ def run_ours(args):
                          "kernel": "xdg spmv_warp_rows<10>",
                          "kernel_ms": kern_ms, "bytes_per_launch": B_local,
                          "traffic": ncu_traffic() if args.n == 128 and world == 1 else None,
-                         "traffic_source": "profiles/r1_spmv_ncu_raw_v2.csv (ncu --set full, "
+                         "traffic_source": "profiles/r2_spmv_ncu_raw.csv (ncu --set full, "
                                            "same command, dram__bytes_read+write per launch)"},
             "e2e": {"value": e2e_val, "unit": "GB/s",
                     "h2d_bytes_per_step": 8 * nloc * N, "d2h_bytes_per_step": 8 * nloc * N,

@@ -504,8 +504,150 @@ namespace omg_graph {
 struct RmDev {
   double best_norm, last, bytes, pad0;
   int ncols, last_dependent, dependent_count, rejected_count, restart_count;
-  int col, path, it, budget, pad1;
+  int col, path, it, budget, ticket;
 };
+
+// ---- rm_step control without conditional nodes (XDG_OMG_FLAT) -------------
+// The IF (restart when full) and SWITCH (accept / dependent / rejected) nodes
+// of an rm_step become two ordinary kernels: every CTA takes the decision
+// from the same device state (thread 0, broadcast through shared memory),
+// does its slice of the chosen path, and the LAST CTA to finish (ticket
+// counter) writes the state updates -- no CTA reads the state after it
+// changed.  Same arithmetic as the conditional bodies (bit-identical); a
+// kernel whose path has no vector work exits at once.
+__device__ __forceinline__ bool last_cta(int* ticket) {
+  __shared__ int is_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const int t = atomicAdd(ticket, 1);
+    is_last = t == (int)gridDim.x - 1;
+    if (is_last) *ticket = 0;
+  }
+  __syncthreads();
+  return is_last != 0;
+}
+
+__global__ void __launch_bounds__(kT)
+rm_flat_begin_kernel(int64_t n, RmDev* st, int max_columns, double restart_bytes,
+                     double* gbytes, double* __restrict__ x0, double* __restrict__ r0,
+                     double* __restrict__ y, double* __restrict__ My, double* __restrict__ x,
+                     double* __restrict__ r) {
+  __shared__ int full_s;
+  if (threadIdx.x == 0) full_s = *(volatile int*)&st->ncols >= max_columns;
+  __syncthreads();
+  if (!full_s) return;  // uniform over the grid: nobody takes a ticket
+  const int64_t stride = (int64_t)gridDim.x * kT;
+  for (int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x; i < n; i += stride) {
+    const double xn = __dadd_rn(x0[i], y[i]);
+    const double rn = __dadd_rn(r0[i], -My[i]);
+    x0[i] = xn;
+    r0[i] = rn;
+    y[i] = 0.0;
+    My[i] = 0.0;
+    x[i] = xn;
+    r[i] = rn;
+  }
+  if (last_cta(&st->ticket) && threadIdx.x == 0) {
+    st->ncols = 0;
+    st->restart_count += 1;
+    *gbytes += restart_bytes;
+  }
+}
+
+__global__ void __launch_bounds__(kT)
+rm_flat_finish_kernel(int64_t n, RmDev* st, const double* sc, double* gbytes, double spmv2,
+                      double cgs_per_col, double cgs_fixed, const double* __restrict__ z,
+                      const double* __restrict__ w, double* __restrict__ y,
+                      double* __restrict__ x0, double* __restrict__ r0,
+                      const double* __restrict__ My_new, double* __restrict__ My,
+                      double* __restrict__ x, double* __restrict__ r, double* __restrict__ Z,
+                      double* __restrict__ W) {
+  __shared__ int path_s, col_s;
+  __shared__ double rho_s;
+  if (threadIdx.x == 0) {  // rm_dev_decide_kernel's decision, state untouched
+    const double scale = sqrt(sc[0]), norm_w = sqrt(sc[1]);
+    int path;
+    double rho = 0.0;
+    if (scale == 0.0 || norm_w <= 1e-13 * scale) {
+      path = 1;
+    } else {
+      rho = sqrt(sc[3]);
+      path = rho > *(volatile double*)&st->best_norm ? 2 : 0;
+    }
+    path_s = path;
+    col_s = *(volatile int*)&st->ncols;
+    rho_s = rho;
+  }
+  __syncthreads();
+  const int path = path_s;
+  const int64_t col = col_s;
+  const int64_t stride = (int64_t)gridDim.x * kT;
+  const int64_t i0 = (int64_t)blockIdx.x * kT + threadIdx.x;
+  if (path == 0) {  // accept (rm_dev_commit_kernel)
+    const double a = sc[2];
+    double* Zc = Z + col * n;
+    double* Wc = W + col * n;
+    for (int64_t i = i0; i < n; i += stride) {
+      const double zi = z[i];
+      const double yi = __dadd_rn(y[i], __dmul_rn(a, zi));
+      const double mn = My_new[i];
+      y[i] = yi;
+      x[i] = __dadd_rn(x0[i], yi);
+      r[i] = __dadd_rn(r0[i], -mn);
+      My[i] = mn;
+      Zc[i] = zi;
+      Wc[i] = w[i];
+    }
+  } else if (path == 1) {  // dependent (rm_current_kernel)
+    for (int64_t i = i0; i < n; i += stride) {
+      x[i] = __dadd_rn(x0[i], y[i]);
+      r[i] = __dadd_rn(r0[i], -My[i]);
+    }
+  } else {  // rejected: restart (rm_dev_restart_kernel)
+    for (int64_t i = i0; i < n; i += stride) {
+      const double xn = __dadd_rn(x0[i], y[i]);
+      const double rn = __dadd_rn(r0[i], -My[i]);
+      x0[i] = xn;
+      r0[i] = rn;
+      y[i] = 0.0;
+      My[i] = 0.0;
+      x[i] = xn;
+      r[i] = rn;
+    }
+  }
+  if (last_cta(&st->ticket) && threadIdx.x == 0) {
+    const double nn = (double)n;
+    double bytes = spmv2 + 96.0 * nn + (col > 0 ? cgs_per_col * col + cgs_fixed : 0.0);
+    if (path == 1) {
+      st->last_dependent = 1;
+      st->dependent_count += 1;
+      bytes += 48.0 * nn;
+    } else if (path == 2) {
+      st->last_dependent = 0;
+      st->rejected_count += 1;
+      st->ncols = 0;
+      st->restart_count += 1;
+      bytes += 80.0 * nn;
+    } else {
+      st->last_dependent = 0;
+      st->col = (int)col;
+      st->ncols = (int)col + 1;
+      st->best_norm = rho_s;
+      bytes += 64.0 * nn;
+    }
+    st->path = path;
+    *gbytes += bytes;
+  }
+}
+
+bool omg_flat_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("XDG_OMG_FLAT");
+    return e != nullptr && atoi(e) != 0;
+  }();
+  return on;
+}
 
 __global__ void rm_dev_pre_kernel(RmDev* st, int max_columns, cudaGraphConditionalHandle h,
                                   double restart_bytes, double* gbytes) {
@@ -730,7 +872,12 @@ int cap_rm_step(GraphOmg& G, int lam, double* z, cudaStream_t s, int depth) {
   const xdg_stream_t xs = reinterpret_cast<xdg_stream_t>(s);
   const int* ncols = &st->ncols;
   // restart when the space is full (solvers.py:574-575)
-  {
+  const bool flat = omg_flat_enabled();
+  if (flat) {
+    rm_flat_begin_kernel<<<grid_for(n, kT, kPerSm), kT, 0, s>>>(
+        n, st, mc, 80.0 * n, G.gbytes, rm.x0, rm.r0, rm.y, rm.My, rm.x, rm.r);
+    XDG_CHECK_LAUNCH();
+  } else {
     cudaGraphConditionalHandle h;
     XDG_TRY(make_handle(s, &h));
     rm_dev_pre_kernel<<<1, 1, 0, s>>>(st, mc, h, 80.0 * n, G.gbytes);
@@ -762,7 +909,13 @@ int cap_rm_step(GraphOmg& G, int lam, double* z, cudaStream_t s, int depth) {
   XDG_TRY(spmv(&lv.M, z, rm.Mz, nullptr, nullptr, nullptr, s));    // exact image
   XDG_TRY(xdg_rm_update(n, rm.r0, rm.My, rm.Mz, sc + 2, rm.My_new, sc + 3, rm.ws, xs));
   g_bytes = saved;
-  {
+  if (flat) {
+    const double sb = spmv_bytes(&lv.M, false);
+    rm_flat_finish_kernel<<<grid_for(n, kT, kPerSm), kT, 0, s>>>(
+        n, st, sc, G.gbytes, 2.0 * sb, 8.0 * n * 5, 8.0 * n * 10, z, w, rm.y, rm.x0, rm.r0,
+        rm.My_new, rm.My, rm.x, rm.r, rm.Z, rm.W);
+    XDG_CHECK_LAUNCH();
+  } else {
     cudaGraphConditionalHandle h;
     XDG_TRY(make_handle(s, &h));
     const double sb = spmv_bytes(&lv.M, false);

@@ -32,6 +32,42 @@ namespace {
 
 constexpr int kT = 256;
 
+// Programmatic dependent launch for the level chain (gather_h -> rows_h ->
+// gather_{h+1} ...): every launch of a sweep depends on the previous one only
+// through the small vectors W / Y / C / X; tasks, nodes and the factor F are
+// read-only.  With XDG_MF_PDL a kernel lets its successor's CTAs become
+// resident at once (launch_dependents) and the successor fetches its first
+// descriptors (and touches its first factor rows) before it waits for the
+// predecessor's stores (griddepcontrol.wait): the launch ramp and the
+// descriptor -> node chain overlap the predecessor's tail.
+bool mf_pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("XDG_MF_PDL");
+    return e != nullptr && atoi(e) != 0;
+  }();
+  return on;
+}
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+template <typename... KArgs, typename... Args>
+cudaError_t launch_chain(void (*kernel)(KArgs...), int grid, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kT);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = mf_pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, KArgs(args)...);
+}
+
 // Sub-warp row dots.  A warp task covers 32/G consecutive rows of one
 // front, G lanes per row (G = power of two chosen per front from the row
 // length, so short rows still keep the whole warp's loads in flight and long
@@ -208,13 +244,32 @@ mf_gather_kernel(int64_t e0, int64_t e1, const int64_t* __restrict__ ent_w,
                  const double* __restrict__ ent_scale,
                  const double* __restrict__ b, const double* __restrict__ C,
                  double* __restrict__ W) {
-  for (int64_t e = e0 + (int64_t)blockIdx.x * kT + threadIdx.x; e < e1;
-       e += (int64_t)gridDim.x * kT) {
-    const int64_t s = ent_src[e];
-    double v = s >= 0 ? __dmul_rn(ent_scale[e], b[s]) : 0.0;
-    for (int64_t k = ent_cptr[e]; k < ent_cptr[e + 1]; ++k)
-      v = __dadd_rn(v, C[ent_cidx[k]]);
-    W[ent_w[e]] = v;
+  pdl_trigger();
+  // the entry lists are static: the first entry's descriptors are loaded
+  // before the wait for the previous launch's C (and for b)
+  int64_t e = e0 + (int64_t)blockIdx.x * kT + threadIdx.x;
+  int64_t s = -1, k0 = 0, k1 = 0, wi = 0;
+  double sc = 0.0;
+  if (e < e1) {
+    s = ent_src[e];
+    sc = ent_scale[e];
+    k0 = ent_cptr[e];
+    k1 = ent_cptr[e + 1];
+    wi = ent_w[e];
+  }
+  pdl_wait();
+  while (e < e1) {
+    double v = s >= 0 ? __dmul_rn(sc, b[s]) : 0.0;
+    for (int64_t k = k0; k < k1; ++k) v = __dadd_rn(v, C[ent_cidx[k]]);
+    W[wi] = v;
+    e += (int64_t)gridDim.x * kT;
+    if (e < e1) {
+      s = ent_src[e];
+      sc = ent_scale[e];
+      k0 = ent_cptr[e];
+      k1 = ent_cptr[e + 1];
+      wi = ent_w[e];
+    }
   }
 }
 
@@ -620,13 +675,7 @@ __global__ void __launch_bounds__(kT, MF_MINB)
 mf_merged_kernel(int64_t t0, int64_t ntasks, int64_t c0, int64_t nctasks,
                  const int4* __restrict__ tasks, Ctx c) {
   __shared__ double part[2][kNG][kGW][2 * kMR];
-  {
-    const int grp = (threadIdx.x >> 5) / kGW;
-    int par = 0;  // alternating buffers: one group barrier per task
-    for (int64_t ct = (int64_t)blockIdx.x * kNG + grp; ct < nctasks;
-         ct += (int64_t)gridDim.x * kNG, par ^= 1)
-      run_merged_group<FWD>(c, tasks[c0 + interleave(ct, nctasks)], grp, part[par][grp]);
-  }
+  pdl_trigger();
   // Warp tasks, software-pipelined through shared memory: while task k runs,
   // the node of task k + 1 and the descriptor of task k + 2 are in flight
   // (cp.async), so a task's chain of dependent loads is its factor rows only
@@ -638,7 +687,6 @@ mf_merged_kernel(int64_t t0, int64_t ntasks, int64_t c0, int64_t nctasks,
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
   const int64_t nw = (int64_t)gridDim.x * (kT / 32);
   const int64_t w0 = (int64_t)blockIdx.x * (kT / 32) + wp;
-  if (w0 >= ntasks) return;
   auto fetch_task = [&](int64_t w, int slot) {  // lane 6: 16-byte descriptor
     if (lane == 6) cp_async16(&tks[wp][slot], tasks + t0 + interleave(w, ntasks));
   };
@@ -647,11 +695,25 @@ mf_merged_kernel(int64_t t0, int64_t ntasks, int64_t c0, int64_t nctasks,
       cp_async16(reinterpret_cast<char*>(&nds[wp][slot]) + 16 * lane,
                  reinterpret_cast<const char*>(c.nodes + node) + 16 * lane);
   };
-  fetch_task(w0, 0);
-  cp_async_wait_all();
-  __syncwarp();
-  fetch_node(tks[wp][0].x, 0);
-  if (w0 + nw < ntasks) fetch_task(w0 + nw, 1);
+  // static data only up to the wait: the first descriptor and node of this
+  // warp's tasks (and of its group's first CTA task) are on their way while
+  // the previous launch of the chain drains
+  if (w0 < ntasks) {
+    fetch_task(w0, 0);
+    cp_async_wait_all();
+    __syncwarp();
+    fetch_node(tks[wp][0].x, 0);
+    if (w0 + nw < ntasks) fetch_task(w0 + nw, 1);
+  }
+  pdl_wait();
+  {
+    const int grp = (threadIdx.x >> 5) / kGW;
+    int par = 0;  // alternating buffers: one group barrier per task
+    for (int64_t ct = (int64_t)blockIdx.x * kNG + grp; ct < nctasks;
+         ct += (int64_t)gridDim.x * kNG, par ^= 1)
+      run_merged_group<FWD>(c, tasks[c0 + interleave(ct, nctasks)], grp, part[par][grp]);
+  }
+  if (w0 >= ntasks) return;
   int k = 0;
   for (int64_t w = w0; w < ntasks; w += nw, k ^= 1) {
     cp_async_wait_all();
@@ -676,9 +738,8 @@ int launch_merged(const xdg_mf* mf, int h, double* x, cudaStream_t s) {
   if (nt <= 0 && nc <= 0) return XDG_OK;
   Ctx c{mf->nodes, mf->F, mf->bidx, mf->pdst, mf->pscale, mf->W, mf->Y, mf->C, x, mf->X};
   const int g = resident_grid(mf_merged_kernel<FWD>, kT, 0, (nt + nc * kGW) * 32);
-  mf_merged_kernel<FWD><<<g, kT, 0, s>>>(t0, nt, c0, nc,
-                                         reinterpret_cast<const int4*>(mf->tasks), c);
-  XDG_CHECK_LAUNCH();
+  XDG_TRY_CUDA(launch_chain(mf_merged_kernel<FWD>, g, s, t0, nt, c0, nc,
+                        reinterpret_cast<const int4*>(mf->tasks), c));
   return XDG_OK;
 }
 
@@ -839,10 +900,9 @@ extern "C" int xdg_mf_solve_phase(const xdg_mf* mf, const double* b, double* x, 
     for (int h = HF; h < H; ++h) {
       const int64_t e0 = mf->lev_ent[h], e1 = mf->lev_ent[h + 1];
       if (e1 > e0) {
-        mf_gather_kernel<<<grid_for(e1 - e0, kT, 8), kT, 0, s>>>(
-            e0, e1, mf->ent_w, mf->ent_src, mf->ent_cptr, mf->ent_cidx, mf->ent_scale, b,
-            mf->C, mf->W);
-        XDG_CHECK_LAUNCH();
+        XDG_TRY_CUDA(launch_chain(mf_gather_kernel, grid_for(e1 - e0, kT, 8), s, e0, e1,
+                              mf->ent_w, mf->ent_src, mf->ent_cptr, mf->ent_cidx,
+                              mf->ent_scale, b, mf->C, mf->W));
       }
       if (mf->merged) {
         XDG_TRY(launch_fwd_cols(mf, h, x, s));
