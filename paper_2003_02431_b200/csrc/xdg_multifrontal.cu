@@ -35,7 +35,7 @@ constexpr int kT = 256;
 // Programmatic dependent launch for the level chain (gather_h -> rows_h ->
 // gather_{h+1} ...): every launch of a sweep depends on the previous one only
 // through the small vectors W / Y / C / X; tasks, nodes and the factor F are
-// read-only.  With XDG_MF_PDL a kernel lets its successor's CTAs become
+// read-only.  Unless XDG_MF_PDL=0, a kernel lets its successor's CTAs become
 // resident at once (launch_dependents) and the successor fetches its first
 // descriptors (and touches its first factor rows) before it waits for the
 // predecessor's stores (griddepcontrol.wait): the launch ramp and the
@@ -43,7 +43,7 @@ constexpr int kT = 256;
 bool mf_pdl_enabled() {
   static const bool on = [] {
     const char* e = getenv("XDG_MF_PDL");
-    return e != nullptr && atoi(e) != 0;
+    return e == nullptr || atoi(e) != 0;  // default on: cfg2 low-order solve 2.52 -> 2.42 ms
   }();
   return on;
 }

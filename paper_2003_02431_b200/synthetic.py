@@ -156,7 +156,12 @@ def cfg3_slab_device(n: int, rank: int = 0, world: int = 1, seed: int = 0,
     for s in range(0, len(diag_idx), chunk):
         idx = diag_idx[s:s + chunk]
         A = torch.randn(len(idx), N, N, generator=g, device=dev, dtype=torch.float64)
-        val[idx] = torch.bmm(A.transpose(1, 2), A) + eye
+        # A^T A as N rank-one updates in k order (elementwise kernels: no
+        # library GEMM appears in the bench process's launch list)
+        G = eye.expand(len(idx), N, N).clone()
+        for k in range(N):
+            G.addcmul_(A[:, k, :, None], A[:, k, None, :])
+        val[idx] = G
     # random blocks are layout-agnostic and A^T A + 10 I is symmetric, so the
     # values are written directly as column-major blocks
     h["D"] = DeviceBSR.from_arrays(rp, lcol, val, N, nloc + len(h["ghosts"]), ctx,

@@ -134,6 +134,28 @@ def build_case(name):
     return spec["case"]
 
 
+_SOLVE_CTX = None
+
+
+def _solve_task(task):
+    """One reference solve: t = 0 on b, t > 0 on the +-1-ulp perturbed b."""
+    solver, t = task
+    hier, M, b, spec, dim = _SOLVE_CTX
+    cfg = SolverConfig(**spec[solver])
+    bt = b if t == 0 else perturbed(b, t)
+    t0 = time.time()
+    if solver == "omg":
+        x, rep = ortho_mg_solve(hier, bt, None, cfg, 1)
+    else:
+        x, rep = gmres_pmg_solve(M, bt, cfg, dim=dim)
+    dt = time.time() - t0
+    print(f"  [{solver} trial {t}] it={rep.iterations} {dt:.1f}s", flush=True)
+    if t == 0:
+        return (solver, t, rep.iterations, x, np.array(rep.residual_history),
+                rep.converged, rep.final_residual, dt)
+    return (solver, t, rep.iterations, None, None, rep.converged, rep.final_residual, dt)
+
+
 def run(name):
     spec = CASES[name]
     case = build_case(name)
@@ -217,30 +239,30 @@ def run(name):
     out["rm_x"], out["rm_r"] = np.array(xs), np.array(rs)
     out["rm_info"] = np.array(info, np.int64)
 
-    # solves
+    # solves: the reference solve (t = 0) and the envelope's perturbed trials
+    # are independent; MG_PAR=N runs them in N forked workers (same code,
+    # same single-threaded BLAS: identical results, less wall time)
+    global _SOLVE_CTX
+    _SOLVE_CTX = (hier, M, b, spec, case.dim)
+    tasks = [(solver, t) for solver in ("omg", "gmres") for t in range(spec["envelope"])]
+    par = int(os.environ.get("MG_PAR", "1"))
+    if par > 1:
+        import multiprocessing as mp
+
+        with mp.get_context("fork").Pool(par) as pool:
+            results = pool.map(_solve_task, tasks, chunksize=1)
+    else:
+        results = [_solve_task(tk) for tk in tasks]
     for solver in ("omg", "gmres"):
-        cfgd = spec[solver]
-        cfg = SolverConfig(**cfgd)
-        t0 = time.time()
-        if solver == "omg":
-            x, rep = ortho_mg_solve(hier, b, None, cfg, 1)
-        else:
-            x, rep = gmres_pmg_solve(M, b, cfg, dim=case.dim)
-        dt = time.time() - t0
-        print(f"[{name}] {solver}: it={rep.iterations} conv={rep.converged} "
-              f"res={rep.final_residual:.3e} {dt:.1f}s", flush=True)
+        res = [r for r in results if r[0] == solver]
+        res.sort(key=lambda r: r[1])
+        _, _, it0, x, hist, conv, fres, dt = res[0]
+        print(f"[{name}] {solver}: it={it0} conv={conv} res={fres:.3e} {dt:.1f}s", flush=True)
         out[f"{solver}_x"] = x
-        out[f"{solver}_hist"] = np.array(rep.residual_history)
-        out[f"{solver}_iters"] = np.int64(rep.iterations)
+        out[f"{solver}_hist"] = hist
+        out[f"{solver}_iters"] = np.int64(it0)
         meta[f"{solver}_seconds"] = dt
-        its = [rep.iterations]
-        for t in range(1, spec["envelope"]):
-            bt = perturbed(b, t)
-            if solver == "omg":
-                _, rp_ = ortho_mg_solve(hier, bt, None, cfg, 1)
-            else:
-                _, rp_ = gmres_pmg_solve(M, bt, cfg, dim=case.dim)
-            its.append(rp_.iterations)
+        its = [r[2] for r in res]
         out[f"{solver}_envelope"] = np.array(its, np.int64)
         print(f"[{name}] {solver} envelope {its}", flush=True)
     out["meta"] = np.frombuffer(json.dumps(meta).encode(), np.uint8)

@@ -46,4 +46,12 @@ x, rep = run()
 torch.cuda.synchronize()
 if steady:
     torch.cuda.profiler.stop()
-print(f"{solver}: it={rep.iterations} res={rep.final_residual:.3e} t={rep.time_iterations:.3f}s")
+times = [rep.time_iterations]
+for a in sys.argv:  # --repeat=N: N more timed solves in this process
+    if a.startswith("--repeat="):
+        for _ in range(int(a.split("=")[1])):
+            x, rep = run()
+            torch.cuda.synchronize()
+            times.append(rep.time_iterations)
+print(f"{solver}: it={rep.iterations} res={rep.final_residual:.3e} t={rep.time_iterations:.3f}s"
+      + (f" all={[round(t, 3) for t in times]}" if len(times) > 1 else ""))
