@@ -442,9 +442,10 @@ class Multifrontal:
         P_list, kids = nested_dissection(G.g_ptr, G.g_col, nv, max(1, leaf_unknowns // m))
         nn = len(P_list)
         self.nnodes = nn
+        Plen0 = np.fromiter((len(P) for P in P_list), np.int64, nn)
+        Pcat0 = np.concatenate(P_list) if nn else np.zeros(0, np.int64)
         owner = np.empty(nv, np.int64)
-        for t, P in enumerate(P_list):
-            owner[P] = t
+        owner[Pcat0] = np.repeat(np.arange(nn), Plen0)
         parent = np.full(nn, -1, np.int64)
         height = np.zeros(nn, np.int64)
         for t in range(nn):
@@ -484,12 +485,12 @@ class Multifrontal:
 
         # position of every vertex inside its owner's P; B positions by key
         ppos = np.empty(nv, np.int64)
-        for P in P_list:
-            ppos[P] = np.arange(len(P))
+        ppos[Pcat0] = _ranges(np.zeros(nn, np.int64), Plen0)
         bkey_node = np.repeat(np.arange(nn), [len(B) for B in B_list])
         bkey_v = np.concatenate(B_list) if nn else np.zeros(0, np.int64)
         bkey = bkey_node * max(nv, 1) + bkey_v
-        bkey_pos = np.concatenate([np.arange(len(B)) for B in B_list]) if nn else bkey
+        bkey_pos = _ranges(np.zeros(nn, np.int64),
+                           np.fromiter((len(B) for B in B_list), np.int64, nn)) if nn else bkey
         so = np.argsort(bkey, kind="stable")
         bkey, bkey_pos = bkey[so], bkey_pos[so]
 
@@ -767,56 +768,65 @@ class Multifrontal:
         # (multi-GPU: entries and tasks of the owned fronts first, then of the
         # shared top fronts -- two sweeps over the heights, self.lev_*[k])
         classes = [need & ~shared, need & shared]
-        ent_w, ent_src, ent_scale = [], [], []
+        # (vectorised over all fronts: a Schwarz plan of 337 systems has
+        # ~27,000 of them, and per-front numpy calls cost 1 s of its setup)
+        Plen = np.array([len(P) for P in P_list], np.int64)
+        Blen = np.array([len(B) for B in B_list], np.int64)
+        Pptr = np.concatenate([[0], np.cumsum(Plen)])
+        Bptr = np.concatenate([[0], np.cumsum(Blen)])
+        Pcat = np.concatenate(P_list) if nn else np.zeros(0, np.int64)
+        Bcat = bkey_v
+        node_of_P = np.repeat(np.arange(nn), Plen)
+        node_of_B = bkey_node
+        seq = np.concatenate([order[cls[order]] for cls in classes]) if nn else order
         lev_ent_k = []
         ent_first = np.zeros(nn, np.int64)  # first entry id of each node
-        inv_perm = [None] * nn
+        cnt_seq = (pn + bn)[seq]
+        ent_first[seq] = np.cumsum(cnt_seq) - cnt_seq
         cur = 0
         for cls in classes:
-          lev_ent = [cur]
-          for h in range(H):
-            for t in order[(height[order] == h) & cls[order]]:
-                p, b = int(pn[t]), int(bn[t])
-                ent_first[t] = cur
-                pu = perms[t]  # permuted position i <- front unknown pu[i]
-                ip = np.empty(p, np.int64)
-                ip[pu] = np.arange(p)
-                inv_perm[t] = ip
-                P = P_list[t]
-                srcP = (vsrc[P][:, None] + am[None, :]).reshape(-1)
-                ent_src.append(srcP[pu])
-                sP = scale_h.reshape(nv, m)[P].reshape(-1)
-                ent_scale.append(sP[pu])
-                ent_scale.append(np.ones(b))
-                ent_src.append(np.full(b, -1, np.int64))
-                ent_w.append(w_off[t] + np.arange(p + b))
-                cur += p + b
-            lev_ent.append(cur)
-          lev_ent_k.append(lev_ent)
-        ent_w = np.concatenate(ent_w) if ent_w else np.zeros(0, np.int64)
-        ent_src = np.concatenate(ent_src) if ent_src else np.zeros(0, np.int64)
-        ent_scale = np.concatenate(ent_scale) if ent_scale else np.zeros(0)
+            hs = height[order[cls[order]]]
+            sz = (pn + bn)[order[cls[order]]]
+            per_h = np.bincount(hs, weights=sz, minlength=H).astype(np.int64) if H else \
+                np.zeros(0, np.int64)
+            lev_ent_k.append([int(v) for v in cur + np.concatenate([[0], np.cumsum(per_h)])])
+            cur += int(sz.sum())
+        E = cur
+        # permuted pivot unknowns of every needed front, fronts in id order:
+        # position i of front t holds front unknown perms[t][i]
+        ids = np.flatnonzero(need)
+        pu_glob = (np.concatenate([perms[t] for t in ids]) if len(ids)
+                   else np.zeros(0, np.int64)) + np.repeat(Pptr[ids] * m, pn[ids])
+        loc = _ranges(np.zeros(len(ids), np.int64), pn[ids])  # i within the front
+        inv_perm_all = np.zeros(int(Pptr[-1]) * m, np.int64)  # front unknown -> position
+        inv_perm_all[pu_glob] = loc
+        src_all = (vsrc[Pcat][:, None] + am[None, :]).reshape(-1)
+        scl_all = scale_h.reshape(nv, m)[Pcat].reshape(-1)
+        ent_src = np.full(E, -1, np.int64)
+        ent_scale = np.ones(E)
+        piv_ent = np.repeat(ent_first[ids], pn[ids]) + loc
+        ent_src[piv_ent] = src_all[pu_glob]
+        ent_scale[piv_ent] = scl_all[pu_glob]
+        ent_w = _ranges(w_off[seq], w_off[seq] + cnt_seq)
         # contributions: child c's boundary unknown j -> parent's entry
-        c_tgt, c_src = [], []
-        for c in range(nn):
-            t = parent[c]
-            if t < 0 or bn[c] == 0 or not need[t]:
-                continue
-            Bc = B_list[c]
-            inP = owner[Bc] == t
-            fu = np.empty(len(Bc), np.int64)  # unpermuted front unknown (mode 0)
-            fu[inP] = ppos[Bc[inP]] * m
-            fu[~inP] = pn[t] + bpos(np.full(int((~inP).sum()), t), Bc[~inP]) * m
-            fu = (fu[:, None] + am[None, :]).reshape(-1)
-            ent = np.where(fu < pn[t], inv_perm[t][np.minimum(fu, max(pn[t] - 1, 0))], fu)
-            c_tgt.append(ent_first[t] + ent)
-            c_src.append(c_off[c] + np.arange(bn[c]))
-        if c_tgt:
-            c_tgt, c_src = np.concatenate(c_tgt), np.concatenate(c_src)
+        par_B = parent[node_of_B] if nn else node_of_B
+        okc = (par_B >= 0) & need[np.maximum(par_B, 0)] if nn else np.zeros(0, bool)
+        cB, tB, vB = node_of_B[okc], par_B[okc], Bcat[okc]
+        jB = (np.arange(len(Bcat)) - Bptr[node_of_B])[okc]  # position in the child's B
+        inP = owner[vB] == tB
+        fu0 = np.empty(len(vB), np.int64)  # unpermuted front unknown (mode 0)
+        fu0[inP] = ppos[vB[inP]] * m
+        fu0[~inP] = pn[tB[~inP]] + bpos(tB[~inP], vB[~inP]) * m
+        fu = (fu0[:, None] + am[None, :]).reshape(-1)
+        tt = np.repeat(tB, m)
+        piv = fu < pn[tt]
+        ent = fu.copy()
+        ent[piv] = inv_perm_all[Pptr[tt[piv]] * m + fu[piv]]
+        c_tgt = ent_first[tt] + ent
+        c_src = ((c_off[cB] + jB * m)[:, None] + am[None, :]).reshape(-1)
+        if len(c_tgt):
             so = np.argsort(c_tgt, kind="stable")  # children in id order per entry
             c_tgt, c_src = c_tgt[so], c_src[so]
-        else:
-            c_tgt = c_src = np.zeros(0, np.int64)
         ent_cptr = np.zeros(len(ent_w) + 1, np.int64)
         np.cumsum(np.bincount(c_tgt, minlength=len(ent_w)), out=ent_cptr[1:])
         # warp tasks, level-sorted: (node, first row), 32/G rows each
@@ -928,13 +938,16 @@ class Multifrontal:
         bidx = np.zeros(int(bn.sum()), np.int64)
         pdst = np.zeros(int(pn.sum()), np.int64)
         pscale = np.ones(int(pn.sum()))
-        for t in range(nn):
-            if bn[t]:  # Y position (owner's pivot space) of each boundary unknown
-                Bt = B_list[t]
-                bidx[c_off[t]:c_off[t] + bn[t]] = (
-                    y_off[owner[Bt]][:, None] + ppos[Bt][:, None] * m + am).reshape(-1)
-            pdst[y_off[t]:y_off[t] + pn[t]] = (vdst[P_list[t]][:, None] + am).reshape(-1)
-            pscale[y_off[t]:y_off[t] + pn[t]] = scale_h.reshape(nv, m)[P_list[t]].reshape(-1)
+        if nn:
+            # Y position (owner's pivot space) of each boundary unknown
+            jB_all = np.arange(len(Bcat)) - Bptr[node_of_B]
+            bpos_all = ((c_off[node_of_B] + jB_all * m)[:, None] + am[None, :]).reshape(-1)
+            bidx[bpos_all] = ((y_off[owner[Bcat]] + ppos[Bcat] * m)[:, None]
+                              + am[None, :]).reshape(-1)
+            jP_all = np.arange(len(Pcat)) - Pptr[node_of_P]
+            ppos_all = ((y_off[node_of_P] + jP_all * m)[:, None] + am[None, :]).reshape(-1)
+            pdst[ppos_all] = (vdst[Pcat][:, None] + am[None, :]).reshape(-1)
+            pscale[ppos_all] = scl_all
         nodes = np.zeros(nn, NODE_DT)
         nodes["p"], nodes["b"], nodes["ldp"], nodes["ldb"] = pn, bn, pp, bp
         nodes["gp"], nodes["gb"] = gp, gb

@@ -39,14 +39,21 @@ def _ranges(starts: np.ndarray, ends: np.ndarray) -> np.ndarray:
 
 
 # Low-order factor selection.  A dense solve streams 8 n^2 bytes in 3
-# launches; the multifrontal one ~8 (p^2 + 2 p b) per front in 5 launches per
-# tree height.  Measured on B200 (cfg2, 32^3 p=3): for the Schwarz blocks'
-# ~1,800-unknown systems dense is faster (OMG 18.2 s vs 19.1 s); for the
-# 336,610-unknown global system of GMRES-PMG dense is impossible (906 GB) and
-# the multifrontal solve streams 12.2 GB in 2.6 ms.  Sparse when a system is
-# larger than DENSE_LOW_MAX_SYSTEM unknowns or the dense factors would take
-# more than a quarter of the free device memory.
+# launches; the multifrontal one ~8 (p^2 + 2 p b) per front in 2 launches per
+# tree height and sweep.  For the 336,610-unknown global system of GMRES-PMG
+# dense is impossible (906 GB).  For Schwarz plans the multifrontal factors
+# move fewer bytes per application but cost more setup (host symbolic phase,
+# hundreds of front buckets), so they pay off when the plan's dense factors
+# are large.  Measured on B200 (round 2 session 5, OMG cold solves incl. the
+# lazy setup, `profiles/r2_omg_loworder_full.txt`): cfg2 level 1 (337
+# systems of ~1,810 unknowns, 8.8 GB dense) 15.1 s dense vs 14.2 s sparse
+# (steady-state 13.8 vs 10.9 s); 16^3 p=3 (1.7 GB dense) 4.13 vs 4.02 s;
+# 8^3 p=3 (0.2 GB) 1.47 vs 1.66 s; cfg4 at 16^3 0.54 vs 1.37 s.  Sparse when
+# a system is larger than DENSE_LOW_MAX_SYSTEM unknowns, when the plan's
+# dense factors exceed SPARSE_MIN_DENSE_BYTES, or when they would take more
+# than 0.6 of the free device memory.
 DENSE_LOW_MAX_SYSTEM = 16000  # unknowns
+SPARSE_MIN_DENSE_BYTES = 1.0e9
 # dense solves by CTA tasks with the right-hand side in shared memory: when
 # there are enough tasks to fill the GPU (4 CTAs per SM) and each system fits
 # 48 KB.  Measured at cfg2 level 1 (337 systems of ~1,810 unknowns): 5.0 TB/s
@@ -67,8 +74,9 @@ def use_multifrontal(dims) -> bool:
         return False
     free, _ = torch.cuda.mem_get_info()
     # the dense factors are built in place and factored in <= 2 GB chunks
-    return (int(dims.max()) > DENSE_LOW_MAX_SYSTEM
-            or 8 * int((dims * dims).sum()) > 0.6 * free)
+    dense_bytes = 8 * int((dims * dims).sum())
+    return (int(dims.max()) > DENSE_LOW_MAX_SYSTEM or dense_bytes > SPARSE_MIN_DENSE_BYTES
+            or dense_bytes > 0.6 * free)
 
 
 class PmgPlan:
