@@ -166,8 +166,15 @@ pmg_high_kernel(int nwork, int N, int m, const int* __restrict__ wi_ptr,
 // lane i of the group owns high row i.  Same arithmetic order per row as
 // pmg_high_kernel (blocks in order, low columns in order, separate mul/add;
 // column-oriented LU substitutions).
+// N_T / M_T > 0: block size and low modes known at compile time (the
+// BASELINE shapes): the residual's column loop and the substitution loops
+// unroll, and the lane's row of the LU factor is loaded up front -- the
+// serial shuffle chain then waits for no memory (it waited for one dependent
+// global load per step: 2 nh round trips per cell).  Same operations in the
+// same order as the generic instantiation (bit-identical).
+template <int N_T, int M_T>
 __global__ void __launch_bounds__(kT)
-pmg_high_packed_kernel(int nwork, int N, int m, const int* __restrict__ wi_ptr,
+pmg_high_packed_kernel(int nwork, int N_rt, int m_rt, const int* __restrict__ wi_ptr,
                        const int* __restrict__ wi_blk, const int* __restrict__ wi_lcol,
                        const int* __restrict__ wi_cell, const int* __restrict__ wi_lrow,
                        const int64_t* __restrict__ wi_xlo,
@@ -177,7 +184,11 @@ pmg_high_packed_kernel(int nwork, int N, int m, const int* __restrict__ wi_ptr,
                        const double* __restrict__ HLU, const int* __restrict__ hperm,
                        const double* __restrict__ b, const double* __restrict__ xlo_buf,
                        double* __restrict__ out_buf) {
+  constexpr bool FIX = N_T > 0;
+  const int N = FIX ? N_T : N_rt;
+  const int m = FIX ? M_T : m_rt;
   const int nh = N - m;
+  constexpr int NH_T = FIX ? N_T - M_T : 1;
   const int cpw = 32 / nh;
   const int lane = threadIdx.x & 31;
   const int grp = lane / nh;
@@ -191,10 +202,23 @@ pmg_high_packed_kernel(int nwork, int N, int m, const int* __restrict__ wi_ptr,
     const bool active = lane_ok && w < nwork;
     int e0 = 0, e1 = 0;
     const double* xlo = xlo_buf;
+    int c = 0, hi = 0;
     if (active) {
       e0 = wi_ptr[w];
       e1 = wi_ptr[w + 1];
       xlo = xlo_buf + wi_xlo[w];
+      c = wi_cell[w];
+      hi = wi_hidx[w];
+    }
+    const double* F = HLU + (int64_t)hi * nh * nh;
+    double frow[NH_T];  // F[j * nh + i], j = 0 .. nh-1: this lane's row of the LU
+    double bi = 0.0;
+    int pi = i;
+    if (FIX && active) {
+#pragma unroll
+      for (int j = 0; j < NH_T; ++j) frow[j] = __ldg(F + j * NH_T + i);
+      bi = b[(int64_t)c * N + m + i];
+      pi = hperm[(int64_t)hi * nh + i];
     }
     const int cnt = __reduce_max_sync(0xffffffffu, e1 - e0);
     double acc = 0.0;
@@ -204,28 +228,52 @@ pmg_high_packed_kernel(int nwork, int N, int m, const int* __restrict__ wi_ptr,
         const int64_t k = wi_blk[e];
         const double* v = val_t + k * N * N + m + i;
         const double* xq = xlo + (int64_t)wi_lcol[e] * m;
-        for (int q = 0; q < m; ++q)
-          acc = __dadd_rn(acc, __dmul_rn(__ldg(v + q * N), __ldg(xq + q)));
+        if (FIX) {
+          double vv[M_T > 0 ? M_T : 1], xx[M_T > 0 ? M_T : 1];
+#pragma unroll
+          for (int q = 0; q < M_T; ++q) {
+            vv[q] = __ldg(v + q * N_T);
+            xx[q] = __ldg(xq + q);
+          }
+#pragma unroll
+          for (int q = 0; q < M_T; ++q) acc = __dadd_rn(acc, __dmul_rn(vv[q], xx[q]));
+        } else {
+          for (int q = 0; q < m; ++q)
+            acc = __dadd_rn(acc, __dmul_rn(__ldg(v + q * N), __ldg(xq + q)));
+        }
       }
     }
     double r = 0.0;
-    int c = 0, hi = 0;
     if (active) {
-      c = wi_cell[w];
-      hi = wi_hidx[w];
-      r = __dadd_rn(b[(int64_t)c * N + m + i], -acc);
+      if (!FIX) {
+        bi = b[(int64_t)c * N + m + i];
+        pi = hperm[(int64_t)hi * nh + i];
+      }
+      r = __dadd_rn(bi, -acc);
     }
-    const double* F = HLU + (int64_t)hi * nh * nh;
-    const int pi = active ? hperm[(int64_t)hi * nh + i] : i;
     double t = __shfl_sync(0xffffffffu, r, base + pi);
-    for (int j = 0; j < nh; ++j) {  // unit lower, column-oriented
-      const double yj = __shfl_sync(0xffffffffu, t, base + j);
-      if (active && i > j) t = __dadd_rn(t, -__dmul_rn(yj, F[(int64_t)j * nh + i]));
-    }
-    for (int j = nh - 1; j >= 0; --j) {  // upper, column-oriented
-      if (active && i == j) t = __ddiv_rn(t, F[(int64_t)j * nh + j]);
-      const double xj = __shfl_sync(0xffffffffu, t, base + j);
-      if (active && i < j) t = __dadd_rn(t, -__dmul_rn(xj, F[(int64_t)j * nh + i]));
+    if (FIX) {
+#pragma unroll
+      for (int j = 0; j < NH_T; ++j) {  // unit lower, column-oriented
+        const double yj = __shfl_sync(0xffffffffu, t, base + j);
+        if (active && i > j) t = __dadd_rn(t, -__dmul_rn(yj, frow[j]));
+      }
+#pragma unroll
+      for (int j = NH_T - 1; j >= 0; --j) {  // upper, column-oriented
+        if (active && i == j) t = __ddiv_rn(t, frow[j]);
+        const double xj = __shfl_sync(0xffffffffu, t, base + j);
+        if (active && i < j) t = __dadd_rn(t, -__dmul_rn(xj, frow[j]));
+      }
+    } else {
+      for (int j = 0; j < nh; ++j) {  // unit lower, column-oriented
+        const double yj = __shfl_sync(0xffffffffu, t, base + j);
+        if (active && i > j) t = __dadd_rn(t, -__dmul_rn(yj, F[(int64_t)j * nh + i]));
+      }
+      for (int j = nh - 1; j >= 0; --j) {  // upper, column-oriented
+        if (active && i == j) t = __ddiv_rn(t, F[(int64_t)j * nh + j]);
+        const double xj = __shfl_sync(0xffffffffu, t, base + j);
+        if (active && i < j) t = __dadd_rn(t, -__dmul_rn(xj, F[(int64_t)j * nh + i]));
+      }
     }
     if (active) {
       double* o = out_buf + wi_out[w];
@@ -330,10 +378,24 @@ extern "C" int xdg_pmg_high(int nwork, int N, int m, const int* wi_ptr,
   if (nh <= 16) {
     const int cpw = 32 / nh;
     const int64_t warps = ((int64_t)nwork + cpw - 1) / cpw;
-    const int g = resident_grid(pmg_high_packed_kernel, kT, 0, warps * 32);
-    pmg_high_packed_kernel<<<g, kT, 0, s>>>(nwork, N, m, wi_ptr, wi_blk, wi_lcol,
-                                            wi_cell, wi_lrow, wi_xlo, wi_hidx,
-                                            wi_out, val_t, HLU, hperm, b, xlo, out);
+#define XDG_PACKED(NN, MM)                                                              \
+  if (N == NN && m == MM) {                                                             \
+    const int g = resident_grid(pmg_high_packed_kernel<NN, MM>, kT, 0, warps * 32);     \
+    pmg_high_packed_kernel<NN, MM><<<g, kT, 0, s>>>(nwork, N, m, wi_ptr, wi_blk,        \
+                                                    wi_lcol, wi_cell, wi_lrow, wi_xlo,  \
+                                                    wi_hidx, wi_out, val_t, HLU, hperm, \
+                                                    b, xlo, out);                       \
+    XDG_CHECK_LAUNCH();                                                                 \
+    return XDG_OK;                                                                      \
+  }
+    // (N, m) of the BASELINE configs: 3D p=3 k_lo=2 / 1, p=2 k_lo=1, p=1 k_lo=0... and 2D p=2
+    XDG_PACKED(20, 10) XDG_PACKED(20, 4) XDG_PACKED(10, 4) XDG_PACKED(10, 1)
+    XDG_PACKED(6, 3) XDG_PACKED(6, 1) XDG_PACKED(4, 1) XDG_PACKED(35, 20)
+#undef XDG_PACKED
+    const int g = resident_grid(pmg_high_packed_kernel<0, 0>, kT, 0, warps * 32);
+    pmg_high_packed_kernel<0, 0><<<g, kT, 0, s>>>(nwork, N, m, wi_ptr, wi_blk, wi_lcol,
+                                                  wi_cell, wi_lrow, wi_xlo, wi_hidx,
+                                                  wi_out, val_t, HLU, hperm, b, xlo, out);
     XDG_CHECK_LAUNCH();
     return XDG_OK;
   }
