@@ -1,0 +1,9 @@
+cd $GRAFT_REPO_ROOT
+# session 5, call 8: cfg4 at full size with the new low-order selection (auto vs dense); per-level multifrontal table and a full ncu capture with the PDL chain
+CELLS=96 timeout 1500 python tools/bench_cfg4.py omg 2>&1 | grep "^{" > gpurun_out/r2_cfg4_96cubed_auto.jsonl; tail -n 1 gpurun_out/r2_cfg4_96cubed_auto.jsonl | cut -c1-700
+CELLS=96 XDG_LOW_ORDER=dense timeout 1500 python tools/bench_cfg4.py omg 2>&1 | grep "^{" > gpurun_out/r2_cfg4_96cubed_dense.jsonl; tail -n 1 gpurun_out/r2_cfg4_96cubed_dense.jsonl | cut -c1-700
+ncu --metrics gpu__time_duration.sum --clock-control none -k regex:mf_ --csv --log-file gpurun_out/r2_mf_pdl_launches.csv python tools/mf_levels.py tests/golden/large/cfg2.npz 10 1 2>/dev/null | grep "^\[" > gpurun_out/r2_mf_pdl_rows.json
+python tools/mf_levels_pair.py gpurun_out/r2_mf_pdl_rows.json gpurun_out/r2_mf_pdl_launches.csv > gpurun_out/r2_mf_levels_pdl.txt
+head -n 50 gpurun_out/r2_mf_levels_pdl.txt
+ncu --set full --clock-control none --import-source on -k regex:mf_merged --launch-skip 28 --launch-count 28 -o gpurun_out/r2_mf_merged_pdl_full -f python tools/mf_levels.py tests/golden/large/cfg2.npz 10 1 > gpurun_out/ncu_mf_full.log 2>&1
+ls -la gpurun_out/*.ncu-rep
