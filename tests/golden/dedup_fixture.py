@@ -30,7 +30,8 @@ def main(src, dst=None):
             print(f"{k}: {len(a)} blocks -> {len(u)} unique")
         else:
             out[k] = a
-    np.savez(dst or src.replace(".npz", "_dedup.npz"), **out)
+    # compressed: the GPU-box snapshot of the working tree is limited to 512 MiB
+    np.savez_compressed(dst or src.replace(".npz", "_dedup.npz"), **out)
 
 
 if __name__ == "__main__":

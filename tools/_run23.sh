@@ -7,3 +7,8 @@ python tools/mf_levels_pair.py gpurun_out/r2_mf_pdl_rows.json gpurun_out/r2_mf_p
 head -n 50 gpurun_out/r2_mf_levels_pdl.txt
 ncu --set full --clock-control none --import-source on -k regex:mf_merged --launch-skip 28 --launch-count 28 -o gpurun_out/r2_mf_merged_pdl_full -f python tools/mf_levels.py tests/golden/large/cfg2.npz 10 1 > gpurun_out/ncu_mf_full.log 2>&1
 ls -la gpurun_out/*.ncu-rep
+for mode in "1 0" "0 0" "0 tree:4" "0 tree:8" "0 level:3"; do
+set -- $mode
+echo "== omg cfg2 150 it steady XDG_MF_MERGE=$1 XDG_MF_FUSE=$2"
+XDG_MF_MERGE=$1 XDG_MF_FUSE=$2 python tools/profile_solve.py tests/golden/large/cfg2.npz omg 150 --steady 2>&1 | tail -n 1
+done | tee gpurun_out/r2_omg_schwarz_mf_modes.txt
