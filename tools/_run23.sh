@@ -12,3 +12,14 @@ set -- $mode
 echo "== omg cfg2 150 it steady XDG_MF_MERGE=$1 XDG_MF_FUSE=$2"
 XDG_MF_MERGE=$1 XDG_MF_FUSE=$2 python tools/profile_solve.py tests/golden/large/cfg2.npz omg 150 --steady 2>&1 | tail -n 1
 done | tee gpurun_out/r2_omg_schwarz_mf_modes.txt
+timeout 1200 python tools/dist_lowfactor_memory.py cfg4 2>&1 | grep "^{" > gpurun_out/r2_dist_lowfactor_cfg4.jsonl; cut -c1-500 gpurun_out/r2_dist_lowfactor_cfg4.jsonl
+for p in 1 2 3 4 5; do
+timeout 900 python tools/time_setup.py --cells 48 --degree $p --radius 0.5 --solve omg 2>&1 | grep "^{" | tail -n 1
+done > gpurun_out/r2_cfg5_psweep_48cubed.jsonl
+cut -c1-90 gpurun_out/r2_cfg5_psweep_48cubed.jsonl; python - <<'PY'
+import json
+for l in open("gpurun_out/r2_cfg5_psweep_48cubed.jsonl"):
+    d = json.loads(l)
+    o = d.get("omg", {})
+    print(d["degree"], d["raw_dofs"], d["setup_s"], o.get("iterations"), o.get("solve_s"), o.get("dof_per_s"), o.get("converged"))
+PY
