@@ -611,7 +611,7 @@ def run_ours(args):
     if world == 1:
         # the public drop-in call on host buffers: BlockSparseMatrix.matvec
         # (blockmatrix.py:119-125 analogue) with pinned x / out -> pinned
-        # staging-free HostStreamSpMV (8 z-slab chunks: H2D || xdg_bsr_spmv
+        # staging-free HostStreamSpMV (z-slab chunks: H2D || xdg_bsr_spmv
         # per chunk through the C-ABI || D2H), blocking until y has landed
         from paper_2003_02431_b200.blockmatrix import BlockSparseMatrix, uniform_layout
 
@@ -622,7 +622,8 @@ def run_ours(args):
         torch.cuda.synchronize(dev)
         e2e_exact = bool(torch.equal(yh, y.cpu()))
         step = (lambda: Mpub.matvec(xh, out=yh))
-        e2e_path = ("BlockSparseMatrix.matvec(pinned x, out=pinned y): H2D (8 z-slab "
+        nchunks = len(Mpub._host_streamer(D)[0].bounds) - 1
+        e2e_path = (f"BlockSparseMatrix.matvec(pinned x, out=pinned y): H2D ({nchunks} z-slab "
                     "chunks) || xdg_bsr_spmv per chunk (C-ABI) || D2H y, full-duplex "
                     "overlapped, host-synchronous per call")
     else:

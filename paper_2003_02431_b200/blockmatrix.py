@@ -250,7 +250,9 @@ class BlockSparseMatrix:
 
         if self._host_stream is None or self._host_stream[0].D is not D:
             n = D.nbr * D.N
-            chunks = 8 if n >= self.STREAM_CHUNK_ROWS else 1
+            # measured at cfg3 (22 M rows; profiles/r2_e2e_chunks.json): 8 / 12 /
+            # 16 / 24 chunks -> 2,500 / 2,575 / 2,538 / 2,385 GB/s host to host
+            chunks = (12 if n >= (1 << 22) else 8) if n >= self.STREAM_CHUNK_ROWS else 1
             self._host_stream = (HostStreamSpMV(D, chunks=chunks),
                                  torch.empty(n, dtype=torch.float64).pin_memory(),
                                  torch.empty(n, dtype=torch.float64).pin_memory())

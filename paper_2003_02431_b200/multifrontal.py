@@ -439,6 +439,12 @@ class Multifrontal:
         self.G = G
         nv = G.nv
         self.total = nv * m
+        # leaf size of the dissection (unknowns): XDG_MF_LEAF for every plan,
+        # XDG_MF_LEAF_MULTI for plans of several independent systems (Schwarz
+        # blocks: shallow trees, launch-bound levels)
+        leaf_env = os.environ.get("XDG_MF_LEAF_MULTI" if len(sets) > 1 else "XDG_MF_LEAF")
+        if leaf_env:
+            leaf_unknowns = int(leaf_env)
         P_list, kids = nested_dissection(G.g_ptr, G.g_col, nv, max(1, leaf_unknowns // m))
         nn = len(P_list)
         self.nnodes = nn

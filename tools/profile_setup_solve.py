@@ -57,4 +57,5 @@ else:
 torch.cuda.synchronize()
 pr.disable()
 print(f"{solver} setup + 1 iteration: {time.perf_counter() - t0:.2f} s")
-pstats.Stats(pr).sort_stats("cumulative").print_stats(35)
+pstats.Stats(pr).sort_stats(os.environ.get("PROFILE_SORT", "cumulative")).print_stats(
+    int(os.environ.get("PROFILE_LINES", "35")))
