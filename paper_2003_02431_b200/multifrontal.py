@@ -182,10 +182,24 @@ class SystemGraph:
         self.gblk, self.sys = cat(gblk), cat(sys_of)
         self.a_row, self.a_col, self.a_k = cat(rows_l), cat(cols_l), cat(ks_l)
         off = self.a_row != self.a_col
-        r = np.concatenate([self.a_row[off], self.a_col[off]])
-        c = np.concatenate([self.a_col[off], self.a_row[off]])
-        key = np.unique(r * max(self.nv, 1) + c)
-        r, c = key // max(self.nv, 1), key % max(self.nv, 1)
+        nv1 = max(self.nv, 1)
+
+        def sorted_unique(k):
+            if len(k) > 1 and not np.all(k[1:] > k[:-1]):
+                k = np.sort(k)
+                k = k[np.concatenate([[True], k[1:] != k[:-1]])]
+            return k
+
+        # entries come row by row with ascending columns (sorted BSR rows and
+        # sorted sets), so the forward keys are already sorted; a structurally
+        # symmetric pattern (every operator here) needs no merge with its
+        # transpose.  (np.unique over both copies: 4.6 s of hashing for the
+        # 1.6 M vertices of cfg4's Schwarz systems.)
+        kf = sorted_unique(self.a_row[off] * nv1 + self.a_col[off])
+        kt = sorted_unique(self.a_col[off] * nv1 + self.a_row[off])
+        key = kf if (len(kf) == len(kt) and np.array_equal(kf, kt)) else \
+            sorted_unique(np.concatenate([kf, kt]))
+        r, c = key // nv1, key % nv1
         self.g_ptr = np.zeros(self.nv + 1, np.int64)
         np.cumsum(np.bincount(r, minlength=self.nv), out=self.g_ptr[1:])
         self.g_col = c
@@ -410,6 +424,14 @@ def _group(n: int) -> int:
     return g
 
 
+def _group_v(n: np.ndarray) -> np.ndarray:
+    """_group over an array."""
+    g = np.ones(len(n), np.int64)
+    for _ in range(5):
+        g = np.where((g < 32) & (MF_U * g < n), g * 2, g)
+    return g
+
+
 def _pad(x: int) -> int:
     return x if x <= 32 else ((x + 31) // 32) * 32
 
@@ -454,10 +476,17 @@ class Multifrontal:
         owner[Pcat0] = np.repeat(np.arange(nn), Plen0)
         parent = np.full(nn, -1, np.int64)
         height = np.zeros(nn, np.int64)
-        for t in range(nn):
-            for c in kids[t]:
-                parent[c] = t
-                height[t] = max(height[t], height[c] + 1)
+        klen = np.fromiter((len(k) for k in kids), np.int64, nn)
+        if klen.sum():
+            kcat = np.concatenate([np.asarray(k, np.int64) for k in kids if len(k)])
+            parent[kcat] = np.repeat(np.arange(nn), klen)
+            # post-order ids (children < parent): heights level by level
+            lev = np.flatnonzero(klen == 0)
+            while len(lev):
+                par = parent[lev]
+                ok = par >= 0
+                np.maximum.at(height, par[ok], height[lev[ok]] + 1)
+                lev = np.unique(par[ok])
         # boundaries (post-order: subtree of t has ids < t, ancestors > t)
         B_list = boundaries(G.g_ptr, G.g_col, nv, P_list, kids)
         pn = np.array([len(P) for P in P_list], np.int64) * m
@@ -595,7 +624,6 @@ class Multifrontal:
         fstride = pp + bp
         cpad = pp.copy()          # pivot padding of a child's stored Schur complement
         ckey = height.copy()      # fronts[] key of a child's stored Schur complement
-        perms = [None] * nn
         # extend-add on the device (xdg_mf_extend_add) or, XDG_MF_EXTEND=torch
         # / host plans, by per-child indexed adds (bit-identical)
         ext_kernel = (ctx is not None and torch.device(dev).type == "cuda"
@@ -612,9 +640,10 @@ class Multifrontal:
             for ts in pass_buckets.values():
                 in_pass[ts] = True
             last_use = np.full(H, -1, np.int64)
-            for t in np.flatnonzero(in_pass):
-                if parent[t] >= 0 and in_pass[parent[t]]:
-                    last_use[height[t]] = max(last_use[height[t]], height[parent[t]])
+            tp = np.flatnonzero(in_pass & (parent >= 0))
+            tp = tp[in_pass[parent[tp]]]
+            if len(tp):
+                np.maximum.at(last_use, height[tp], height[parent[tp]])
             for h in range(H):
                 hb = [(k, ts) for k, ts in pass_buckets.items() if k[0] == h]
                 if not hb:
@@ -631,10 +660,11 @@ class Multifrontal:
                 # identity on the pivot padding
                 pad_idx = []
                 for (_, P_, B_), ts in hb:
-                    for t in ts:
-                        if pn[t] < P_:
-                            i = np.arange(pn[t], P_)
-                            pad_idx.append(fbase[t] + i * (P_ + B_) + i)
+                    ts_ = np.asarray(ts, np.int64)
+                    ts_ = ts_[pn[ts_] < P_]
+                    if len(ts_):
+                        i = _ranges(pn[ts_], np.full(len(ts_), P_, np.int64))
+                        pad_idx.append(np.repeat(fbase[ts_], P_ - pn[ts_]) + i * (P_ + B_ + 1))
                 if pad_idx:
                     flat[torch.from_numpy(np.concatenate(pad_idx)).to(dev)] = 1.0
                 # original entries whose earlier-eliminated end is a front of h
@@ -759,10 +789,15 @@ class Multifrontal:
                 t = allts[int(np.flatnonzero(flags)[0])]
                 blk = tuple(int(b) for b in G.gblk[P_list[t][:8]])
                 raise SingularSystemError(f"{what} is singular (front on blocks {blk}...)")
+        # pivot permutations of all fronts, laid out front after front in id
+        # order (front t at pu_off[t]: position i <- front unknown pu_all[..+i])
+        pu_off = np.concatenate([[0], np.cumsum(pn)])
+        pu_all = np.zeros(int(pu_off[-1]), np.int64)
         for ts, perm in dev_perms:
-            ph = perm.cpu().numpy()
-            for q, t in enumerate(ts):
-                perms[t] = ph[q, :pn[t]].astype(np.int64)
+            ph = perm.cpu().numpy().astype(np.int64)
+            ts_ = np.asarray(ts, np.int64)
+            keep = np.arange(ph.shape[1])[None, :] < pn[ts_][:, None]
+            pu_all[(pu_off[ts_][:, None] + np.arange(ph.shape[1])[None, :])[keep]] = ph[keep]
         fronts.clear()
         t2 = time.perf_counter()
 
@@ -801,8 +836,8 @@ class Multifrontal:
         # permuted pivot unknowns of every needed front, fronts in id order:
         # position i of front t holds front unknown perms[t][i]
         ids = np.flatnonzero(need)
-        pu_glob = (np.concatenate([perms[t] for t in ids]) if len(ids)
-                   else np.zeros(0, np.int64)) + np.repeat(Pptr[ids] * m, pn[ids])
+        pu_glob = (pu_all[_ranges(pu_off[ids], pu_off[ids] + pn[ids])]
+                   + np.repeat(Pptr[ids] * m, pn[ids]))
         loc = _ranges(np.zeros(len(ids), np.int64), pn[ids])  # i within the front
         inv_perm_all = np.zeros(int(Pptr[-1]) * m, np.int64)  # front unknown -> position
         inv_perm_all[pu_glob] = loc
@@ -836,8 +871,8 @@ class Multifrontal:
         ent_cptr = np.zeros(len(ent_w) + 1, np.int64)
         np.cumsum(np.bincount(c_tgt, minlength=len(ent_w)), out=ent_cptr[1:])
         # warp tasks, level-sorted: (node, first row), 32/G rows each
-        gp = np.array([_group(int(x)) for x in pn], np.int64)
-        gb = np.array([_group(int(x)) if x else g for x, g in zip(bn, gp)], np.int64)
+        gp = _group_v(pn)
+        gb = np.where(bn > 0, _group_v(bn), gp)
         if merged:  # a backward row = U^-1 row (<= p long) + N_PB row (b long)
             gb = np.maximum(gp, gb)
 
