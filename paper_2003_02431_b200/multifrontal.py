@@ -495,8 +495,8 @@ class Multifrontal:
         self.height = height
         H = int(height.max()) + 1 if nn else 0
         self.nlevels = H
-        pp = np.array([_pad(int(x)) for x in pn], np.int64)
-        bp = np.array([_pad(int(x)) if x else 0 for x in bn], np.int64)
+        pp = np.where(pn <= 32, pn, (pn + 31) // 32 * 32)  # _pad
+        bp = np.where(bn <= 32, bn, (bn + 31) // 32 * 32)
         # multi-GPU (comm with world > 1): subtree-to-rank proportional
         # mapping; a rank factors and solves its owned subtrees plus the
         # shared top fronts (replicated), see proportional_map
@@ -548,10 +548,20 @@ class Multifrontal:
         buckets = {}  # (h, pp, bp) -> node list: fronts of the first pass
         buckets_sh = {}  # the shared (replicated) top fronts: second pass
         shared = self.rank_of < 0
-        for t in order:
-            if need[t]:
-                (buckets_sh if shared[t] else buckets).setdefault(
-                    (int(height[t]), int(pp[t]), int(bp[t])), []).append(int(t))
+        for sel_, bk_ in ((need & ~shared, buckets), (need & shared, buckets_sh)):
+            ts_all = order[sel_[order]]
+            if not len(ts_all):
+                continue
+            K = int(max(pp.max(), bp.max())) + 1
+            keys = (height[ts_all] * K + pp[ts_all]) * K + bp[ts_all]
+            _, first, inv = np.unique(keys, return_index=True, return_inverse=True)
+            rank = np.empty(len(first), np.int64)  # buckets in order of first appearance
+            rank[np.argsort(first, kind="stable")] = np.arange(len(first))
+            so_ = np.argsort(rank[inv], kind="stable")
+            cuts = np.flatnonzero(np.diff(rank[inv][so_])) + 1
+            for grp in np.split(ts_all[so_], cuts):
+                t0_ = int(grp[0])
+                bk_[(int(height[t0_]), int(pp[t0_]), int(bp[t0_]))] = grp.tolist()
         inv_off = np.zeros(nn, np.int64)
         lbp_off = np.zeros(nn, np.int64)
         upb_off = np.zeros(nn, np.int64)
@@ -757,7 +767,7 @@ class Multifrontal:
                             ft[:, :, P_:P_ + B_].copy_(out_m.transpose(1, 2))
                     bad_nodes.append((ts, bad))
                     dev_perms.append((ts, perm))  # read back once, after all heights
-                    for q, t in enumerate(ts):  # Schur complements other ranks need
+                    for q, t in enumerate(ts if xpos else ()):  # Schur complements other ranks need
                         if t in xpos:
                             b_ = int(bn[t])
                             xsend[int(t)] = Fb[q, P_:P_ + b_, P_:P_ + b_].reshape(-1).clone()
