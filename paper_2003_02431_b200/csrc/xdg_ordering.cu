@@ -17,6 +17,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <thread>
 #include <vector>
 
 #include "xdg_common.cuh"
@@ -27,8 +28,10 @@ struct ND {
   const int64_t* ptr;
   const int64_t* col;
   int64_t leaf;
-  std::vector<char> active;
-  std::vector<int64_t> dist;
+  // per-vertex scratch shared by the workers of xdg_nd_order: a worker only
+  // touches the vertices of its own connected components
+  char* active;
+  int64_t* dist;
   std::vector<int64_t> node_ptr{0};
   std::vector<int64_t> node_verts;
   std::vector<int64_t> parent;
@@ -174,33 +177,71 @@ extern "C" int64_t xdg_nd_order(int64_t nv, const int64_t* ptr, const int64_t* c
     node_ptr[0] = 0;
     return 0;
   }
-  ND nd;
-  nd.ptr = ptr;
-  nd.col = col;
-  nd.leaf = leaf < 1 ? 1 : leaf;
-  nd.active.assign(nv, 0);
-  nd.dist.assign(nv, -1);
+  std::vector<char> active(nv, 0);
+  std::vector<int64_t> dist(nv, -1);
   // connected components in order of their lowest vertex
-  std::vector<int64_t> comp(nv, -1), queue;
+  std::vector<int64_t> comp(nv, -1), cverts, cptr{0};
+  cverts.reserve(nv);
   for (int64_t s = 0; s < nv; ++s) {
     if (comp[s] >= 0) continue;
-    queue.assign(1, s);
+    const size_t q0 = cverts.size();
+    cverts.push_back(s);
     comp[s] = s;
-    for (size_t i = 0; i < queue.size(); ++i) {
-      const int64_t v = queue[i];
+    for (size_t i = q0; i < cverts.size(); ++i) {
+      const int64_t v = cverts[i];
       for (int64_t k = ptr[v]; k < ptr[v + 1]; ++k)
         if (comp[col[k]] < 0) {
           comp[col[k]] = s;
-          queue.push_back(col[k]);
+          cverts.push_back(col[k]);
         }
     }
-    std::sort(queue.begin(), queue.end());
-    nd.run(queue);
+    std::sort(cverts.begin() + q0, cverts.end());
+    cptr.push_back((int64_t)cverts.size());
   }
-  const int64_t nn = (int64_t)nd.parent.size();
-  std::copy(nd.node_ptr.begin(), nd.node_ptr.end(), node_ptr);
-  std::copy(nd.node_verts.begin(), nd.node_verts.end(), node_verts);
-  std::copy(nd.parent.begin(), nd.parent.end(), parent);
+  // the components are independent (the Schwarz blocks' systems: thousands
+  // of them): contiguous chunks of components per worker thread, results
+  // appended in component order -- the same forest as one thread builds
+  const int64_t nc = (int64_t)cptr.size() - 1;
+  int64_t nthreads = (int64_t)std::thread::hardware_concurrency();
+  nthreads = std::max<int64_t>(1, std::min<int64_t>({nthreads, 32, nc / 8}));
+  std::vector<ND> nds(nthreads);
+  std::vector<int64_t> cut(nthreads + 1, nc);
+  cut[0] = 0;
+  for (int64_t t = 1; t < nthreads; ++t) {  // chunks of about equal vertex counts
+    const int64_t want = nv * t / nthreads;
+    cut[t] = std::lower_bound(cptr.begin(), cptr.end(), want) - cptr.begin();
+    cut[t] = std::min(std::max(cut[t], cut[t - 1]), nc);
+  }
+  auto work = [&](int64_t t) {
+    ND& nd = nds[t];
+    nd.ptr = ptr;
+    nd.col = col;
+    nd.leaf = leaf < 1 ? 1 : leaf;
+    nd.active = active.data();
+    nd.dist = dist.data();
+    for (int64_t c = cut[t]; c < cut[t + 1]; ++c)
+      nd.run(std::vector<int64_t>(cverts.begin() + cptr[c], cverts.begin() + cptr[c + 1]));
+  };
+  if (nthreads == 1) {
+    work(0);
+  } else {
+    std::vector<std::thread> pool;
+    for (int64_t t = 0; t < nthreads; ++t) pool.emplace_back(work, t);
+    for (auto& th : pool) th.join();
+  }
+  int64_t nn = 0, nvert = 0;
+  node_ptr[0] = 0;
+  for (int64_t t = 0; t < nthreads; ++t) {
+    const ND& nd = nds[t];
+    const int64_t k = (int64_t)nd.parent.size();
+    for (int64_t i = 0; i < k; ++i) {
+      node_ptr[nn + i + 1] = nvert + nd.node_ptr[i + 1];
+      parent[nn + i] = nd.parent[i] < 0 ? -1 : nd.parent[i] + nn;
+    }
+    std::copy(nd.node_verts.begin(), nd.node_verts.end(), node_verts + nvert);
+    nn += k;
+    nvert += (int64_t)nd.node_verts.size();
+  }
   return nn;
 }
 

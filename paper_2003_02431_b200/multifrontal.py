@@ -293,6 +293,17 @@ class _ND:
         return np.bincount(owner, weights=hit, minlength=len(verts)) > 0
 
 
+def _parent_of(kids) -> np.ndarray:
+    """parent[c] of every front from the children lists (-1: root)."""
+    nn = len(kids)
+    parent = np.full(nn, -1, np.int64)
+    klen = np.fromiter((len(k) for k in kids), np.int64, nn)
+    if klen.sum():
+        kcat = np.fromiter((c for k in kids for c in k), np.int64, int(klen.sum()))
+        parent[kcat] = np.repeat(np.arange(nn), klen)
+    return parent
+
+
 def nested_dissection(g_ptr, g_col, nv, leaf):
     """Post-ordered elimination forest (P list, children list): the native
     xdg_nd_order (csrc/xdg_ordering.cu); nested_dissection_py is the same
@@ -323,8 +334,7 @@ def boundaries(g_ptr, g_col, nv, P, kids):
     np.cumsum([len(p) for p in P], out=node_ptr[1:])
     verts = np.ascontiguousarray(np.concatenate(P) if nn else np.zeros(0, np.int64), np.int64)
     parent = np.full(max(nn, 1), -1, np.int64)
-    for t, ks in enumerate(kids):
-        parent[ks] = t
+    parent[:nn] = _parent_of(kids)
     lib = nat.load()
     tot = int(lib.xdg_nd_boundaries(int(nv), g_ptr.ctypes.data, g_col.ctypes.data, nn,
                                     node_ptr.ctypes.data, verts.ctypes.data,
@@ -478,8 +488,7 @@ class Multifrontal:
         height = np.zeros(nn, np.int64)
         klen = np.fromiter((len(k) for k in kids), np.int64, nn)
         if klen.sum():
-            kcat = np.concatenate([np.asarray(k, np.int64) for k in kids if len(k)])
-            parent[kcat] = np.repeat(np.arange(nn), klen)
+            parent = _parent_of(kids)
             # post-order ids (children < parent): heights level by level
             lev = np.flatnonzero(klen == 0)
             while len(lev):

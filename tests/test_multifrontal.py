@@ -157,6 +157,23 @@ def test_native_ordering_matches_numpy_restatement(shape, leaf, seed):
     assert all(np.array_equal(a, b) for a, b in zip(B, Bp))
 
 
+def test_native_ordering_many_components_threaded():
+    """Hundreds of independent systems (Schwarz blocks): xdg_nd_order works on
+    chunks of connected components in worker threads; the forest equals the
+    numpy restatement's (one thread, component by component)."""
+    from paper_2003_02431_b200.multifrontal import nested_dissection_py
+
+    rp, col, _ = grid_bsr((24, 24), 1, seed=4)
+    idx = np.arange(24 * 24).reshape(24, 24)
+    sets = [np.sort(idx[max(i - 1, 0):i + 5, max(j - 1, 0):j + 5].ravel())
+            for i in range(0, 24, 4) for j in range(0, 24, 4)] * 4  # 144 overlapping boxes
+    G = SystemGraph(rp, col, sets)
+    P, kids = nested_dissection(G.g_ptr, G.g_col, G.nv, 6)
+    Pp, kp = nested_dissection_py(G.g_ptr, G.g_col, G.nv, 6)
+    assert len(P) == len(Pp) and kids == kp
+    assert all(np.array_equal(a, b) for a, b in zip(P, Pp))
+
+
 def test_proportional_map_subtrees_and_shared_tops():
     """Subtree-to-rank mapping (multi-GPU factor): every front mapped;
     owned subtrees closed under children; a shared front has only shared or
