@@ -293,6 +293,23 @@ class _ND:
         return np.bincount(owner, weights=hit, minlength=len(verts)) > 0
 
 
+class _Ragged(list):
+    """List of index arrays that are slices of one flat array (`flat`,
+    `ptr`): the fronts / boundary sets as the native ordering returns them.
+    `_flat` gives the concatenation back without touching the slices."""
+    flat = None
+    ptr = None
+
+
+def _flat(L):
+    """(concatenation, lengths) of a list of index arrays."""
+    if isinstance(L, _Ragged) and L.flat is not None:
+        return L.flat, np.diff(L.ptr)
+    n = len(L)
+    lens = np.fromiter((len(a) for a in L), np.int64, n)
+    return (np.concatenate(L) if n else np.zeros(0, np.int64)), lens
+
+
 def _parent_of(kids) -> np.ndarray:
     """parent[c] of every front from the children lists (-1: root)."""
     nn = len(kids)
@@ -316,7 +333,8 @@ def nested_dissection(g_ptr, g_col, nv, leaf):
     nn = int(nat.load().xdg_nd_order(int(nv), g_ptr.ctypes.data, g_col.ctypes.data,
                                       int(leaf), node_ptr.ctypes.data, verts.ctypes.data,
                                       parent.ctypes.data))
-    P = [verts[node_ptr[t]:node_ptr[t + 1]] for t in range(nn)]
+    P = _Ragged(verts[node_ptr[t]:node_ptr[t + 1]] for t in range(nn))
+    P.flat, P.ptr = verts[:node_ptr[nn]], node_ptr[:nn + 1]
     kids = [[] for _ in range(nn)]
     for c in range(nn):
         if parent[c] >= 0:
@@ -330,9 +348,10 @@ def boundaries(g_ptr, g_col, nv, P, kids):
     nn = len(P)
     g_ptr = np.ascontiguousarray(g_ptr, np.int64)
     g_col = np.ascontiguousarray(g_col, np.int64)
+    pcat, plen = _flat(P)
     node_ptr = np.zeros(nn + 1, np.int64)
-    np.cumsum([len(p) for p in P], out=node_ptr[1:])
-    verts = np.ascontiguousarray(np.concatenate(P) if nn else np.zeros(0, np.int64), np.int64)
+    np.cumsum(plen, out=node_ptr[1:])
+    verts = np.ascontiguousarray(pcat, np.int64)
     parent = np.full(max(nn, 1), -1, np.int64)
     parent[:nn] = _parent_of(kids)
     lib = nat.load()
@@ -342,7 +361,9 @@ def boundaries(g_ptr, g_col, nv, P, kids):
     b_ptr = np.zeros(nn + 1, np.int64)
     b_verts = np.zeros(max(tot, 1), np.int64)
     lib.xdg_nd_boundaries_copy(b_ptr.ctypes.data, b_verts.ctypes.data)
-    return [b_verts[b_ptr[t]:b_ptr[t + 1]] for t in range(nn)]
+    B = _Ragged(b_verts[b_ptr[t]:b_ptr[t + 1]] for t in range(nn))
+    B.flat, B.ptr = b_verts[:b_ptr[nn]], b_ptr
+    return B
 
 
 def boundaries_py(g_ptr, g_col, P, kids, owner):
@@ -480,8 +501,7 @@ class Multifrontal:
         P_list, kids = nested_dissection(G.g_ptr, G.g_col, nv, max(1, leaf_unknowns // m))
         nn = len(P_list)
         self.nnodes = nn
-        Plen0 = np.fromiter((len(P) for P in P_list), np.int64, nn)
-        Pcat0 = np.concatenate(P_list) if nn else np.zeros(0, np.int64)
+        Pcat0, Plen0 = _flat(P_list)
         owner = np.empty(nv, np.int64)
         owner[Pcat0] = np.repeat(np.arange(nn), Plen0)
         parent = np.full(nn, -1, np.int64)
@@ -498,8 +518,9 @@ class Multifrontal:
                 lev = np.unique(par[ok])
         # boundaries (post-order: subtree of t has ids < t, ancestors > t)
         B_list = boundaries(G.g_ptr, G.g_col, nv, P_list, kids)
-        pn = np.array([len(P) for P in P_list], np.int64) * m
-        bn = np.array([len(B) for B in B_list], np.int64) * m
+        Bcat0, Blen0 = _flat(B_list)
+        pn = Plen0 * m
+        bn = Blen0 * m
         self.P_list, self.B_list, self.kids, self.parent = P_list, B_list, kids, parent
         self.height = height
         H = int(height.max()) + 1 if nn else 0
@@ -530,11 +551,10 @@ class Multifrontal:
         # position of every vertex inside its owner's P; B positions by key
         ppos = np.empty(nv, np.int64)
         ppos[Pcat0] = _ranges(np.zeros(nn, np.int64), Plen0)
-        bkey_node = np.repeat(np.arange(nn), [len(B) for B in B_list])
-        bkey_v = np.concatenate(B_list) if nn else np.zeros(0, np.int64)
+        bkey_node = np.repeat(np.arange(nn), Blen0)
+        bkey_v = Bcat0
         bkey = bkey_node * max(nv, 1) + bkey_v
-        bkey_pos = _ranges(np.zeros(nn, np.int64),
-                           np.fromiter((len(B) for B in B_list), np.int64, nn)) if nn else bkey
+        bkey_pos = _ranges(np.zeros(nn, np.int64), Blen0) if nn else bkey
         so = np.argsort(bkey, kind="stable")
         bkey, bkey_pos = bkey[so], bkey_pos[so]
 
@@ -705,9 +725,9 @@ class Multifrontal:
                     flat[torch.from_numpy(tgt.reshape(-1)).to(dev)] = blocks.reshape(-1)
                 # children's Schur complements (extend-add), child by child
                 if ext_kernel:
-                    self._extend_add(ctx, hb, kids, bn, cpad, fbase, fstride, ckey, fronts,
+                    self._extend_add(ctx, hb, parent, bn, cpad, fbase, fstride, ckey, fronts,
                                      flat, B_list, front_pos, m)
-                for t in (t for (_, _, _), ts in hb for t in ts if not ext_kernel):
+                for t in (() if ext_kernel else (t for (_, _, _), ts in hb for t in ts)):
                     if not kids[t]:
                         continue
                     Ft = flat[fbase[t]:fbase[t] + fstride[t] ** 2].view(fstride[t], fstride[t])
@@ -830,11 +850,9 @@ class Multifrontal:
         classes = [need & ~shared, need & shared]
         # (vectorised over all fronts: a Schwarz plan of 337 systems has
         # ~27,000 of them, and per-front numpy calls cost 1 s of its setup)
-        Plen = np.array([len(P) for P in P_list], np.int64)
-        Blen = np.array([len(B) for B in B_list], np.int64)
+        Plen, Blen, Pcat = Plen0, Blen0, Pcat0
         Pptr = np.concatenate([[0], np.cumsum(Plen)])
         Bptr = np.concatenate([[0], np.cumsum(Blen)])
-        Pcat = np.concatenate(P_list) if nn else np.zeros(0, np.int64)
         Bcat = bkey_v
         node_of_P = np.repeat(np.arange(nn), Plen)
         node_of_B = bkey_node
@@ -1049,26 +1067,35 @@ class Multifrontal:
 
     # ------------------------------------------------------------------
     @staticmethod
-    def _extend_add(ctx, hb, kids, bn, pp, fbase, fstride, height, fronts, flat, B_list,
+    def _extend_add(ctx, hb, parent, bn, pp, fbase, fstride, height, fronts, flat, B_list,
                     front_pos, m):
         """Device extend-add of one height (xdg_mf_extend_add): round r adds
-        the r-th child (kids order, bn > 0) of every parent, one launch per
-        (round, child height)."""
-        groups = {}
-        for t in (t for (_, _, _), ts in hb for t in ts):
-            r = 0
-            for c in kids[t]:
-                if bn[c] == 0:
-                    continue
-                groups.setdefault((r, int(height[c])), []).append((t, c))
-                r += 1
+        the r-th child (ascending id = kids order, bn > 0) of every parent, one
+        launch per (round, child height).  Array operations over all the
+        (parent, child) pairs of the height."""
+        nn = len(parent)
+        in_h = np.zeros(nn, bool)
+        for (_, _, _), ts in hb:
+            in_h[ts] = True
+        cc_all = np.flatnonzero((parent >= 0) & (bn > 0))
+        cc_all = cc_all[in_h[parent[cc_all]]]
+        if not len(cc_all):
+            return
+        so = np.argsort(parent[cc_all], kind="stable")  # children ascending per parent
+        cc_all = cc_all[so]
+        tt_all = parent[cc_all]
+        first = np.concatenate([[True], tt_all[1:] != tt_all[:-1]])
+        start = np.maximum.accumulate(np.where(first, np.arange(len(tt_all)), 0))
+        rnd = np.arange(len(tt_all)) - start
+        Bflat, Blen = _flat(B_list)
+        Bptr = np.concatenate([[0], np.cumsum(Blen)])
+        key = rnd * (int(height.max()) + 2) + (height[cc_all] + 1)  # ckey may be -1
         dev = flat.device
-        for key in sorted(groups):
-            prs = groups[key]
-            tt = np.array([t for t, _ in prs], np.int64)
-            cc = np.array([c for _, c in prs], np.int64)
-            nodes_ = np.repeat(tt, [len(B_list[c]) for c in cc])
-            verts = np.concatenate([B_list[c] for c in cc])
+        for k in np.unique(key):
+            selk = key == k
+            tt, cc = tt_all[selk], cc_all[selk]
+            nodes_ = np.repeat(tt, Blen[cc])
+            verts = Bflat[_ranges(Bptr[cc], Bptr[cc + 1])]
             U = (front_pos(nodes_, verts)[:, None] + np.arange(m)[None, :]).reshape(-1)
             n = bn[cc].astype(np.int64)
             uoff = np.concatenate([[0], np.cumsum(n)[:-1]])
@@ -1076,8 +1103,8 @@ class Multifrontal:
                             1).astype(np.int64)
             pair_d = torch.from_numpy(np.ascontiguousarray(pair)).to(dev)
             U_d = torch.from_numpy(np.ascontiguousarray(U, np.int64)).to(dev)
-            child = fronts[key[1]]
-            nat.check(ctx.lib.xdg_mf_extend_add(len(prs), pair_d.data_ptr(), U_d.data_ptr(),
+            child = fronts[int(height[cc[0]])]
+            nat.check(ctx.lib.xdg_mf_extend_add(len(tt), pair_d.data_ptr(), U_d.data_ptr(),
                                                 child.data_ptr(), flat.data_ptr(),
                                                 int(n.max()), ctx.stream), "mf_extend_add")
 
