@@ -712,17 +712,21 @@ class Multifrontal:
                     nd_ = a_node[sel]
                     rpos = front_pos(nd_, G.a_row[sel])
                     cpos = front_pos(nd_, G.a_col[sel])
-                    st = fstride[nd_]
-                    am = np.arange(m)
-                    tgt = (fbase[nd_][:, None, None]
-                           + (rpos[:, None, None] + am[None, :, None]) * st[:, None, None]
-                           + cpos[:, None, None] + am[None, None, :])
-                    ks = torch.from_numpy(G.a_k[sel]).to(dev)
-                    blocks = vblk[ks][:, :m, :m].transpose(1, 2)
-                    sr = scale.view(nv, m)[torch.from_numpy(G.a_row[sel]).to(dev)]
-                    scl = scale.view(nv, m)[torch.from_numpy(G.a_col[sel]).to(dev)]
+                    # one upload of the per-entry scalars; the m x m target
+                    # indices are expanded on the device (on the host they were
+                    # nnzb m^2 int64 words: 1.5 GB built and copied at cfg4 size)
+                    ent = torch.from_numpy(np.stack(
+                        [fbase[nd_] + rpos * fstride[nd_] + cpos, fstride[nd_], G.a_k[sel],
+                         G.a_row[sel], G.a_col[sel]])).to(dev)
+                    am_d = torch.arange(m, device=dev)
+                    tgt = (ent[0][:, None, None] + am_d[None, :, None] * ent[1][:, None, None]
+                           + am_d[None, None, :])
+                    blocks = vblk[ent[2]][:, :m, :m].transpose(1, 2)
+                    sr = scale.view(nv, m)[ent[3]]
+                    scl = scale.view(nv, m)[ent[4]]
                     blocks = blocks * sr[:, :, None] * scl[:, None, :]
-                    flat[torch.from_numpy(tgt.reshape(-1)).to(dev)] = blocks.reshape(-1)
+                    flat[tgt.reshape(-1)] = blocks.reshape(-1)
+                    del ent, tgt, blocks, sr, scl
                 # children's Schur complements (extend-add), child by child
                 if ext_kernel:
                     self._extend_add(ctx, hb, parent, bn, cpad, fbase, fstride, ckey, fronts,
