@@ -301,6 +301,12 @@ class _Ragged(list):
     ptr = None
 
 
+class _Kids(list):
+    """Children lists of the fronts with the parent array they were built
+    from (`_parent_of` returns it without walking the lists)."""
+    parent = None
+
+
 def _flat(L):
     """(concatenation, lengths) of a list of index arrays."""
     if isinstance(L, _Ragged) and L.flat is not None:
@@ -313,6 +319,8 @@ def _flat(L):
 def _parent_of(kids) -> np.ndarray:
     """parent[c] of every front from the children lists (-1: root)."""
     nn = len(kids)
+    if isinstance(kids, _Kids) and kids.parent is not None:
+        return kids.parent
     parent = np.full(nn, -1, np.int64)
     klen = np.fromiter((len(k) for k in kids), np.int64, nn)
     if klen.sum():
@@ -335,10 +343,11 @@ def nested_dissection(g_ptr, g_col, nv, leaf):
                                       parent.ctypes.data))
     P = _Ragged(verts[node_ptr[t]:node_ptr[t + 1]] for t in range(nn))
     P.flat, P.ptr = verts[:node_ptr[nn]], node_ptr[:nn + 1]
-    kids = [[] for _ in range(nn)]
-    for c in range(nn):
-        if parent[c] >= 0:
-            kids[parent[c]].append(c)
+    kids = _Kids([] for _ in range(nn))
+    par = parent[:nn]
+    for c in np.flatnonzero(par >= 0).tolist():
+        kids[par[c]].append(c)
+    kids.parent = par.copy()
     return P, kids
 
 
@@ -506,9 +515,9 @@ class Multifrontal:
         owner[Pcat0] = np.repeat(np.arange(nn), Plen0)
         parent = np.full(nn, -1, np.int64)
         height = np.zeros(nn, np.int64)
-        klen = np.fromiter((len(k) for k in kids), np.int64, nn)
-        if klen.sum():
-            parent = _parent_of(kids)
+        if nn:
+            parent = np.array(_parent_of(kids), np.int64)
+            klen = np.bincount(parent[parent >= 0], minlength=nn)
             # post-order ids (children < parent): heights level by level
             lev = np.flatnonzero(klen == 0)
             while len(lev):
