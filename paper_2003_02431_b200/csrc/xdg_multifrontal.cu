@@ -78,7 +78,13 @@ cudaError_t launch_chain(void (*kernel)(KArgs...), int grid, cudaStream_t s, Arg
 #define MF_U 8  // loads in flight per lane per chunk
 #endif
 #ifndef MF_MINB
-#define MF_MINB 3  // resident CTAs per SM the row kernels are compiled for
+// resident CTAs per SM the row kernels are compiled for.  Measured with the
+// PDL chain (cfg2 low-order solve, profiles/r2_mf_variants*.txt; MINB x rows
+// per warp task x loads in flight): 3 x 2 x 8 2.42 ms, 2 x 3 x 8 2.23 ms,
+// 2 x 4 x 8 2.34, 2 x 4 x 12 2.32, 2 x 3 x 6/10/12 2.31-2.32, 3 x 3 x 8 2.47,
+// 4 x 2 x 8 3.38 (spills): three rows share each vector load and 128
+// registers keep 24 factor loads per lane in flight.
+#define MF_MINB 2
 #endif
 
 template <typename V>
@@ -161,7 +167,7 @@ __device__ __forceinline__ void group_dot2(const double* __restrict__ ra,
 // [lo, hi); loads are clamped to hi - 1 (inside the padded rows) and masked.
 // Used for fronts whose rows get a whole warp (G = 32).
 #ifndef MF_MR
-#define MF_MR 2
+#define MF_MR 3
 #endif
 #ifndef MF_MU
 #define MF_MU 8

@@ -1009,7 +1009,12 @@ class Multifrontal:
         LONG = _long_row()
         import os as _os
         WAVES = float(_os.environ.get("XDG_MF_CTA_WAVES", "2.0"))
-        RESIDENT_WARPS = 148 * 24  # B200: 148 SMs x 3 CTAs x 8 warps (80 registers)
+        # group tasks where a launch has fewer than WAVES x 3,552 warp tasks (a
+        # measured threshold: 1 / 2 / 3 x 2,368 -> 2.33 / 2.23 / 2.23 ms with the
+        # current row kernels, profiles/r2_mf_mr3_waves.txt; kept at its
+        # round-1 value 2 x 148 x 24 so the task split -- and with it the
+        # summation order of the long rows -- does not follow kernel retuning)
+        RESIDENT_WARPS = 148 * 24
         all_tasks, lev_task_k = [], []
         base = 0
         for cls in classes:
