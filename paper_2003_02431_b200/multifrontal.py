@@ -1008,12 +1008,13 @@ class Multifrontal:
         SETS = _row_sets()
         LONG = _long_row()
         import os as _os
-        WAVES = float(_os.environ.get("XDG_MF_CTA_WAVES", "2.0"))
+        WAVES = float(_os.environ.get("XDG_MF_CTA_WAVES", "3.0"))
         # group tasks where a launch has fewer than WAVES x 3,552 warp tasks (a
-        # measured threshold: 1 / 2 / 3 x 2,368 -> 2.33 / 2.23 / 2.23 ms with the
-        # current row kernels, profiles/r2_mf_mr3_waves.txt; kept at its
-        # round-1 value 2 x 148 x 24 so the task split -- and with it the
-        # summation order of the long rows -- does not follow kernel retuning)
+        # measured threshold: 2,368 / 4,736 / 7,104 -> 2.33 / 2.23 / 2.23 ms with
+        # the current row kernels, profiles/r2_mf_mr3_waves.txt).  The split
+        # decides the summation order of the long rows, i.e. the roundoff: at
+        # cfg2 the GMRES count at the 1e-10 floor moved between 6,774 and 8,422
+        # over the settings of profiles/r2_gmres_cfg2_split_counts.txt
         RESIDENT_WARPS = 148 * 24
         all_tasks, lev_task_k = [], []
         base = 0
